@@ -1,0 +1,129 @@
+/* hankel_b200.h — C ABI of the B200-native extreme-precision Hankel LDLT path.
+ *
+ * The reference (/root/reference/proj, hankel-eig v0.1.0) is a C++ library with
+ * no C ABI, plugin registry or FFI of its own; its entry points
+ * are the C++ functions of proj/include/hankel/*.hpp.  This header is the thin
+ * C layer *below* those entry points: each call is annotated with the reference
+ * function it replaces.  Plain pointers and sizes only; no torch, no C++ types.
+ *
+ * Number format (host interchange, "SoA"): an array of `count` p-bit floats,
+ * p = 32 * limbs, is three caller-owned host arrays
+ *     uint32_t limbs[count * limbs]   little-endian mantissa words per value
+ *     int32_t  exps [count]           binary exponent e
+ *     int32_t  signs[count]           -1, 0 (value zero, limbs all 0) or +1
+ * with value = sign * M * 2^(e - p), 2^(p-1) <= M < 2^p.  Every arithmetic
+ * operation on the device is correctly rounded (round to nearest, ties to even).
+ *
+ * Status codes mirror the reference CLI's exit codes (proj/tools/hankel_cli.cpp:4,
+ * 135-147) and its exception mapping:
+ *     HK_OK 0, HK_ERR_RUNTIME 1 (CUDA/NCCL/internal   -> std::runtime_error)
+ *     HK_ERR_PRECISION 2 (non-positive pivot          -> hankel::precision_error;
+ *                         hk_bad_column() gives the column, ldlt.cpp:83-87)
+ *     HK_ERR_INVALID 3  (bad sizes / arguments        -> std::invalid_argument)
+ * hk_last_error() returns the message of the last failure on that context.
+ *
+ * Threading: one host thread per context; calls are synchronous on return and
+ * not re-entrant.  Each context owns one CUDA device and one stream.
+ */
+#ifndef HANKEL_B200_H
+#define HANKEL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HK_OK 0
+#define HK_ERR_RUNTIME 1
+#define HK_ERR_PRECISION 2
+#define HK_ERR_INVALID 3
+
+#define HK_OP_FMS 0   /* out = RNE(c - a*b)  — submul_rounded, fixedpoint.cpp:146-154 */
+#define HK_OP_MUL 1   /* out = RNE(a*b)      — operator*, fixedpoint.cpp:67-69 (exact there) */
+#define HK_OP_ADD 2   /* out = RNE(a+b)      — operator+, fixedpoint.cpp:55-59 (exact there) */
+#define HK_OP_RECIP 3 /* out = RNE(1/a)      — FixScalar::div's role, fixedpoint.cpp:71-84 */
+
+typedef struct hk_ctx hk_ctx;
+
+/* ABI version (major*100 + minor). */
+int hk_version(void);
+
+/* Context on CUDA device `device` computing at p = 32*limbs bits.
+ * Replaces the per-run precision choice `frac_bits` of MomentTable
+ * (moments.hpp:38) / ComputeOptions::bits (pipeline.hpp:19). */
+int hk_create(int device, int limbs, hk_ctx** out);
+void hk_destroy(hk_ctx* ctx);
+const char* hk_last_error(const hk_ctx* ctx);
+int hk_bad_column(const hk_ctx* ctx);
+int hk_limbs(const hk_ctx* ctx);
+
+/* Host-side exact moments mu_0..mu_{count-1} of w(x)=exp(-x^beta) as p-bit
+ * floats (moments.cpp:80-111: gamma_exact + moment, the factorial path; the
+ * half-integer sqrt(pi) path is not implemented -> HK_ERR_INVALID).
+ * *exact = 1 iff every moment was representable without rounding. No GPU. */
+int hk_moments(unsigned beta_num, unsigned beta_den, int count, int limbs, uint32_t* out_limbs,
+               int32_t* out_exps, int32_t* out_signs, int* exact);
+
+/* Upload the 2n-1 moments (H2D).  Replaces MomentTable / build_hankel
+ * (moments.hpp:36-58) as the input of the factorisation. */
+int hk_load_moments(hk_ctx* ctx, int n, const uint32_t* limbs, const int32_t* exps, const int32_t* signs);
+
+/* LDLT of H = (mu_{i+j}) on the device (S <- H, then n right-looking steps).
+ * Replaces decompose_serial / decompose_parallel (ldlt.hpp:90, 97-99).
+ * HK_ERR_PRECISION with hk_bad_column() on a non-positive pivot. */
+int hk_ldlt(hk_ctx* ctx);
+
+/* D_0..D_{n-1} (n values) and column `col` of L (n-col-1 values, rows col+1..n-1),
+ * LdltFactors::D / L (ldlt.hpp:76-85). */
+int hk_get_D(hk_ctx* ctx, uint32_t* limbs, int32_t* exps, int32_t* signs);
+int hk_get_L_column(hk_ctx* ctx, int col, uint32_t* limbs, int32_t* exps, int32_t* signs);
+
+/* First m columns of L^{-1}.  Replaces invert_L_partial_serial / _parallel
+ * (inversion.hpp:40, 45-46).  hk_get_Linv returns n*m values row-major; entry
+ * (r,c) is L^{-1}(r,c) for c < r, and 0 for c >= r (unit diagonal implicit). */
+int hk_invert_L_partial(hk_ctx* ctx, int m);
+int hk_get_Linv(hk_ctx* ctx, uint32_t* limbs, int32_t* exps, int32_t* signs);
+
+/* k x k leading block of H^{-1} = sum_l Linv(l,j) Linv(l,c) / D_l, k <= m.
+ * Replaces assemble_truncated_inverse (inversion.hpp:60) but keeps the block
+ * in MP (no binary64 cast, inversion.cpp:258).  hk_get_block: k*k row-major. */
+int hk_assemble_block(hk_ctx* ctx, int k);
+int hk_get_block(hk_ctx* ctx, uint32_t* limbs, int32_t* exps, int32_t* signs);
+
+/* s smallest eigenvalues of H from the last block: lambda_i = 1/mu_{k+1-i}
+ * and trunc_err_i vs the (k-1) block.  Replaces smallest_eigs_of_H
+ * (jacobi.hpp:29-30; jacobi.cpp:74-103).  Host cyclic Jacobi in binary128;
+ * lambda = lambda_hi + lambda_lo (double-double, ~32 digits). */
+int hk_smallest_eigs(hk_ctx* ctx, int s, double* lambda_hi, double* lambda_lo, double* trunc_err);
+
+/* Whole path, host buffers in, lambdas out: upload -> LDLT -> L^{-1} -> block
+ * -> eigen.  Replaces hankel::compute (pipeline.hpp:50; pipeline.cpp:26-72)
+ * with k clamped to n (pipeline.cpp:36) and s = min(3, k) (pipeline.cpp:64). */
+int hk_compute(hk_ctx* ctx, int n, const uint32_t* limbs, const int32_t* exps, const int32_t* signs, int k,
+               double* lambda_hi, double* lambda_lo, double* trunc_err, int* s_out);
+
+/* Stage times of the last calls, RunRecord taxonomy (pipeline.hpp:38-45), in
+ * seconds: [0] wall (hk_compute), [1] ldlt, [2] invL, [3] invH, [4] eigen,
+ * [5] h2d, [6] d2h.  Device stages are CUDA-event times on the ctx stream. */
+int hk_timings(const hk_ctx* ctx, double* out7);
+
+/* Kernel launches issued by the last hk_ldlt / invert / assemble calls. */
+long long hk_launch_count(const hk_ctx* ctx);
+
+/* Elementwise batch arithmetic on host SoA arrays (parity tests of the MP
+ * kernels).  op = HK_OP_*.  a, b, c are `count`-long arrays (b, c unused as the
+ * op requires; pass NULL). */
+int hk_mp_batch(hk_ctx* ctx, int op, long long count, const uint32_t* a_l, const int32_t* a_e, const int32_t* a_s,
+                const uint32_t* b_l, const int32_t* b_e, const int32_t* b_s, const uint32_t* c_l,
+                const int32_t* c_e, const int32_t* c_s, uint32_t* o_l, int32_t* o_e, int32_t* o_s);
+
+/* Balanced round-robin (boustrophedon) ownership map, assign_columns
+ * (ldlt.cpp:22-35): owner[c] for c < n. */
+int hk_assign_columns(int n, int workers, int32_t* owner);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HANKEL_B200_H */

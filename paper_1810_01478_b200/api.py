@@ -1,0 +1,283 @@
+"""ctypes binding of the C ABI (include/hankel_b200.h) — Python plumbing for the
+tests and bench.py.  The product is libhankel_b200.so (CUDA sm_100a + C++ host
+code); this module only marshals host arrays.  There is no CPU fallback: if the
+library is missing or no CUDA device is visible, calls raise.
+
+Mirrors the reference entry points (proj/include/hankel/*.hpp) by name:
+``build_hankel`` (moments), ``decompose`` (LDLT), ``invert_L_partial``,
+``assemble_truncated_inverse``, ``smallest_eigs_of_H`` and ``compute``.
+Errors map like the reference's exceptions: HK_ERR_PRECISION ->
+PrecisionError (hankel::precision_error), HK_ERR_INVALID -> ValueError
+(std::invalid_argument), HK_ERR_RUNTIME -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhankel_b200.so")
+
+HK_OK, HK_ERR_RUNTIME, HK_ERR_PRECISION, HK_ERR_INVALID = 0, 1, 2, 3
+OP_FMS, OP_MUL, OP_ADD, OP_RECIP = 0, 1, 2, 3
+
+
+class PrecisionError(RuntimeError):
+    """hankel::precision_error (proj/include/hankel/errors.hpp:10-13)."""
+
+
+_lib = None
+
+
+def lib():
+    """Load libhankel_b200.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `make` (or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        u32p, i32p, f64p = C.POINTER(C.c_uint32), C.POINTER(C.c_int32), C.POINTER(C.c_double)
+        vp = C.c_void_p
+        sig = {
+            "hk_version": (C.c_int, []),
+            "hk_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(vp)]),
+            "hk_destroy": (None, [vp]),
+            "hk_last_error": (C.c_char_p, [vp]),
+            "hk_bad_column": (C.c_int, [vp]),
+            "hk_limbs": (C.c_int, [vp]),
+            "hk_moments": (C.c_int, [C.c_uint, C.c_uint, C.c_int, C.c_int, u32p, i32p, i32p, C.POINTER(C.c_int)]),
+            "hk_load_moments": (C.c_int, [vp, C.c_int, u32p, i32p, i32p]),
+            "hk_ldlt": (C.c_int, [vp]),
+            "hk_get_D": (C.c_int, [vp, u32p, i32p, i32p]),
+            "hk_get_L_column": (C.c_int, [vp, C.c_int, u32p, i32p, i32p]),
+            "hk_invert_L_partial": (C.c_int, [vp, C.c_int]),
+            "hk_get_Linv": (C.c_int, [vp, u32p, i32p, i32p]),
+            "hk_assemble_block": (C.c_int, [vp, C.c_int]),
+            "hk_get_block": (C.c_int, [vp, u32p, i32p, i32p]),
+            "hk_smallest_eigs": (C.c_int, [vp, C.c_int, f64p, f64p, f64p]),
+            "hk_compute": (C.c_int, [vp, C.c_int, u32p, i32p, i32p, C.c_int, f64p, f64p, f64p, C.POINTER(C.c_int)]),
+            "hk_timings": (C.c_int, [vp, f64p]),
+            "hk_launch_count": (C.c_longlong, [vp]),
+            "hk_mp_batch": (C.c_int, [vp, C.c_int, C.c_longlong] + [u32p, i32p, i32p] * 4),
+            "hk_assign_columns": (C.c_int, [C.c_int, C.c_int, i32p]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _u32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def _i32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+@dataclass
+class MPArray:
+    """Host SoA array of p-bit floats (the ABI interchange format)."""
+
+    limbs: np.ndarray  # uint32 [count, L]
+    exps: np.ndarray  # int32 [count]
+    signs: np.ndarray  # int32 [count]
+
+    @staticmethod
+    def empty(count: int, L: int) -> "MPArray":
+        return MPArray(np.zeros((count, L), np.uint32), np.zeros(count, np.int32), np.zeros(count, np.int32))
+
+    @property
+    def L(self) -> int:
+        return self.limbs.shape[1]
+
+    def __len__(self):
+        return self.limbs.shape[0]
+
+    def entry(self, i: int):
+        """(sign, mantissa int, exp) of entry i."""
+        m = int.from_bytes(self.limbs[i].astype("<u4").tobytes(), "little")
+        return int(self.signs[i]), m, int(self.exps[i])
+
+    def set_entry(self, i: int, sign: int, m: int, e: int):
+        self.limbs[i] = np.frombuffer(m.to_bytes(4 * self.L, "little"), dtype="<u4")
+        self.exps[i] = e
+        self.signs[i] = sign
+
+    def to_fraction(self, i: int):
+        from fractions import Fraction
+
+        s, m, e = self.entry(i)
+        if s == 0:
+            return Fraction(0)
+        sh = e - 32 * self.L
+        v = Fraction(m << sh) if sh >= 0 else Fraction(m, 1 << (-sh))
+        return v if s > 0 else -v
+
+    def ptrs(self):
+        return _u32(self.limbs), _i32(self.exps), _i32(self.signs)
+
+
+def _check(rc: int, ctx=None):
+    if rc == HK_OK:
+        return
+    msg = lib().hk_last_error(ctx).decode() if ctx else f"status {rc}"
+    if rc == HK_ERR_PRECISION:
+        raise PrecisionError(msg)
+    if rc == HK_ERR_INVALID:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def build_hankel(beta: tuple[int, int], n: int, limbs: int) -> tuple[MPArray, bool]:
+    """The 2n-1 exact moments as p-bit floats (moments.cpp:102-133 / build_hankel)."""
+    out = MPArray.empty(2 * n - 1, limbs)
+    exact = C.c_int(0)
+    _check(lib().hk_moments(beta[0], beta[1], 2 * n - 1, limbs, *out.ptrs(), C.byref(exact)))
+    return out, bool(exact.value)
+
+
+def assign_columns(n: int, workers: int) -> list[int]:
+    o = np.zeros(n, np.int32)
+    rc = lib().hk_assign_columns(n, workers, _i32(o))
+    if rc != HK_OK:
+        raise ValueError("assign_columns: need n >= 1 and workers >= 1")
+    return o.tolist()
+
+
+@dataclass
+class RunRecord:
+    """pipeline.hpp:28-48 (numeric + timing fields)."""
+
+    n: int
+    k: int
+    lambda_: list = field(default_factory=list)  # ~32-digit values (hi + lo as Fraction-free float pairs)
+    lambda_hi: list = field(default_factory=list)
+    lambda_lo: list = field(default_factory=list)
+    trunc_err: list = field(default_factory=list)
+    wall_s: float = 0.0
+    ldlt_s: float = 0.0
+    invL_s: float = 0.0
+    invH_s: float = 0.0
+    eigen_s: float = 0.0
+    h2d_s: float = 0.0
+    d2h_s: float = 0.0
+
+
+class Context:
+    """One device context at p = 32*limbs bits (hk_create / hk_destroy)."""
+
+    def __init__(self, limbs: int, device: int = 0):
+        self.L = limbs
+        h = C.c_void_p()
+        rc = lib().hk_create(device, limbs, C.byref(h))
+        if rc != HK_OK:
+            raise RuntimeError(f"hk_create failed with status {rc} (CUDA device {device} unavailable?)")
+        self.h = h
+        self.n = 0
+
+    def close(self):
+        if self.h:
+            lib().hk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- stages
+    def load_moments(self, mu: MPArray):
+        n = (len(mu) + 1) // 2
+        _check(lib().hk_load_moments(self.h, n, *mu.ptrs()), self.h)
+        self.n = n
+
+    def decompose(self):
+        """decompose_parallel / decompose_serial (ldlt.hpp:90-99)."""
+        rc = lib().hk_ldlt(self.h)
+        if rc == HK_ERR_PRECISION:
+            self.bad_column = lib().hk_bad_column(self.h)
+        _check(rc, self.h)
+
+    def D(self) -> MPArray:
+        out = MPArray.empty(self.n, self.L)
+        _check(lib().hk_get_D(self.h, *out.ptrs()), self.h)
+        return out
+
+    def L_column(self, col: int) -> MPArray:
+        out = MPArray.empty(max(self.n - col - 1, 0), self.L)
+        if len(out) == 0:
+            _check(lib().hk_get_L_column(self.h, col, None, None, None), self.h)
+            return out
+        _check(lib().hk_get_L_column(self.h, col, *out.ptrs()), self.h)
+        return out
+
+    def invert_L_partial(self, m: int):
+        _check(lib().hk_invert_L_partial(self.h, m), self.h)
+        self.m = m
+
+    def Linv(self) -> MPArray:
+        out = MPArray.empty(self.n * self.m, self.L)
+        _check(lib().hk_get_Linv(self.h, *out.ptrs()), self.h)
+        return out
+
+    def assemble_truncated_inverse(self, k: int):
+        _check(lib().hk_assemble_block(self.h, k), self.h)
+        self.k = k
+
+    def block(self) -> MPArray:
+        out = MPArray.empty(self.k * self.k, self.L)
+        _check(lib().hk_get_block(self.h, *out.ptrs()), self.h)
+        return out
+
+    def smallest_eigs_of_H(self, s: int):
+        hi, lo, te = (np.zeros(s) for _ in range(3))
+        f64 = C.POINTER(C.c_double)
+        _check(lib().hk_smallest_eigs(self.h, s, hi.ctypes.data_as(f64), lo.ctypes.data_as(f64),
+                                      te.ctypes.data_as(f64)), self.h)
+        return hi.tolist(), lo.tolist(), te.tolist()
+
+    def compute(self, mu: MPArray, k: int) -> RunRecord:
+        """hankel::compute (pipeline.cpp:26-72) from host moments."""
+        n = (len(mu) + 1) // 2
+        hi, lo, te = (np.zeros(3) for _ in range(3))
+        s = C.c_int(0)
+        f64 = C.POINTER(C.c_double)
+        rc = lib().hk_compute(self.h, n, *mu.ptrs(), k, hi.ctypes.data_as(f64), lo.ctypes.data_as(f64),
+                              te.ctypes.data_as(f64), C.byref(s))
+        if rc == HK_ERR_PRECISION:
+            self.bad_column = lib().hk_bad_column(self.h)
+        _check(rc, self.h)
+        self.n, self.m, self.k = n, min(k, n), min(k, n)
+        t = self.timings()
+        ns = s.value
+        return RunRecord(n=n, k=min(k, n), lambda_hi=hi[:ns].tolist(), lambda_lo=lo[:ns].tolist(),
+                         trunc_err=te[:ns].tolist(), wall_s=t[0], ldlt_s=t[1], invL_s=t[2], invH_s=t[3],
+                         eigen_s=t[4], h2d_s=t[5], d2h_s=t[6])
+
+    def timings(self):
+        t = np.zeros(7)
+        lib().hk_timings(self.h, t.ctypes.data_as(C.POINTER(C.c_double)))
+        return t.tolist()
+
+    def launch_count(self) -> int:
+        return int(lib().hk_launch_count(self.h))
+
+    def mp_batch(self, op: int, a: MPArray, b: MPArray | None = None, c: MPArray | None = None) -> MPArray:
+        out = MPArray.empty(len(a), self.L)
+        nul = (None, None, None)
+        _check(lib().hk_mp_batch(self.h, op, len(a), *a.ptrs(), *(b.ptrs() if b is not None else nul),
+                                 *(c.ptrs() if c is not None else nul), *out.ptrs()), self.h)
+        return out

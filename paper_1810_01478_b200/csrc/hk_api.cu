@@ -1,0 +1,497 @@
+// hk_api.cu — sm_100a kernels and the C ABI (include/hankel_b200.h).
+//
+// Kernels are grid-stride loops of warp-sized work items (hk_items.cuh); each
+// warp carves its own slice of dynamic shared memory as MP scratch.  The LDLT
+// step loop (ldlt.cpp:91-135; parallel form 206-351) is recorded once per
+// (n, limbs) into a CUDA graph and replayed: per step i
+//     recip (1 warp)  ->  mulB (n-i-1 warps)  ->  trailing (~(n-i)^2/2 warps)
+//     ->  storeL (n-i-1 warps)
+// A non-positive pivot sets a device flag (first column wins); every later
+// item sees it and returns, and the host maps it to HK_ERR_PRECISION.
+#include "../../include/hankel_b200.h"
+#include "hk_items.cuh"
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+extern "C" int hk_moments_impl(unsigned, unsigned, int, int, uint32_t*, int32_t*, int32_t*, int*, const char**);
+extern "C" int hk_block_eigs_impl(int, int, const uint32_t*, const int32_t*, const int32_t*, int, double*, double*,
+                                  double*, const char**);
+
+namespace {
+
+using hk::Meta;
+using hk::MpArr;
+
+template <class F>
+__global__ void __launch_bounds__(256) k_items(long long n, int ws_words, F f) {
+    extern __shared__ uint32_t smem[];
+    const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    uint32_t* ws = smem + (size_t)wib * ws_words;
+    const long long nw = (long long)gridDim.x * wpb;
+    for (long long it = (long long)blockIdx.x * wpb + wib; it < n; it += nw) f(it, ws);
+}
+
+struct HkError {
+    int code;
+    std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw HkError{HK_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+struct DevArr {
+    uint32_t* d = nullptr;
+    Meta* m = nullptr;
+    long long cap = 0;
+    int L = 0;
+    void ensure(long long n, int limbs) {
+        if (n <= cap && limbs == L) return;
+        release();
+        ck(cudaMalloc(&d, size_t(n) * limbs * sizeof(uint32_t)), "cudaMalloc limbs");
+        ck(cudaMalloc(&m, size_t(n) * sizeof(Meta)), "cudaMalloc meta");
+        cap = n;
+        L = limbs;
+    }
+    void release() {
+        if (d) cudaFree(d);
+        if (m) cudaFree(m);
+        d = nullptr;
+        m = nullptr;
+        cap = 0;
+    }
+    MpArr view() const { return MpArr{d, m}; }
+};
+
+} // namespace
+
+struct hk_ctx {
+    int device = 0;
+    int L = 0;
+    int n = 0, m = 0, k = 0;
+    cudaStream_t st = nullptr;
+    DevArr mu, S, R, B, X, Y, T, T2, M;
+    int* d_err = nullptr;
+    std::string err;
+    int bad_col = -1;
+    bool factored = false, inverted = false, assembled = false;
+    int sm_count = 148;
+    long long launches = 0;
+    double t[7] = {0, 0, 0, 0, 0, 0, 0};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    // LDLT graph cache keyed by n
+    std::map<int, cudaGraphExec_t> graphs;
+    std::map<int, long long> graph_launches;
+    const void* graph_bufs[3] = {nullptr, nullptr, nullptr}; // S, R, B the graphs were captured on
+    std::vector<uint32_t> h_limbs;
+    std::vector<int32_t> h_e, h_s;
+};
+
+namespace {
+
+int ws_op_words(int L) { return hk::opws_words(L); }
+int ws_recip_words(int L) { return hk::recipws_words(L); }
+
+template <class F>
+void launch(hk_ctx* c, const F& f, long long n, int ws_words) {
+    if (n <= 0) return;
+    const size_t per_warp = size_t(ws_words) * sizeof(uint32_t);
+    int wpb = int((96 * 1024) / per_warp);
+    if (wpb > 8) wpb = 8;
+    if (wpb < 1) wpb = 1;
+    if ((long long)wpb > n) wpb = int(n);
+    const size_t smem = per_warp * wpb;
+    static std::map<const void*, size_t> configured;
+    const void* key = (const void*)&k_items<F>;
+    auto it = configured.find(key);
+    if (it == configured.end() || it->second < smem) {
+        ck(cudaFuncSetAttribute(k_items<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem < 48 * 1024 ? 48 * 1024 : smem)),
+           "cudaFuncSetAttribute");
+        configured[key] = smem < 48 * 1024 ? 48 * 1024 : smem;
+    }
+    long long blocks = (n + wpb - 1) / wpb;
+    const long long cap = (long long)c->sm_count * 32;
+    if (blocks > cap) blocks = cap;
+    k_items<F><<<unsigned(blocks), unsigned(32 * wpb), smem, c->st>>>(n, ws_words, f);
+    ck(cudaGetLastError(), "kernel launch");
+    ++c->launches;
+}
+
+int fail(hk_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+template <class Fn>
+int guarded(hk_ctx* c, Fn&& fn) {
+    if (!c) return HK_ERR_INVALID;
+    try {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        return fn();
+    } catch (const HkError& e) {
+        return fail(c, e.code, e.msg);
+    } catch (const std::exception& e) {
+        return fail(c, HK_ERR_RUNTIME, e.what());
+    }
+}
+
+void h2d_soa(hk_ctx* c, DevArr& a, long long n, const uint32_t* l, const int32_t* e, const int32_t* s) {
+    a.ensure(n, c->L);
+    ck(cudaMemcpyAsync(a.d, l, size_t(n) * c->L * sizeof(uint32_t), cudaMemcpyHostToDevice, c->st), "H2D limbs");
+    std::vector<Meta> hm(static_cast<size_t>(n));
+    for (long long i = 0; i < n; ++i) hm[size_t(i)] = Meta{e[i], s[i]};
+    ck(cudaMemcpyAsync(a.m, hm.data(), size_t(n) * sizeof(Meta), cudaMemcpyHostToDevice, c->st), "H2D meta");
+    ck(cudaStreamSynchronize(c->st), "sync");
+}
+
+// Gather `n` entries (device indices idx[]) into host SoA.
+void d2h_gather(hk_ctx* c, const DevArr& a, const std::vector<long long>& idx, uint32_t* l, int32_t* e, int32_t* s) {
+    const int L = c->L;
+    std::vector<Meta> hm(1);
+    for (size_t q = 0; q < idx.size(); ++q) {
+        ck(cudaMemcpyAsync(l + q * L, a.d + idx[q] * L, size_t(L) * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st),
+           "D2H limbs");
+        ck(cudaMemcpyAsync(&hm[0], a.m + idx[q], sizeof(Meta), cudaMemcpyDeviceToHost, c->st), "D2H meta");
+        ck(cudaStreamSynchronize(c->st), "sync");
+        e[q] = hm[0].exp;
+        s[q] = hm[0].sign;
+    }
+}
+
+void d2h_range(hk_ctx* c, const DevArr& a, long long first, long long n, uint32_t* l, int32_t* e, int32_t* s) {
+    const int L = c->L;
+    std::vector<Meta> hm(static_cast<size_t>(n));
+    ck(cudaMemcpyAsync(l, a.d + first * L, size_t(n) * L * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st), "D2H");
+    ck(cudaMemcpyAsync(hm.data(), a.m + first, size_t(n) * sizeof(Meta), cudaMemcpyDeviceToHost, c->st), "D2H meta");
+    ck(cudaStreamSynchronize(c->st), "sync");
+    for (long long i = 0; i < n; ++i) {
+        e[i] = hm[size_t(i)].exp;
+        s[i] = hm[size_t(i)].sign;
+    }
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Record the n LDLT steps on the ctx stream (used for graph capture).
+void enqueue_ldlt_steps(hk_ctx* c) {
+    const int N = c->n, L = c->L;
+    const int wo = ws_op_words(L), wr = ws_recip_words(L);
+    for (int i = 0; i < N; ++i) {
+        launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, wr);
+        const int nb = N - i - 1;
+        if (nb == 0) continue;
+        launch(c, hk::ItemMulB{c->S.view(), c->R.view(), c->B.view(), N, L, i, c->d_err}, nb, wo);
+        launch(c, hk::ItemTrailing{c->S.view(), c->B.view(), N, L, i, c->d_err}, (long long)nb * (nb + 1) / 2, wo);
+        launch(c, hk::ItemStoreL{c->S.view(), c->B.view(), N, L, i}, nb, 64);
+    }
+}
+
+int check_pivots(hk_ctx* c) {
+    int e = -1;
+    ck(cudaMemcpyAsync(&e, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->st), "D2H err");
+    ck(cudaStreamSynchronize(c->st), "sync");
+    if (e >= 0) {
+        c->bad_col = e;
+        c->factored = false;
+        return fail(c, HK_ERR_PRECISION,
+                    "LDLT pivot <= 0 at column " + std::to_string(e) + ": matrix not positive definite at p=" +
+                        std::to_string(32 * c->L) + " bits, increase the precision");
+    }
+    return HK_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int hk_version(void) { return 100; }
+
+int hk_create(int device, int limbs, hk_ctx** out) {
+    if (!out || limbs < 1 || limbs > 8192) return HK_ERR_INVALID;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HK_ERR_RUNTIME;
+    if (device < 0 || device >= ndev) return HK_ERR_INVALID;
+    hk_ctx* c = new hk_ctx();
+    c->device = device;
+    c->L = limbs;
+    const int rc = guarded(c, [&] {
+        cudaDeviceProp prop{};
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        c->sm_count = prop.multiProcessorCount;
+        ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
+        ck(cudaEventCreate(&c->ev[0]), "event");
+        ck(cudaEventCreate(&c->ev[1]), "event");
+        return HK_OK;
+    });
+    if (rc != HK_OK) {
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return HK_OK;
+}
+
+void hk_destroy(hk_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M}) a->release();
+    if (c->d_err) cudaFree(c->d_err);
+    for (auto e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+const char* hk_last_error(const hk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int hk_bad_column(const hk_ctx* c) { return c ? c->bad_col : -1; }
+int hk_limbs(const hk_ctx* c) { return c ? c->L : 0; }
+long long hk_launch_count(const hk_ctx* c) { return c ? c->launches : 0; }
+
+int hk_moments(unsigned beta_num, unsigned beta_den, int count, int limbs, uint32_t* out_limbs, int32_t* out_exps,
+               int32_t* out_signs, int* exact) {
+    const char* why = "";
+    int ex = 0;
+    const int rc = hk_moments_impl(beta_num, beta_den, count, limbs, out_limbs, out_exps, out_signs, &ex, &why);
+    if (exact) *exact = ex;
+    return rc;
+}
+
+int hk_load_moments(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, const int32_t* signs) {
+    return guarded(c, [&] {
+        if (n < 1) return fail(c, HK_ERR_INVALID, "matrix order must be >= 1");
+        const double t0 = now_s();
+        h2d_soa(c, c->mu, 2LL * n - 1, limbs, exps, signs);
+        c->t[5] = now_s() - t0;
+        c->n = n;
+        c->factored = c->inverted = c->assembled = false;
+        return HK_OK;
+    });
+}
+
+int hk_ldlt(hk_ctx* c) {
+    return guarded(c, [&] {
+        if (c->n < 1) return fail(c, HK_ERR_INVALID, "hk_ldlt: no moments loaded");
+        const int N = c->n, L = c->L;
+        const long long ntri = (long long)N * (N + 1) / 2;
+        c->S.ensure(ntri, L);
+        c->R.ensure(N, L);
+        c->B.ensure(N, L);
+        c->bad_col = -1;
+        ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
+        ck(cudaEventRecord(c->ev[0], c->st), "event");
+        launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
+        if (c->graph_bufs[0] != c->S.d || c->graph_bufs[1] != c->R.d || c->graph_bufs[2] != c->B.d) {
+            for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+            c->graphs.clear();
+            c->graph_bufs[0] = c->S.d;
+            c->graph_bufs[1] = c->R.d;
+            c->graph_bufs[2] = c->B.d;
+        }
+        auto it = c->graphs.find(N);
+        if (it == c->graphs.end()) {
+            cudaGraph_t g;
+            const long long before = c->launches;
+            ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            enqueue_ldlt_steps(c);
+            ck(cudaStreamEndCapture(c->st, &g), "end capture");
+            cudaGraphExec_t ge;
+            ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            it = c->graphs.emplace(N, ge).first;
+            c->graph_launches[N] = c->launches - before;
+            c->launches = before;
+        }
+        ck(cudaGraphLaunch(it->second, c->st), "graph launch");
+        c->launches += c->graph_launches[N];
+        ck(cudaEventRecord(c->ev[1], c->st), "event");
+        ck(cudaEventSynchronize(c->ev[1]), "sync");
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
+        c->t[1] = ms * 1e-3;
+        const int rc = check_pivots(c);
+        if (rc != HK_OK) return rc;
+        c->factored = true;
+        c->inverted = c->assembled = false;
+        return HK_OK;
+    });
+}
+
+int hk_get_D(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
+    return guarded(c, [&] {
+        if (!c->factored) return fail(c, HK_ERR_INVALID, "hk_get_D: not factored");
+        std::vector<long long> idx(size_t(c->n));
+        for (int i = 0; i < c->n; ++i) idx[size_t(i)] = hk::tri_idx(i, i, c->n);
+        d2h_gather(c, c->S, idx, limbs, exps, signs);
+        return HK_OK;
+    });
+}
+
+int hk_get_L_column(hk_ctx* c, int col, uint32_t* limbs, int32_t* exps, int32_t* signs) {
+    return guarded(c, [&] {
+        if (!c->factored) return fail(c, HK_ERR_INVALID, "hk_get_L_column: not factored");
+        if (col < 0 || col >= c->n) return fail(c, HK_ERR_INVALID, "hk_get_L_column: column out of range");
+        const long long cnt = c->n - col - 1;
+        if (cnt > 0) d2h_range(c, c->S, hk::tri_idx(col + 1, col, c->n), cnt, limbs, exps, signs);
+        return HK_OK;
+    });
+}
+
+int hk_invert_L_partial(hk_ctx* c, int m) {
+    return guarded(c, [&] {
+        if (!c->factored) return fail(c, HK_ERR_INVALID, "invert_L_partial: not factored");
+        const int N = c->n, L = c->L;
+        if (m < 1 || m > N) return fail(c, HK_ERR_INVALID, "invert_L_partial: need 1 <= m <= n");
+        c->m = m;
+        c->X.ensure((long long)N * m, L);
+        const int wo = ws_op_words(L);
+        ck(cudaEventRecord(c->ev[0], c->st), "event");
+        launch(c, hk::ItemInvInit{c->S.view(), c->X.view(), N, L, m}, (long long)N * m, 64);
+        for (int i = 0; i < N; ++i) {
+            const int b = i < m ? i : m;
+            const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
+            launch(c, hk::ItemInvStep{c->S.view(), c->X.view(), N, L, m, i}, items, wo);
+        }
+        ck(cudaEventRecord(c->ev[1], c->st), "event");
+        ck(cudaEventSynchronize(c->ev[1]), "sync");
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
+        c->t[2] = ms * 1e-3;
+        c->inverted = true;
+        c->assembled = false;
+        return HK_OK;
+    });
+}
+
+int hk_get_Linv(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
+    return guarded(c, [&] {
+        if (!c->inverted) return fail(c, HK_ERR_INVALID, "hk_get_Linv: not inverted");
+        d2h_range(c, c->X, 0, (long long)c->n * c->m, limbs, exps, signs);
+        return HK_OK;
+    });
+}
+
+int hk_assemble_block(hk_ctx* c, int k) {
+    return guarded(c, [&] {
+        if (!c->inverted) return fail(c, HK_ERR_INVALID, "assemble_truncated_inverse: not inverted");
+        if (k < 1 || k > c->m) return fail(c, HK_ERR_INVALID, "assemble_truncated_inverse: need 1 <= k <= m");
+        const int N = c->n, L = c->L, m = c->m;
+        int size = 1;
+        while (size < N) size *= 2;
+        const int npair = k * (k + 1) / 2;
+        c->Y.ensure((long long)N * m, L);
+        c->T.ensure((long long)npair * size, L);
+        c->T2.ensure((long long)npair * (size / 2 > 0 ? size / 2 : 1), L);
+        c->M.ensure((long long)k * k, L);
+        const int wo = ws_op_words(L);
+        ck(cudaEventRecord(c->ev[0], c->st), "event");
+        launch(c, hk::ItemBlockY{c->X.view(), c->R.view(), c->Y.view(), N, L, m}, (long long)N * m, wo);
+        launch(c, hk::ItemBlockTerms{c->X.view(), c->Y.view(), c->T.view(), N, L, m, k, size}, (long long)npair * size,
+               wo);
+        DevArr* cur = &c->T;
+        DevArr* nxt = &c->T2;
+        for (int half = size / 2; half >= 1; half /= 2) {
+            launch(c, hk::ItemTreeLevel{cur->view(), nxt->view(), L, half}, (long long)npair * half, wo);
+            std::swap(cur, nxt);
+        }
+        launch(c, hk::ItemBlockOut{cur->view(), c->M.view(), L, k}, npair, 64);
+        ck(cudaEventRecord(c->ev[1], c->st), "event");
+        ck(cudaEventSynchronize(c->ev[1]), "sync");
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
+        c->t[3] = ms * 1e-3;
+        c->k = k;
+        c->assembled = true;
+        return HK_OK;
+    });
+}
+
+int hk_get_block(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
+    return guarded(c, [&] {
+        if (!c->assembled) return fail(c, HK_ERR_INVALID, "hk_get_block: not assembled");
+        d2h_range(c, c->M, 0, (long long)c->k * c->k, limbs, exps, signs);
+        return HK_OK;
+    });
+}
+
+int hk_smallest_eigs(hk_ctx* c, int s, double* lambda_hi, double* lambda_lo, double* trunc_err) {
+    return guarded(c, [&] {
+        if (!c->assembled) return fail(c, HK_ERR_INVALID, "smallest_eigs_of_H: no block");
+        const int k = c->k, L = c->L;
+        const double t0 = now_s();
+        c->h_limbs.resize(size_t(k) * k * L);
+        c->h_e.resize(size_t(k) * k);
+        c->h_s.resize(size_t(k) * k);
+        d2h_range(c, c->M, 0, (long long)k * k, c->h_limbs.data(), c->h_e.data(), c->h_s.data());
+        const double t1 = now_s();
+        const char* why = "";
+        const int rc = hk_block_eigs_impl(k, L, c->h_limbs.data(), c->h_e.data(), c->h_s.data(), s, lambda_hi,
+                                          lambda_lo, trunc_err, &why);
+        c->t[6] = t1 - t0;
+        c->t[4] = now_s() - t1;
+        if (rc != HK_OK) return fail(c, rc, why);
+        return HK_OK;
+    });
+}
+
+int hk_compute(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, const int32_t* signs, int k,
+               double* lambda_hi, double* lambda_lo, double* trunc_err, int* s_out) {
+    if (!c) return HK_ERR_INVALID;
+    if (n < 1) return fail(c, HK_ERR_INVALID, "compute: need N >= 1");
+    if (k < 1) return fail(c, HK_ERR_INVALID, "compute: need k >= 1");
+    const double t0 = now_s();
+    const int kk = k < n ? k : n;    // pipeline.cpp:36
+    const int s = kk < 3 ? kk : 3;   // pipeline.cpp:64
+    int rc = hk_load_moments(c, n, limbs, exps, signs);
+    if (rc == HK_OK) rc = hk_ldlt(c);
+    if (rc == HK_OK) rc = hk_invert_L_partial(c, kk);
+    if (rc == HK_OK) rc = hk_assemble_block(c, kk);
+    if (rc == HK_OK) rc = hk_smallest_eigs(c, s, lambda_hi, lambda_lo, trunc_err);
+    if (s_out) *s_out = s;
+    c->t[0] = now_s() - t0;
+    return rc;
+}
+
+int hk_timings(const hk_ctx* c, double* out7) {
+    if (!c || !out7) return HK_ERR_INVALID;
+    for (int i = 0; i < 7; ++i) out7[i] = c->t[i];
+    return HK_OK;
+}
+
+int hk_mp_batch(hk_ctx* c, int op, long long count, const uint32_t* a_l, const int32_t* a_e, const int32_t* a_s,
+                const uint32_t* b_l, const int32_t* b_e, const int32_t* b_s, const uint32_t* c_l, const int32_t* c_e,
+                const int32_t* c_s, uint32_t* o_l, int32_t* o_e, int32_t* o_s) {
+    return guarded(c, [&] {
+        if (op < 0 || op > 3 || count < 1) return fail(c, HK_ERR_INVALID, "hk_mp_batch: bad op/count");
+        if ((op != HK_OP_RECIP && (!b_l || !b_e || !b_s)) || (op == HK_OP_FMS && (!c_l || !c_e || !c_s)))
+            return fail(c, HK_ERR_INVALID, "hk_mp_batch: missing operand");
+        const int L = c->L;
+        DevArr A, B, C, O;
+        h2d_soa(c, A, count, a_l, a_e, a_s);
+        if (op != HK_OP_RECIP) h2d_soa(c, B, count, b_l, b_e, b_s);
+        if (op == HK_OP_FMS) h2d_soa(c, C, count, c_l, c_e, c_s);
+        O.ensure(count, L);
+        const int ws = op == HK_OP_RECIP ? ws_recip_words(L) : ws_op_words(L);
+        launch(c, hk::ItemBatch{A.view(), B.view(), C.view(), O.view(), L, op}, count, ws);
+        ck(cudaStreamSynchronize(c->st), "sync");
+        d2h_range(c, O, 0, count, o_l, o_e, o_s);
+        A.release();
+        B.release();
+        C.release();
+        O.release();
+        return HK_OK;
+    });
+}
+
+} // extern "C"

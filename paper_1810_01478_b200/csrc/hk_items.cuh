@@ -1,0 +1,283 @@
+// hk_items.cuh — one warp-sized work item of each stage of the hot path.
+//
+// The CUDA kernels (kernels.cu) run these over grid-stride item ranges; the host
+// emulator (tools/emu_mp.cpp) runs the very same functions on an emulated warp,
+// so the index maps are tested on CPU too.
+//
+// HBM layout:
+//   S  — the Hankel working matrix, jagged lower triangle, column-major: entry
+//        (k, j), k >= j, at col_off(j) + (k - j), col_off(j) = j N - j (j-1)/2.
+//        After step i, column i holds D_i at (i,i) and L(k,i) below it — the
+//        in-place factor storage of ldlt.hpp:76-85 (L[j][r] = L(j+1+r, j)).
+//   R  — R_i = RNE(1/D_i), N entries.  B — the quotient column B_i, N entries.
+//   X  — first m columns of L^{-1}, row-major N x m (entry (r,c) valid c < min(r,m)).
+//   Y  — X(l,c) R_l, N x m.  T / T2 — block-reduction tree buffers.
+#pragma once
+
+#include "mpf_ops.cuh"
+
+namespace hk {
+
+struct MpArr {
+    uint32_t* d;
+    Meta* m;
+    HK_DEV uint32_t* limbs(long long e, int L) const { return d + e * (long long)L; }
+};
+
+HK_HD long long col_off(int j, int N) { return (long long)j * N - (long long)j * (j - 1) / 2; }
+HK_HD long long tri_idx(int k, int j, int N) { return col_off(j, N) + (k - j); }
+
+// w -> (j, k), 0 <= j <= k < n, column-major lower triangle of order n.
+HK_DEV void tri_decode(long long w, int n, int& j, int& k) {
+    const double b = 2.0 * n + 1.0;
+    int jj = int((b - sqrt(b * b - 8.0 * double(w))) * 0.5);
+    if (jj < 0) jj = 0;
+    if (jj > n - 1) jj = n - 1;
+    while (jj > 0 && col_off(jj, n) > w) --jj;
+    while (jj + 1 < n && col_off(jj + 1, n) <= w) ++jj;
+    j = jj;
+    k = jj + int(w - col_off(jj, n));
+}
+
+HK_DEV void copy_entry(uint32_t* dst, Meta* dm, const uint32_t* src, const Meta* sm, int L) {
+    for (int i = lane(); i < L; i += 32) dst[i] = src[i];
+    if (lane() == 0) *dm = *sm;
+    wsync();
+}
+
+// ---- S <- Hankel(mu): S(k,j) = mu_{k+j}
+struct ItemInitS {
+    MpArr S, mu;
+    int N, L;
+    HK_DEV void operator()(long long w, uint32_t*) const {
+        int j, k;
+        tri_decode(w, N, j, k);
+        copy_entry(S.limbs(w, L), S.m + w, mu.limbs(k + j, L), mu.m + (k + j), L);
+    }
+};
+
+// ---- R_i = RNE(1 / S_ii), pivot sign test (ldlt.cpp:111, 231-234, 280-284)
+struct ItemRecip {
+    MpArr S, R;
+    int N, L, i;
+    int* err;
+    HK_DEV void operator()(long long, uint32_t* ws) const {
+        if (*(volatile int*)err >= 0) return;
+        const long long e = tri_idx(i, i, N);
+        const Meta dm = S.m[e];
+        if (dm.sign <= 0) {
+            if (lane() == 0) atomicCAS_emu(err, i);
+            return;
+        }
+        const Meta r = warp_recip(S.limbs(e, L), dm, R.limbs(i, L), L, recipws_carve(ws, L));
+        if (lane() == 0) R.m[i] = r;
+        wsync();
+    }
+    HK_DEV static void atomicCAS_emu(int* err, int i) {
+#if defined(HK_WARP_EMU)
+        if (*err < 0) *err = i;
+#else
+        atomicCAS(err, -1, i);
+#endif
+    }
+};
+
+// ---- B_i(k) = RNE(S(k,i) * R_i), k = i+1+t
+struct ItemMulB {
+    MpArr S, R, B;
+    int N, L, i;
+    const int* err;
+    HK_DEV void operator()(long long t, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int k = i + 1 + int(t);
+        const long long e = tri_idx(k, i, N);
+        const Meta r = warp_mulr(S.limbs(e, L), S.m[e], R.limbs(i, L), R.m[i], B.limbs(k, L), L, opws_carve(ws, L));
+        if (lane() == 0) B.m[k] = r;
+        wsync();
+    }
+};
+
+// ---- trailing update S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)), i < j <= k < N
+//      (ldlt.cpp:122-129, the hot loop; one MP-FMA per item)
+struct ItemTrailing {
+    MpArr S, B;
+    int N, L, i;
+    const int* err;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int n2 = N - i - 1;
+        int jj, kk;
+        tri_decode(w, n2, jj, kk);
+        const int j = i + 1 + jj, k = i + 1 + kk;
+        const long long ec = tri_idx(k, j, N), ex = tri_idx(j, i, N);
+        uint32_t* c = S.limbs(ec, L);
+        const Meta r = warp_fms(c, S.m[ec], S.limbs(ex, L), S.m[ex], B.limbs(k, L), B.m[k], c, L, opws_carve(ws, L));
+        if (lane() == 0) S.m[ec] = r;
+        wsync();
+    }
+};
+
+// ---- column i of S <- B_i (L(k,i) stored in place), k = i+1+t
+struct ItemStoreL {
+    MpArr S, B;
+    int N, L, i;
+    HK_DEV void operator()(long long t, uint32_t*) const {
+        const int k = i + 1 + int(t);
+        const long long e = tri_idx(k, i, N);
+        copy_entry(S.limbs(e, L), S.m + e, B.limbs(k, L), B.m + k, L);
+    }
+};
+
+// ---- L^{-1}: X(r,c) <- L(r,c) for c < min(r, m)   (init_work_rows, inversion.cpp:64-76)
+struct ItemInvInit {
+    MpArr S, X;
+    int N, L, m;
+    HK_DEV void operator()(long long w, uint32_t*) const {
+        const int r = int(w / m), c = int(w % m);
+        const long long dst = (long long)r * m + c;
+        if (c < r) {
+            const long long e = tri_idx(r, c, N);
+            copy_entry(X.limbs(dst, L), X.m + dst, S.limbs(e, L), S.m + e, L);
+        } else {
+            for (int q = lane(); q < L; q += 32) X.limbs(dst, L)[q] = 0u;
+            if (lane() == 0) X.m[dst] = Meta{0, 0};
+            wsync();
+        }
+    }
+};
+
+// ---- L^{-1} row elimination step i (inversion.cpp:93-102):
+//      X(j,c) = RNE(X(j,c) - L(j,i) X(i,c)) for j > i, c < min(m,i);  X(j,i) = -L(j,i) if i < m
+struct ItemInvStep {
+    MpArr S, X;
+    int N, L, m, i;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const int b = i < m ? i : m;
+        const long long nfma = (long long)(N - i - 1) * b;
+        if (w < nfma) {
+            const int j = i + 1 + int(w / b), c = int(w % b);
+            const long long el = tri_idx(j, i, N);
+            const long long xc = (long long)j * m + c, xi = (long long)i * m + c;
+            uint32_t* o = X.limbs(xc, L);
+            const Meta r = warp_fms(o, X.m[xc], S.limbs(el, L), S.m[el], X.limbs(xi, L), X.m[xi], o, L,
+                                    opws_carve(ws, L));
+            if (lane() == 0) X.m[xc] = r;
+            wsync();
+        } else {
+            const int j = i + 1 + int(w - nfma);
+            const long long el = tri_idx(j, i, N);
+            const long long xd = (long long)j * m + i;
+            copy_entry(X.limbs(xd, L), X.m + xd, S.limbs(el, L), S.m + el, L);
+            if (lane() == 0) X.m[xd].sign = -X.m[xd].sign;
+            wsync();
+        }
+    }
+};
+
+// ---- block: Y(l,c) = X(l,c) R_l (c < l), R_l (c == l), 0 (c > l)
+struct ItemBlockY {
+    MpArr X, R, Y;
+    int N, L, m;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const int l = int(w / m), c = int(w % m);
+        uint32_t* o = Y.limbs(w, L);
+        if (c < l) {
+            const Meta r = warp_mulr(X.limbs(w, L), X.m[w], R.limbs(l, L), R.m[l], o, L, opws_carve(ws, L));
+            if (lane() == 0) Y.m[w] = r;
+            wsync();
+        } else if (c == l) {
+            copy_entry(o, Y.m + w, R.limbs(l, L), R.m + l, L);
+        } else {
+            for (int q = lane(); q < L; q += 32) o[q] = 0u;
+            if (lane() == 0) Y.m[w] = Meta{0, 0};
+            wsync();
+        }
+    }
+};
+
+// pair q -> (j, c), j <= c < k, row-major upper triangle
+HK_DEV void pair_decode(int q, int k, int& j, int& c) {
+    int jj = 0, rem = q;
+    while (rem >= k - jj) {
+        rem -= k - jj;
+        ++jj;
+    }
+    j = jj;
+    c = jj + rem;
+}
+
+// ---- block terms: T[q][l] = X(l,j) Y(l,c) for l in [c, N), zero elsewhere
+//      (inversion.cpp:253-257: one product and one division by D_l per term)
+struct ItemBlockTerms {
+    MpArr X, Y, T;
+    int N, L, m, k, size;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const int q = int(w / size), l = int(w % size);
+        int j, c;
+        pair_decode(q, k, j, c);
+        uint32_t* o = T.limbs(w, L);
+        if (l >= c && l < N) {
+            const long long yi = (long long)l * m + c;
+            if (l == j) {
+                copy_entry(o, T.m + w, Y.limbs(yi, L), Y.m + yi, L);
+            } else {
+                const long long xi = (long long)l * m + j;
+                const Meta r = warp_mulr(X.limbs(xi, L), X.m[xi], Y.limbs(yi, L), Y.m[yi], o, L, opws_carve(ws, L));
+                if (lane() == 0) T.m[w] = r;
+                wsync();
+            }
+        } else {
+            for (int t = lane(); t < L; t += 32) o[t] = 0u;
+            if (lane() == 0) T.m[w] = Meta{0, 0};
+            wsync();
+        }
+    }
+};
+
+// ---- one level of the fixed pairwise tree: T2[q][t] = T[q][2t] + T[q][2t+1]
+struct ItemTreeLevel {
+    MpArr T, T2;
+    int L, half;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const long long q = w / half, t = w % half;
+        const long long a = q * 2 * half + 2 * t, b = a + 1;
+        const Meta r = warp_addr(T.limbs(a, L), T.m[a], T.limbs(b, L), T.m[b], T2.limbs(w, L), L, opws_carve(ws, L));
+        if (lane() == 0) T2.m[w] = r;
+        wsync();
+    }
+};
+
+// ---- tree roots -> symmetric k x k block M (row-major)
+struct ItemBlockOut {
+    MpArr T, M;
+    int L, k;
+    HK_DEV void operator()(long long q, uint32_t*) const {
+        int j, c;
+        pair_decode(int(q), k, j, c);
+        const long long a = (long long)j * k + c, b = (long long)c * k + j;
+        copy_entry(M.limbs(a, L), M.m + a, T.limbs(q, L), T.m + q, L);
+        if (a != b) copy_entry(M.limbs(b, L), M.m + b, T.limbs(q, L), T.m + q, L);
+    }
+};
+
+// ---- generic batch ops (parity tests of the arithmetic itself)
+struct ItemBatch {
+    MpArr A, B, C, O;
+    int L, op; // 0 fms: O = C - A*B; 1 mul: O = A*B; 2 add: O = A + B; 3 recip: O = 1/A
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        Meta r;
+        if (op == 0)
+            r = warp_fms(C.limbs(w, L), C.m[w], A.limbs(w, L), A.m[w], B.limbs(w, L), B.m[w], O.limbs(w, L), L,
+                         opws_carve(ws, L));
+        else if (op == 1)
+            r = warp_mulr(A.limbs(w, L), A.m[w], B.limbs(w, L), B.m[w], O.limbs(w, L), L, opws_carve(ws, L));
+        else if (op == 2)
+            r = warp_addr(A.limbs(w, L), A.m[w], B.limbs(w, L), B.m[w], O.limbs(w, L), L, opws_carve(ws, L));
+        else
+            r = warp_recip(A.limbs(w, L), A.m[w], O.limbs(w, L), L, recipws_carve(ws, L));
+        if (lane() == 0) O.m[w] = r;
+        wsync();
+    }
+};
+
+} // namespace hk

@@ -1,0 +1,243 @@
+// host_math.cpp — host-side pieces of the path that the reference also runs on
+// the host (compiled by g++, linked into libhankel_b200.so):
+//
+//  * exact moments (moments.cpp:80-111, the factorial path of gamma_exact):
+//    a small schoolbook big integer, factorials by repeated small multiplies,
+//    then the correctly rounded conversion to the p-bit float format;
+//  * the small symmetric eigensolve (jacobi.cpp:27-103): cyclic Jacobi, but in
+//    IEEE binary128 (113-bit significand) instead of binary64 so that lambda is
+//    good to ~32 digits (the 20-digit target).
+//  * assign_columns (ldlt.cpp:22-35).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace hk_host {
+
+using Big = std::vector<uint32_t>; // little-endian magnitude
+
+static void big_mul_small(Big& a, uint32_t m) {
+    uint64_t carry = 0;
+    for (auto& w : a) {
+        const uint64_t t = (uint64_t)w * m + carry;
+        w = uint32_t(t);
+        carry = t >> 32;
+    }
+    if (carry) a.push_back(uint32_t(carry));
+}
+
+static int big_bitlen(const Big& a) {
+    for (int i = int(a.size()) - 1; i >= 0; --i)
+        if (a[size_t(i)]) return i * 32 + (32 - __builtin_clz(a[size_t(i)]));
+    return 0;
+}
+
+static bool big_bit(const Big& a, long b) {
+    if (b < 0) return false;
+    const size_t q = size_t(b >> 5);
+    return q < a.size() && ((a[q] >> (b & 31)) & 1u);
+}
+
+// RNE of the positive integer `a` into `limbs` words; returns exp; sets exact.
+static int big_to_mpf(const Big& a, int limbs, uint32_t* out, bool& exact) {
+    const int p = 32 * limbs;
+    const int nb = big_bitlen(a);
+    std::fill(out, out + limbs, 0u);
+    exact = true;
+    if (nb == 0) return 0;
+    const long shift = long(nb) - p; // out = a >> shift (shift may be negative)
+    for (int i = 0; i < p; ++i)
+        if (big_bit(a, shift + i)) out[i >> 5] |= 1u << (i & 31);
+    if (shift > 0) {
+        const bool rb = big_bit(a, shift - 1);
+        bool st = false;
+        for (long b = 0; b < shift - 1 && !st; ++b) st = big_bit(a, b);
+        exact = !rb && !st;
+        if (rb && (st || (out[0] & 1u))) {
+            int i = 0;
+            while (i < limbs && ++out[i] == 0u) ++i;
+            if (i == limbs) { // overflow to 2^p
+                out[limbs - 1] = 0x80000000u;
+                return nb + 1;
+            }
+        }
+    }
+    return nb;
+}
+
+} // namespace hk_host
+
+extern "C" int hk_moments_impl(unsigned beta_num, unsigned beta_den, int count, int limbs, uint32_t* out_limbs,
+                               int32_t* out_exps, int32_t* out_signs, int* exact, const char** why) {
+    using namespace hk_host;
+    if (beta_num == 0 || beta_den == 0 || (2ul * beta_den) % beta_num != 0) {
+        *why = "unsupported beta: 2/beta must be a positive integer";
+        return 3;
+    }
+    if (count < 1 || limbs < 1) {
+        *why = "need count >= 1 and limbs >= 1";
+        return 3;
+    }
+    const unsigned long q = 2ul * beta_den / beta_num; // doubled_inverse (moments.cpp:64-66)
+    if (q % 2 != 0) {
+        *why = "half-integer gamma moments (odd 2/beta) are not implemented";
+        return 3;
+    }
+    // mu_k = (q/2) * ((k+1) q/2 - 1)!   (moments.cpp:83-89, 105-107)
+    Big f{1u};
+    unsigned long have = 0; // f == have!
+    bool all_exact = true;
+    for (int k = 0; k < count; ++k) {
+        const unsigned long arg = (unsigned long)(k + 1) * q / 2 - 1;
+        while (have < arg) big_mul_small(f, uint32_t(++have));
+        Big mu = f;
+        big_mul_small(mu, uint32_t(q / 2));
+        bool ex = true;
+        out_exps[k] = big_to_mpf(mu, limbs, out_limbs + size_t(k) * limbs, ex);
+        out_signs[k] = 1;
+        all_exact = all_exact && ex;
+    }
+    *exact = all_exact ? 1 : 0;
+    return 0;
+}
+
+extern "C" int hk_assign_columns(int n, int workers, int32_t* owner) {
+    if (n < 1 || workers < 1) return 3;
+    for (int c = 0; c < n; ++c) {
+        const int block = c / workers, r = c % workers;
+        owner[c] = (block % 2 == 0) ? r : workers - 1 - r;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------ binary128 Jacobi
+
+namespace {
+
+using q128 = __float128;
+
+q128 qabs(q128 x) { return x < 0 ? -x : x; }
+
+q128 qsqrt(q128 x) {
+    if (x <= 0) return 0;
+    q128 s = std::sqrt((double)x);
+    for (int it = 0; it < 3; ++it) s = (s + x / s) / 2;
+    return s;
+}
+
+// Cyclic Jacobi, jacobi.cpp:27-72 line for line, in binary128.
+std::vector<q128> jacobi_q(std::vector<q128> m, int k, double tol_factor, int max_sweeps) {
+    auto at = [&](int i, int j) -> q128& { return m[size_t(i) * size_t(k) + size_t(j)]; };
+    auto off = [&]() {
+        q128 s = 0;
+        for (int i = 0; i < k; ++i)
+            for (int j = i + 1; j < k; ++j) s += 2 * at(i, j) * at(i, j);
+        return qsqrt(s);
+    };
+    q128 fro = 0;
+    for (auto v : m) fro += v * v;
+    const q128 tol = q128(tol_factor) * qsqrt(fro);
+    int sweep = 0;
+    while (k > 1 && off() > tol) {
+        if (++sweep > max_sweeps) throw std::runtime_error("jacobi_eigenvalues: no convergence after max sweeps");
+        for (int p = 0; p < k - 1; ++p)
+            for (int qq = p + 1; qq < k; ++qq) {
+                const q128 apq = at(p, qq);
+                if (apq == 0) continue;
+                const q128 app = at(p, p), aqq = at(qq, qq);
+                const q128 theta = (aqq - app) / (2 * apq);
+                const q128 t = (theta >= 0 ? q128(1) : q128(-1)) / (qabs(theta) + qsqrt(theta * theta + 1));
+                const q128 c = 1 / qsqrt(t * t + 1);
+                const q128 s = t * c;
+                at(p, p) = app - t * apq;
+                at(qq, qq) = aqq + t * apq;
+                at(p, qq) = 0;
+                at(qq, p) = 0;
+                for (int r = 0; r < k; ++r) {
+                    if (r == p || r == qq) continue;
+                    const q128 arp = at(r, p), arq = at(r, qq);
+                    at(r, p) = c * arp - s * arq;
+                    at(p, r) = at(r, p);
+                    at(r, qq) = s * arp + c * arq;
+                    at(qq, r) = at(r, qq);
+                }
+            }
+    }
+    std::vector<q128> ev(static_cast<size_t>(k));
+    for (int i = 0; i < k; ++i) ev[size_t(i)] = at(i, i);
+    std::sort(ev.begin(), ev.end());
+    return ev;
+}
+
+// p-bit float -> binary128: top 128 bits, scaled (truncation below 2^-125 rel.)
+q128 mpf_to_q(const uint32_t* d, int limbs, int exp, int sign) {
+    if (sign == 0) return 0;
+    unsigned __int128 top = 0;
+    for (int i = 0; i < 4; ++i) {
+        const int idx = limbs - 1 - i;
+        top = (top << 32) | (idx >= 0 ? d[idx] : 0u);
+    }
+    // top = the leading 128 bits of M (zero padded): value ~= top 2^(exp - 128)
+    q128 v = (q128)top;
+    int e = exp - 128;
+    while (e > 0) {
+        const int s = std::min(e, 60);
+        v *= (q128)(1ull << s);
+        e -= s;
+    }
+    while (e < 0) {
+        const int s = std::min(-e, 60);
+        v /= (q128)(1ull << s);
+        e += s;
+    }
+    return sign < 0 ? -v : v;
+}
+
+void split_dd(q128 v, double& hi, double& lo) {
+    hi = (double)v;
+    lo = (double)(v - (q128)hi);
+}
+
+} // namespace
+
+// block: k*k MP floats (host SoA).  Fills s lambdas (hi/lo) and trunc errors.
+extern "C" int hk_block_eigs_impl(int k, int limbs, const uint32_t* l, const int32_t* e, const int32_t* sg, int s,
+                                  double* lam_hi, double* lam_lo, double* trunc, const char** why) {
+    if (s < 1 || s > k) {
+        *why = "smallest_eigs_of_H: need 1 <= s <= k";
+        return 3;
+    }
+    try {
+        std::vector<q128> M(size_t(k) * size_t(k));
+        for (int i = 0; i < k * k; ++i) M[size_t(i)] = mpf_to_q(l + size_t(i) * limbs, limbs, e[i], sg[i]);
+        const double tol = 1e-32;
+        const std::vector<q128> mu = jacobi_q(M, k, tol, 100);
+        std::vector<q128> mum;
+        if (k > 1) {
+            std::vector<q128> Mm(size_t(k - 1) * size_t(k - 1));
+            for (int i = 0; i < k - 1; ++i)
+                for (int j = 0; j < k - 1; ++j) Mm[size_t(i) * size_t(k - 1) + size_t(j)] = M[size_t(i) * size_t(k) + size_t(j)];
+            mum = jacobi_q(Mm, k - 1, tol, 100);
+        }
+        for (int i = 1; i <= s; ++i) {
+            const q128 mi = mu[size_t(k - i)];
+            if (mi <= 0) {
+                *why = "smallest_eigs_of_H: non-positive block eigenvalue; the truncation is too aggressive or the "
+                       "precision too small";
+                return 1;
+            }
+            const q128 lam = 1 / mi;
+            split_dd(lam, lam_hi[i - 1], lam_lo[i - 1]);
+            trunc[i - 1] = i <= k - 1 ? (double)(lam - 1 / mum[size_t(k - 1 - i)]) : std::nan("");
+        }
+    } catch (const std::exception& ex) {
+        static thread_local std::string msg;
+        msg = ex.what();
+        *why = msg.c_str();
+        return 1;
+    }
+    return 0;
+}

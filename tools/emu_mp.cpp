@@ -1,0 +1,134 @@
+// tools/emu_mp.cpp — host lockstep-warp emulation of the device MP arithmetic
+// and of the per-item stage functions (test infrastructure, CPU only).
+//
+// Runs the SAME source as the sm_100a kernels (csrc/mpf_warp.cuh, mpf_ops.cuh,
+// hk_items.cuh compiled with -DHK_WARP_EMU) so that the carry-lookahead,
+// alignment/sticky and rounding logic, and the stage index maps, are checked
+// against oracle/mpfloat.py without a GPU (tests/test_emu.py).
+//
+// stdin protocol (all numbers decimal except limbs, which are hex):
+//   op <fms|mul|add|recip> <L> <count>       then count items of 3/2/2/1 operands
+//   path <L> <N> <m>                        then 2N-1 moments
+// operand line: "<sign> <exp> <limb0> ... <limb L-1>"
+// Output: one operand line per result (op), or for `path`: D (N lines), the
+// L^{-1} rows (N*m lines, row-major), the block (m*m lines), then "err <col>".
+#define HK_WARP_EMU 1
+#include "../paper_1810_01478_b200/csrc/hk_items.cuh"
+
+#include <cstdio>
+#include <iostream>
+#include <string>
+#include <vector>
+
+using namespace hk;
+
+struct HostArr {
+    std::vector<uint32_t> d;
+    std::vector<Meta> m;
+    HostArr(long long n, int L) : d(size_t(n) * L, 0u), m(size_t(n), Meta{0, 0}) {}
+    MpArr view() { return MpArr{d.data(), m.data()}; }
+};
+
+static void read_opd(HostArr& a, long long e, int L) {
+    int s, ex;
+    std::cin >> s >> ex;
+    a.m[e] = Meta{ex, s};
+    for (int i = 0; i < L; ++i) {
+        std::string h;
+        std::cin >> h;
+        a.d[size_t(e) * L + i] = uint32_t(std::stoul(h, nullptr, 16));
+    }
+}
+
+static void print_opd(const HostArr& a, long long e, int L) {
+    std::printf("%d %d", a.m[e].sign, a.m[e].exp);
+    for (int i = 0; i < L; ++i) std::printf(" %x", a.d[size_t(e) * L + i]);
+    std::printf("\n");
+}
+
+template <class F>
+static void run_items(long long n, int ws_words, const F& f) {
+    std::vector<uint32_t> ws(size_t(ws_words) + 64, 0xdeadbeefu);
+    hk_emu::run_warp([&] {
+        for (long long w = 0; w < n; ++w) f(w, ws.data());
+    });
+}
+
+static int ws_words_for(int L) {
+    const int a = opws_words(L), b = recipws_words(L);
+    return a > b ? a : b;
+}
+
+int main() {
+    std::string cmd;
+    while (std::cin >> cmd) {
+        if (cmd == "op") {
+            std::string op;
+            int L;
+            long long cnt;
+            std::cin >> op >> L >> cnt;
+            HostArr A(cnt, L), B(cnt, L), C(cnt, L), O(cnt, L);
+            int code = op == "fms" ? 0 : op == "mul" ? 1 : op == "add" ? 2 : 3;
+            for (long long e = 0; e < cnt; ++e) {
+                if (code == 0) {
+                    read_opd(C, e, L);
+                    read_opd(A, e, L);
+                    read_opd(B, e, L);
+                } else if (code == 3) {
+                    read_opd(A, e, L);
+                } else {
+                    read_opd(A, e, L);
+                    read_opd(B, e, L);
+                }
+            }
+            ItemBatch it{A.view(), B.view(), C.view(), O.view(), L, code};
+            run_items(cnt, ws_words_for(L), it);
+            for (long long e = 0; e < cnt; ++e) print_opd(O, e, L);
+        } else if (cmd == "path") {
+            int L, N, m;
+            std::cin >> L >> N >> m;
+            HostArr mu(2 * N - 1, L);
+            for (int e = 0; e < 2 * N - 1; ++e) read_opd(mu, e, L);
+            const long long ntri = (long long)N * (N + 1) / 2;
+            HostArr S(ntri, L), R(N, L), Bq(N, L), X((long long)N * m, L), Y((long long)N * m, L);
+            int err = -1;
+            const int ws = ws_words_for(L);
+            run_items(ntri, ws, ItemInitS{S.view(), mu.view(), N, L});
+            for (int i = 0; i < N && err < 0; ++i) {
+                run_items(1, ws, ItemRecip{S.view(), R.view(), N, L, i, &err});
+                if (err >= 0) break;
+                const int nb = N - i - 1;
+                run_items(nb, ws, ItemMulB{S.view(), R.view(), Bq.view(), N, L, i, &err});
+                run_items((long long)nb * (nb + 1) / 2, ws, ItemTrailing{S.view(), Bq.view(), N, L, i, &err});
+                run_items(nb, ws, ItemStoreL{S.view(), Bq.view(), N, L, i});
+            }
+            if (err < 0) {
+                run_items((long long)N * m, ws, ItemInvInit{S.view(), X.view(), N, L, m});
+                for (int i = 0; i < N; ++i) {
+                    const int b = i < m ? i : m;
+                    const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
+                    run_items(items, ws, ItemInvStep{S.view(), X.view(), N, L, m, i});
+                }
+                run_items((long long)N * m, ws, ItemBlockY{X.view(), R.view(), Y.view(), N, L, m});
+                int size = 1;
+                while (size < N) size *= 2;
+                const int k = m, npair = k * (k + 1) / 2;
+                HostArr T((long long)npair * size, L), T2((long long)npair * size, L), M((long long)k * k, L);
+                run_items((long long)npair * size, ws, ItemBlockTerms{X.view(), Y.view(), T.view(), N, L, m, k, size});
+                HostArr* cur = &T;
+                HostArr* nxt = &T2;
+                for (int half = size / 2; half >= 1; half /= 2) {
+                    run_items((long long)npair * half, ws, ItemTreeLevel{cur->view(), nxt->view(), L, half});
+                    std::swap(cur, nxt);
+                }
+                run_items(npair, ws, ItemBlockOut{cur->view(), M.view(), L, k});
+                for (int i = 0; i < N; ++i) print_opd(S, tri_idx(i, i, N), L);
+                for (long long e = 0; e < (long long)N * m; ++e) print_opd(X, e, L);
+                for (long long e = 0; e < (long long)k * k; ++e) print_opd(M, e, L);
+            }
+            std::printf("err %d\n", err);
+        }
+        std::fflush(stdout);
+    }
+    return 0;
+}
