@@ -130,7 +130,7 @@ int run_dump(const Args& a) {
     js << "],\"L_col0\":[";
     for (size_t r = 0; r < f.L[0].size(); ++r) js << (r ? "," : "") << "\"" << hex(f.L[0][r]) << "\"";
     js << "],\"Linv\":[";
-    for (int r = 0; r < a.n; ++r) {
+    for (int r = 0; r < (a.n <= 128 ? a.n : 0); ++r) {  // bulky: only for small orders
         js << (r ? "," : "") << "[";
         for (size_t c = 0; c < inv.rows[size_t(r)].size(); ++c) js << (c ? "," : "") << "\"" << hex(inv.rows[size_t(r)][c]) << "\"";
         js << "]";

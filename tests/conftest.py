@@ -1,0 +1,34 @@
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
+
+
+def _ensure_built(target):
+    if not os.path.exists(os.path.join(ROOT, target)):
+        subprocess.run(["make", "-C", ROOT, target], check=True, capture_output=True)
+
+
+@pytest.fixture(scope="session")
+def emu_bin():
+    _ensure_built("build/emu_mp")
+    return os.path.join(ROOT, "build", "emu_mp")
+
+
+@pytest.fixture(scope="session")
+def ref_driver():
+    path = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    if not os.path.exists(path):
+        if not os.path.isdir("/root/reference"):
+            pytest.skip("oracle/_ref not built and /root/reference absent")
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True, capture_output=True)
+    return path

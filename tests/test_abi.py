@@ -1,0 +1,73 @@
+"""The drop-in boundary on CPU: libhankel_b200.so loads, exports every symbol
+include/hankel_b200.h declares, and its host-only entry points work; with no GPU
+the device entry points fail loudly (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from oracle import restate as R
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "hankel_b200.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(hk_[A-Za-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1810_01478_b200 import api
+
+    lib = ctypes.CDLL(api.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert api.lib().hk_version() == 100
+
+
+def test_host_moments_match_reference_moments():
+    from paper_1810_01478_b200 import api
+
+    for beta, L in (((1, 2), 64), ((1, 1), 48), ((1, 3), 200)):
+        n = 40
+        mu, exact = api.build_hankel(beta, n, L)
+        assert exact
+        for j in range(2 * n - 1):
+            assert mu.to_fraction(j) == R.moment_integer(beta, j)
+    # precision too small -> correctly rounded, flagged inexact
+    mu, exact = api.build_hankel((1, 2), 30, 2)
+    assert not exact
+    from oracle import mpfloat as F
+
+    for j in range(59):
+        s, m, e = mu.entry(j)
+        assert F.MPF(s, m, e) == F.from_int(R.moment_integer((1, 2), j), 64)
+    with pytest.raises(ValueError):
+        api.build_hankel((2, 1), 4, 4)  # beta = 2: half-integer gamma path not implemented
+    with pytest.raises(ValueError):
+        api.build_hankel((3, 1), 4, 4)  # 2/beta not an integer (moments.cpp:74-75)
+
+
+def test_assign_columns_matches_reference():
+    from paper_1810_01478_b200 import api
+
+    for n in (1, 5, 6, 17, 64):
+        for w in (1, 2, 3, 4, 8):
+            assert api.assign_columns(n, w) == R.assign_columns(n, w)
+    with pytest.raises(ValueError):
+        api.assign_columns(0, 2)
+
+
+def test_device_entry_points_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_1810_01478_b200 import api
+
+    with pytest.raises(RuntimeError):
+        api.Context(4)

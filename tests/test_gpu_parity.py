@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle (run on a B200).
+
+Bit-exact where the product's semantics are defined (every MP op correctly
+rounded -> oracle/mpfloat.py is the spec); tolerance-based against the
+reference's fixed-point results exactly as north_star states: pivots d_n to
+relative 1e-20 and lambda_min to >= 20 significant digits (tests/golden/*.json,
+made from the reference by tests/golden/make_golden.py).
+"""
+import json
+import math
+import os
+import random
+
+import mpmath
+import pytest
+
+from oracle import mpfloat as F
+from oracle import restate as R
+from tests.mpf_helpers import fms_cases, from_arr, rnd, to_arr
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+PIVOT_RTOL = mpmath.mpf("1e-20")   # north_star: pivots to relative 1e-20
+LAMBDA_DIGITS = 20                 # north_star: lambda_min to >= 20 significant digits
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1810_01478_b200 import api as a
+
+    return a
+
+
+def mpf_of(fr):
+    return mpmath.mpf(fr.numerator) / fr.denominator
+
+
+# ------------------------------------------------------------------ arithmetic
+
+
+@pytest.mark.parametrize("L,count", [(1, 200), (2, 200), (3, 200), (8, 200), (33, 100), (96, 100), (192, 100),
+                                     (1152, 24), (1536, 16), (3584, 6)])
+def test_mp_ops_bit_exact(api, L, count):
+    rng = random.Random(20240517 + L)
+    p = 32 * L
+    with api.Context(L) as ctx:
+        cases = fms_cases(L, rng, count)
+        cs, xs, ys = (to_arr([t[i] for t in cases], L) for i in range(3))
+        got = from_arr(ctx.mp_batch(api.OP_FMS, xs, ys, cs))
+        assert got == [F.fms(c, x, y, p) for c, x, y in cases]
+        xs_l = [t[1] if t[1].s else rnd(L, rng) for t in cases]
+        got = from_arr(ctx.mp_batch(api.OP_MUL, to_arr(xs_l, L), ys))
+        assert got == [F.mul(x, t[2], p) for x, t in zip(xs_l, cases)]
+        got = from_arr(ctx.mp_batch(api.OP_ADD, to_arr(xs_l, L), cs))
+        assert got == [F.add(x, t[0], p) for x, t in zip(xs_l, cases)]
+        nrec = min(count, 24)
+        got = from_arr(ctx.mp_batch(api.OP_RECIP, to_arr(xs_l[:nrec], L)))
+        assert got == [F.recip(x, p) for x in xs_l[:nrec]]
+
+
+# ------------------------------------------------------------------ the path, bit-exact vs the model
+
+
+def run_path(api, beta, n, L, k):
+    mu, exact = api.build_hankel(beta, n, L)
+    assert exact
+    ctx = api.Context(L)
+    ctx.load_moments(mu)
+    ctx.decompose()
+    ctx.invert_L_partial(k)
+    ctx.assemble_truncated_inverse(k)
+    return ctx
+
+
+@pytest.mark.parametrize("beta,n,L,k", [((1, 2), 1, 2, 1), ((1, 2), 2, 4, 2), ((1, 2), 8, 4, 4), ((1, 1), 24, 6, 8),
+                                        ((1, 3), 20, 16, 12), ((1, 2), 64, 96, 8)])
+def test_path_bit_exact_vs_model(api, beta, n, L, k):
+    p = 32 * L
+    mu = [R.moment_integer(beta, j) for j in range(2 * n - 1)]
+    D, Lf, Rr = F.ldlt(mu, n, p)
+    X = F.invert_L_partial(Lf, n, k, p)
+    M = F.block(X, Rr, n, k, p)
+    with run_path(api, beta, n, L, k) as ctx:
+        assert from_arr(ctx.D()) == D
+        if n > 1:
+            assert from_arr(ctx.L_column(0)) == Lf[0]
+            assert from_arr(ctx.L_column(n - 2)) == Lf[n - 2]
+        gx = from_arr(ctx.Linv())
+        assert all(gx[r * k + c] == X[r][c] for r in range(n) for c in range(min(r, k)))
+        assert all(gx[r * k + c] == F.ZERO for r in range(n) for c in range(min(r, k), k))
+        assert from_arr(ctx.block()) == M
+
+
+def digest(vals):
+    import hashlib
+
+    h = hashlib.sha256()
+    for x in vals:
+        h.update(f"{x.s}:{x.e}:{x.m:x};".encode())
+    return h.hexdigest()
+
+
+def test_c2_bit_exact_vs_model_digest(api):
+    g = json.load(open(os.path.join(GOLD, "model_c2.json")))
+    n, L, k = g["n"], g["p"] // 32, g["k"]
+    with run_path(api, (1, 1), n, L, k) as ctx:
+        assert digest(from_arr(ctx.D())) == g["D_sha256"]
+        assert digest(from_arr(ctx.L_column(0))) == g["L_col0_sha256"]
+        assert digest(from_arr(ctx.Linv())) == g["Linv_sha256"]
+        assert digest(from_arr(ctx.block())) == g["block_sha256"]
+
+
+# ------------------------------------------------------------------ tolerance parity vs the reference
+
+
+def check_vs_golden(api, name):
+    g = json.load(open(os.path.join(GOLD, f"{name}.json")))
+    beta, n, L, k = tuple(g["beta"]), g["n"], g["p"] // 32, g["k"]
+    mu, exact = api.build_hankel(beta, n, L)
+    assert exact
+    with api.Context(L) as ctx:
+        rec = ctx.compute(mu, k)
+        D = ctx.D()
+        blk = ctx.block()
+    with mpmath.workdps(80):
+        worst = mpmath.mpf(0)
+        for i, want in enumerate(g["pivots"]):
+            worst = max(worst, abs(mpf_of(D.to_fraction(i)) / mpmath.mpf(want) - 1))
+        assert worst < PIVOT_RTOL, f"{name}: worst pivot rel err {worst}"
+        ev = R.block_eigs_mp([blk.to_fraction(i) for i in range(k * k)], k, dps=80)
+        for i in range(min(3, k)):
+            lam = 1 / ev[k - 1 - i]
+            want = mpmath.mpf(g["lambda"][i])
+            digits = -mpmath.log10(abs(lam / want - 1)) if lam != want else 80
+            assert digits >= LAMBDA_DIGITS, f"{name}: lambda_{i+1} only {digits} digits"
+        # host binary128 eigensolve: lambda_hi + lambda_lo to >= 20 digits too
+        lam1 = mpmath.mpf(rec.lambda_hi[0]) + mpmath.mpf(rec.lambda_lo[0])
+        assert abs(lam1 / mpmath.mpf(g["lambda"][0]) - 1) < mpmath.mpf(10) ** (-LAMBDA_DIGITS)
+    assert rec.lambda_hi[:3] == pytest.approx(g["reference_lambda_binary64"], rel=1e-13)
+    return worst
+
+
+def test_c1_parity_vs_reference(api):
+    check_vs_golden(api, "c1")
+
+
+def test_c2_parity_vs_reference(api):
+    check_vs_golden(api, "c2")
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLD, "c3.json")), reason="c3 golden not generated")
+def test_c3_parity_vs_reference(api):
+    check_vs_golden(api, "c3")
+
+
+def test_c2_closed_form_pivots(api):
+    """beta = 1: d_n = (n!)^2 exactly — independent of the reference."""
+    n, L = 256, 192
+    with run_path(api, (1, 1), n, L, 8) as ctx:
+        D = ctx.D()
+        for i in range(n):
+            assert D.to_fraction(i) == math.factorial(i) ** 2
+
+
+# ------------------------------------------------------------------ reference test mirrors and edge cases
+
+
+def test_reference_small_cases(api):
+    # test_ldlt.cpp:80-87 and test_inversion.cpp:44-51: D = (2, 168), L21 = 6, Linv21 = -6
+    with run_path(api, (1, 2), 2, 4, 2) as ctx:
+        D = ctx.D()
+        assert [D.to_fraction(i) for i in range(2)] == [2, 168]
+        assert ctx.L_column(0).to_fraction(0) == 6
+        assert ctx.Linv().to_fraction(2) == -6
+        # test_inversion.cpp:121-133: H_2^{-1} = (1/336)[[240,-12],[-12,2]]
+        blk = ctx.block()
+        from fractions import Fraction
+
+        for i, want in enumerate([Fraction(240, 336), Fraction(-12, 336), Fraction(-12, 336), Fraction(2, 336)]):
+            assert abs(blk.to_fraction(i) - want) <= abs(want) * Fraction(1, 2**120)
+        hi, lo, te = ctx.smallest_eigs_of_H(1)
+        assert hi[0] == pytest.approx(1.39648834586837266, rel=1e-15)  # test_jacobi.cpp:103-111
+        assert te[0] < 0
+
+
+def test_one_by_one_returns_mu0(api):
+    # test_pipeline.cpp:33-39
+    mu, _ = api.build_hankel((1, 2), 1, 8)
+    with api.Context(8) as ctx:
+        rec = ctx.compute(mu, 1)
+        assert rec.k == 1 and rec.lambda_hi == [2.0] and math.isnan(rec.trunc_err[0])
+
+
+def test_k_clamped_and_trunc_err_negative(api):
+    # pipeline.cpp:36 (k clamped to n) and test_pipeline.cpp:76-79 (negative trunc errors once k < N):
+    # with ~32 digits the errors resolve where the reference's binary64 rounds them to 0.
+    mu, _ = api.build_hankel((1, 2), 12, 16)
+    with api.Context(16) as ctx:
+        rec = ctx.compute(mu, 8)
+        assert all(t < 0 for t in rec.trunc_err)
+        rec5 = ctx.compute(api.build_hankel((1, 2), 5, 16)[0], 8)
+        assert rec5.k == 5
+
+
+def test_block_eigenvalue_grows_with_k(api):
+    # test_inversion.cpp:159-171
+    prev = 0.0
+    with run_path(api, (1, 2), 12, 16, 8) as ctx:
+        for k in range(2, 9):
+            ctx.assemble_truncated_inverse(k)
+            hi, lo, _ = ctx.smallest_eigs_of_H(1)
+            mu_max = 1 / (hi[0] + lo[0])
+            assert mu_max >= prev
+            prev = mu_max
+
+
+def test_precision_exhaustion_raises_with_column(api):
+    """beta = 1 at p = 32 bits: a pivot goes non-positive -> precision_error with the
+    first bad column (ldlt.cpp:83-87); the model agrees on the column."""
+    n, L = 16, 1
+    mu, _ = api.build_hankel((1, 1), n, L)
+    mu_int = [R.moment_integer((1, 1), j) for j in range(2 * n - 1)]
+    with pytest.raises(ArithmeticError) as ei:
+        F.ldlt(mu_int, n, 32)
+    want = int(str(ei.value).rsplit(" ", 1)[1])
+    with api.Context(L) as ctx:
+        ctx.load_moments(mu)
+        with pytest.raises(api.PrecisionError):
+            ctx.decompose()
+        assert ctx.bad_column == want
+        with pytest.raises(ValueError):
+            ctx.D()  # not factored
+
+
+def test_invalid_arguments(api):
+    mu, _ = api.build_hankel((1, 2), 4, 4)
+    with api.Context(4) as ctx:
+        with pytest.raises(ValueError):
+            ctx.invert_L_partial(2)  # not factored yet
+        ctx.load_moments(mu)
+        ctx.decompose()
+        with pytest.raises(ValueError):
+            ctx.invert_L_partial(5)  # m > n (inversion.cpp:80)
+        ctx.invert_L_partial(3)
+        with pytest.raises(ValueError):
+            ctx.assemble_truncated_inverse(4)  # k > m (inversion.cpp:234)
+
+
+def test_repeat_runs_bitwise_deterministic(api):
+    mu, _ = api.build_hankel((1, 2), 40, 32)
+    with api.Context(32) as ctx:
+        r1 = ctx.compute(mu, 8)
+        D1, B1 = from_arr(ctx.D()), from_arr(ctx.block())
+        r2 = ctx.compute(mu, 8)
+        assert from_arr(ctx.D()) == D1 and from_arr(ctx.block()) == B1
+        assert r1.lambda_hi == r2.lambda_hi and r1.lambda_lo == r2.lambda_lo
