@@ -118,6 +118,21 @@ int hk_mp_batch(hk_ctx* ctx, int op, long long count, const uint32_t* a_l, const
                 const uint32_t* b_l, const int32_t* b_e, const int32_t* b_s, const uint32_t* c_l,
                 const int32_t* c_e, const int32_t* c_s, uint32_t* o_l, int32_t* o_e, int32_t* o_s);
 
+/* The context's CUDA stream (cudaStream_t as void*), so a caller can order
+ * its own events / work with the path's kernels. */
+void* hk_stream(const hk_ctx* ctx);
+
+/* Measurement hook (no reference counterpart): run the LDLT once more,
+ * eagerly, with CUDA events around every trailing-update launch (the hot
+ * kernel, ldlt.cpp:122-129).  Outputs total trailing-kernel milliseconds, total
+ * LDLT milliseconds and the number of trailing launches. */
+int hk_profile_ldlt(hk_ctx* ctx, double* ms_trailing, double* ms_total, long long* n_trailing);
+
+/* Measured integer-MAC peak of the device: 32x32->64-bit limb MACs per second
+ * of the IMAD.WIDE carry chain the MP kernels use (register-only microkernel
+ * over all SMs).  The roofline denominator for the IMAD path. */
+int hk_peak_imad(int device, double* limb_macs_per_s);
+
 /* Balanced round-robin (boustrophedon) ownership map, assign_columns
  * (ldlt.cpp:22-35): owner[c] for c < n. */
 int hk_assign_columns(int n, int workers, int32_t* owner);

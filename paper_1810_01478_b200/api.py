@@ -63,6 +63,9 @@ def lib():
             "hk_launch_count": (C.c_longlong, [vp]),
             "hk_mp_batch": (C.c_int, [vp, C.c_int, C.c_longlong] + [u32p, i32p, i32p] * 4),
             "hk_assign_columns": (C.c_int, [C.c_int, C.c_int, i32p]),
+            "hk_stream": (vp, [vp]),
+            "hk_profile_ldlt": (C.c_int, [vp, f64p, f64p, C.POINTER(C.c_longlong)]),
+            "hk_peak_imad": (C.c_int, [C.c_int, f64p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -140,6 +143,15 @@ def build_hankel(beta: tuple[int, int], n: int, limbs: int) -> tuple[MPArray, bo
     exact = C.c_int(0)
     _check(lib().hk_moments(beta[0], beta[1], 2 * n - 1, limbs, *out.ptrs(), C.byref(exact)))
     return out, bool(exact.value)
+
+
+def peak_imad(device: int = 0) -> float:
+    """Measured IMAD.WIDE limb-MAC/s of the device (roofline denominator)."""
+    v = C.c_double()
+    rc = lib().hk_peak_imad(device, C.byref(v))
+    if rc != HK_OK:
+        raise RuntimeError(f"hk_peak_imad failed ({rc})")
+    return v.value
 
 
 def assign_columns(n: int, workers: int) -> list[int]:
@@ -271,6 +283,16 @@ class Context:
         t = np.zeros(7)
         lib().hk_timings(self.h, t.ctypes.data_as(C.POINTER(C.c_double)))
         return t.tolist()
+
+    def stream_ptr(self) -> int:
+        """cudaStream_t of the context (for torch.cuda.ExternalStream)."""
+        return int(lib().hk_stream(self.h) or 0)
+
+    def profile_ldlt(self):
+        """(ms in trailing-update kernels, ms total LDLT, number of trailing launches), eager run."""
+        a, b, n = C.c_double(), C.c_double(), C.c_longlong()
+        _check(lib().hk_profile_ldlt(self.h, C.byref(a), C.byref(b), C.byref(n)), self.h)
+        return a.value, b.value, n.value
 
     def launch_count(self) -> int:
         return int(lib().hk_launch_count(self.h))

@@ -495,3 +495,118 @@ int hk_mp_batch(hk_ctx* c, int op, long long count, const uint32_t* a_l, const i
 }
 
 } // extern "C"
+
+// ------------------------------------------------------------------ measurement hooks
+
+namespace {
+
+// Register-only IMAD.WIDE carry-chain microkernel: 8 independent 96-bit
+// accumulators per thread, the exact instruction mix of the column-sum loop.
+__global__ void __launch_bounds__(256) k_peak_imad(int iters, uint32_t seed, uint32_t* sink) {
+    uint32_t a0[8], a1[8], a2[8], x[8];
+    const uint32_t y = seed ^ (threadIdx.x * 2654435761u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        a0[j] = a1[j] = a2[j] = 0;
+        x[j] = seed * (j + 1) + threadIdx.x;
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm volatile("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+                         "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+                         "addc.u32 %2, %2, 0;"
+                         : "+r"(a0[j]), "+r"(a1[j]), "+r"(a2[j])
+                         : "r"(x[j]), "r"(y));
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s ^= a0[j] ^ a1[j] ^ a2[j];
+    if (s == 0x12345678u) sink[threadIdx.x] = s;
+}
+
+} // namespace
+
+extern "C" {
+
+void* hk_stream(const hk_ctx* c) { return c ? (void*)c->st : nullptr; }
+
+int hk_profile_ldlt(hk_ctx* c, double* ms_trailing, double* ms_total, long long* n_trailing) {
+    return guarded(c, [&] {
+        if (c->n < 1) return fail(c, HK_ERR_INVALID, "hk_profile_ldlt: no moments loaded");
+        const int N = c->n, L = c->L;
+        const long long ntri = (long long)N * (N + 1) / 2;
+        c->S.ensure(ntri, L);
+        c->R.ensure(N, L);
+        c->B.ensure(N, L);
+        ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
+        std::vector<cudaEvent_t> ev(size_t(2 * N) + 2);
+        for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+        const int wo = ws_op_words(L), wr = ws_recip_words(L);
+        ck(cudaEventRecord(ev[0], c->st), "event");
+        launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
+        long long nt = 0;
+        for (int i = 0; i < N; ++i) {
+            launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, wr);
+            const int nb = N - i - 1;
+            if (nb == 0) continue;
+            launch(c, hk::ItemMulB{c->S.view(), c->R.view(), c->B.view(), N, L, i, c->d_err}, nb, wo);
+            ck(cudaEventRecord(ev[2 + 2 * nt], c->st), "event");
+            launch(c, hk::ItemTrailing{c->S.view(), c->B.view(), N, L, i, c->d_err}, (long long)nb * (nb + 1) / 2, wo);
+            ck(cudaEventRecord(ev[3 + 2 * nt], c->st), "event");
+            ++nt;
+            launch(c, hk::ItemStoreL{c->S.view(), c->B.view(), N, L, i}, nb, 64);
+        }
+        ck(cudaEventRecord(ev[1], c->st), "event");
+        ck(cudaEventSynchronize(ev[1]), "sync");
+        double tr = 0;
+        for (long long q = 0; q < nt; ++q) {
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, ev[2 + 2 * q], ev[3 + 2 * q]), "elapsed");
+            tr += ms;
+        }
+        float tot = 0;
+        ck(cudaEventElapsedTime(&tot, ev[0], ev[1]), "elapsed");
+        for (auto& e : ev) cudaEventDestroy(e);
+        *ms_trailing = tr;
+        *ms_total = tot;
+        *n_trailing = nt;
+        const int rc = check_pivots(c);
+        if (rc == HK_OK) c->factored = true;
+        return rc;
+    });
+}
+
+int hk_peak_imad(int device, double* out) {
+    if (!out) return HK_ERR_INVALID;
+    if (cudaSetDevice(device) != cudaSuccess) return HK_ERR_RUNTIME;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return HK_ERR_RUNTIME;
+    uint32_t* sink = nullptr;
+    if (cudaMalloc(&sink, 1024 * sizeof(uint32_t)) != cudaSuccess) return HK_ERR_RUNTIME;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+    k_peak_imad<<<blocks, threads>>>(64, 1u, sink); // warm-up
+    double best = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(a);
+        k_peak_imad<<<blocks, threads>>>(iters, 12345u + rep, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        const double macs = double(blocks) * threads * iters * 8.0;
+        if (ms > 0 && macs / (ms * 1e-3) > best) best = macs / (ms * 1e-3);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return HK_ERR_RUNTIME;
+    *out = best;
+    return HK_OK;
+}
+
+} // extern "C"
