@@ -74,7 +74,7 @@ def run_path(api, beta, n, L, k):
 
 
 @pytest.mark.parametrize("beta,n,L,k", [((1, 2), 1, 2, 1), ((1, 2), 2, 4, 2), ((1, 2), 8, 4, 4), ((1, 1), 24, 6, 8),
-                                        ((1, 3), 20, 16, 12), ((1, 2), 64, 96, 8)])
+                                        ((1, 3), 20, 24, 12), ((1, 2), 64, 96, 8)])
 def test_path_bit_exact_vs_model(api, beta, n, L, k):
     p = 32 * L
     mu = [R.moment_integer(beta, j) for j in range(2 * n - 1)]
