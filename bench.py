@@ -233,7 +233,8 @@ def bench_ours(args, cfg):
     d2h = kk * kk * (4 * L + 8) + 3 * 3 * 8
 
     # ---- roofline of the dominant kernel (trailing update), instrumented eager run
-    ms_tr, ms_ldlt, n_tr = ctx.profile_ldlt()
+    prof, n_tr = ctx.profile_ldlt()
+    ms_tr, ms_ldlt = prof["trailing"], prof["total"]
     alg_macs = fmas(n) * L * L  # L^2 limb-MACs per MP-FMA
     achieved = alg_macs / (ms_tr * 1e-3) / 1e12
     peak = api.peak_imad(local) / 1e12
@@ -258,6 +259,7 @@ def bench_ours(args, cfg):
                      "per_launch": f"avg over {n_tr} launches: {ms_tr / n_tr:.4f} ms, "
                                    f"{alg_macs / n_tr:.3e} algorithmic limb-MACs",
                      "share_of_ldlt": ms_tr / ms_ldlt,
+                     "eager_ldlt_kernel_ms": prof,
                      "peak_how": "hk_peak_imad: register-only IMAD.WIDE carry-chain microkernel on this GPU, "
                                  "best of 5 (MEASURED_PEAKS.json has no integer peak)"},
         "gpu_launches": launches,

@@ -123,10 +123,11 @@ int hk_mp_batch(hk_ctx* ctx, int op, long long count, const uint32_t* a_l, const
 void* hk_stream(const hk_ctx* ctx);
 
 /* Measurement hook (no reference counterpart): run the LDLT once more,
- * eagerly, with CUDA events around every trailing-update launch (the hot
- * kernel, ldlt.cpp:122-129).  Outputs total trailing-kernel milliseconds, total
- * LDLT milliseconds and the number of trailing launches. */
-int hk_profile_ldlt(hk_ctx* ctx, double* ms_trailing, double* ms_total, long long* n_trailing);
+ * eagerly on one stream, with CUDA events around every launch.  ms5 receives
+ * the summed kernel milliseconds of [0] trailing update (the hot kernel,
+ * ldlt.cpp:122-129), [1] reciprocal, [2] B column, [3] L store, and [4] the
+ * whole eager LDLT; *n_trailing the number of trailing launches. */
+int hk_profile_ldlt(hk_ctx* ctx, double* ms5, long long* n_trailing);
 
 /* Measured integer-MAC peak of the device: 32x32->64-bit limb MACs per second
  * of the IMAD.WIDE carry chain the MP kernels use (register-only microkernel

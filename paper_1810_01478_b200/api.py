@@ -64,7 +64,7 @@ def lib():
             "hk_mp_batch": (C.c_int, [vp, C.c_int, C.c_longlong] + [u32p, i32p, i32p] * 4),
             "hk_assign_columns": (C.c_int, [C.c_int, C.c_int, i32p]),
             "hk_stream": (vp, [vp]),
-            "hk_profile_ldlt": (C.c_int, [vp, f64p, f64p, C.POINTER(C.c_longlong)]),
+            "hk_profile_ldlt": (C.c_int, [vp, f64p, C.POINTER(C.c_longlong)]),
             "hk_peak_imad": (C.c_int, [C.c_int, f64p]),
         }
         for name, (res, args) in sig.items():
@@ -289,10 +289,12 @@ class Context:
         return int(lib().hk_stream(self.h) or 0)
 
     def profile_ldlt(self):
-        """(ms in trailing-update kernels, ms total LDLT, number of trailing launches), eager run."""
-        a, b, n = C.c_double(), C.c_double(), C.c_longlong()
-        _check(lib().hk_profile_ldlt(self.h, C.byref(a), C.byref(b), C.byref(n)), self.h)
-        return a.value, b.value, n.value
+        """Eager instrumented LDLT: ({kernel: summed ms}, number of trailing launches)."""
+        ms = np.zeros(5)
+        n = C.c_longlong()
+        _check(lib().hk_profile_ldlt(self.h, ms.ctypes.data_as(C.POINTER(C.c_double)), C.byref(n)), self.h)
+        keys = ("trailing", "recip", "mulB", "storeL", "total")
+        return dict(zip(keys, ms.tolist())), n.value
 
     def launch_count(self) -> int:
         return int(lib().hk_launch_count(self.h))

@@ -76,7 +76,10 @@ struct hk_ctx {
     int device = 0;
     int L = 0;
     int n = 0, m = 0, k = 0;
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr;  // bulk / default stream of the context
+    cudaStream_t st2 = nullptr; // high-priority look-ahead stream
+    cudaEvent_t evFork = nullptr, evJoin = nullptr;
+    std::vector<cudaEvent_t> evP, evR; // per-step dependencies (graph capture)
     DevArr mu, S, R, B, X, Y, T, T2, M;
     int* d_err = nullptr;
     std::string err;
@@ -99,9 +102,13 @@ namespace {
 int ws_op_words(int L) { return hk::opws_words(L); }
 int ws_recip_words(int L) { return hk::recipws_words(L); }
 
+// One warp per item, one short-lived block per `wpb` items (no grid-stride
+// persistence), so blocks of the high-priority look-ahead stream are
+// dispatched as soon as any bulk block retires.
 template <class F>
-void launch(hk_ctx* c, const F& f, long long n, int ws_words) {
+void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = nullptr) {
     if (n <= 0) return;
+    if (!st) st = c->st;
     const size_t per_warp = size_t(ws_words) * sizeof(uint32_t);
     int wpb = int((96 * 1024) / per_warp);
     if (wpb > 8) wpb = 8;
@@ -117,9 +124,9 @@ void launch(hk_ctx* c, const F& f, long long n, int ws_words) {
         configured[key] = smem < 48 * 1024 ? 48 * 1024 : smem;
     }
     long long blocks = (n + wpb - 1) / wpb;
-    const long long cap = (long long)c->sm_count * 32;
+    const long long cap = 1LL << 30;
     if (blocks > cap) blocks = cap;
-    k_items<F><<<unsigned(blocks), unsigned(32 * wpb), smem, c->st>>>(n, ws_words, f);
+    k_items<F><<<unsigned(blocks), unsigned(32 * wpb), smem, st>>>(n, ws_words, f);
     ck(cudaGetLastError(), "kernel launch");
     ++c->launches;
 }
@@ -181,18 +188,62 @@ double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// Record the n LDLT steps on the ctx stream (used for graph capture).
+// B_i lives in buffer i % 2 (B_{i+1} is produced while B_i is still read).
+MpArr b_buf(hk_ctx* c, int i) {
+    const long long off = (long long)(i & 1) * c->n;
+    return MpArr{c->B.d + off * c->L, c->B.m + off};
+}
+
+// Record the n LDLT steps with depth-1 look-ahead (ldlt.cpp:271-331) on two
+// streams (captured into one graph):
+//   LA   (high priority): P(i+1) = update column i+1 with step i, R_{i+1} = recip,
+//                         B_{i+1} = column * R_{i+1}          — the latency chain
+//   BULK (ctx stream)   : U(i) = step-i update of columns i+2..N-1, then
+//                         STORE(i): column i <- B_i (L in place)
+// U(i) needs B_i (end of P(i)); P(i+1) needs column i+1 after step i-1 (end of
+// U(i-1)+STORE(i-1)); STORE(i) needs P(i+1) to have read S(i+1,i).  So P(i+1)
+// overlaps U(i) and the critical path per step is max(U(i), P(i+1)).
 void enqueue_ldlt_steps(hk_ctx* c) {
     const int N = c->n, L = c->L;
     const int wo = ws_op_words(L), wr = ws_recip_words(L);
+    cudaStream_t la = c->st2, bulk = c->st;
+    std::vector<cudaEvent_t>& evP = c->evP;
+    std::vector<cudaEvent_t>& evR = c->evR;
+    ck(cudaEventRecord(c->evFork, bulk), "fork");
+    ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
+    launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, 0, c->d_err}, 1, wr, la);
+    launch(c, hk::ItemMulB{c->S.view(), c->R.view(), b_buf(c, 0), N, L, 0, c->d_err}, N - 1, wo, la);
+    ck(cudaEventRecord(evP[0], la), "evP");
     for (int i = 0; i < N; ++i) {
-        launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, wr);
-        const int nb = N - i - 1;
-        if (nb == 0) continue;
-        launch(c, hk::ItemMulB{c->S.view(), c->R.view(), c->B.view(), N, L, i, c->d_err}, nb, wo);
-        launch(c, hk::ItemTrailing{c->S.view(), c->B.view(), N, L, i, c->d_err}, (long long)nb * (nb + 1) / 2, wo);
-        launch(c, hk::ItemStoreL{c->S.view(), c->B.view(), N, L, i}, nb, 64);
+        ck(cudaStreamWaitEvent(bulk, evP[i], 0), "wait P");
+        const long long nu = (long long)(N - i - 2) * (N - i - 1) / 2;
+        launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 2, c->d_err}, nu, wo, bulk);
+        if (i + 1 < N) {
+            if (i > 0) ck(cudaStreamWaitEvent(la, evR[i - 1], 0), "wait R");
+            launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 1, c->d_err}, N - i - 1, wo, la);
+            launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wr, la);
+            launch(c, hk::ItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err}, N - i - 2, wo,
+                   la);
+            ck(cudaEventRecord(evP[i + 1], la), "evP");
+            ck(cudaStreamWaitEvent(bulk, evP[i + 1], 0), "wait P next");
+        }
+        launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i), N, L, i}, N - i - 1, 64, bulk);
+        ck(cudaEventRecord(evR[i], bulk), "evR");
     }
+    ck(cudaEventRecord(c->evJoin, la), "join");
+    ck(cudaStreamWaitEvent(bulk, c->evJoin, 0), "join wait");
+}
+
+void ensure_step_events(hk_ctx* c, int N) {
+    auto grow = [](std::vector<cudaEvent_t>& v, int n) {
+        while ((int)v.size() < n) {
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            v.push_back(e);
+        }
+    };
+    grow(c->evP, N);
+    grow(c->evR, N);
 }
 
 int check_pivots(hk_ctx* c) {
@@ -229,6 +280,11 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
         c->sm_count = prop.multiProcessorCount;
         ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "cudaStreamCreate");
+        int lo = 0, hi = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+        ck(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi), "cudaStreamCreate la");
+        ck(cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming), "event");
         ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
         ck(cudaEventCreate(&c->ev[0]), "event");
         ck(cudaEventCreate(&c->ev[1]), "event");
@@ -250,6 +306,11 @@ void hk_destroy(hk_ctx* c) {
     if (c->d_err) cudaFree(c->d_err);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto e : c->evP) cudaEventDestroy(e);
+    for (auto e : c->evR) cudaEventDestroy(e);
+    if (c->evFork) cudaEventDestroy(c->evFork);
+    if (c->evJoin) cudaEventDestroy(c->evJoin);
+    if (c->st2) cudaStreamDestroy(c->st2);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
 }
@@ -287,7 +348,8 @@ int hk_ldlt(hk_ctx* c) {
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
-        c->B.ensure(N, L);
+        c->B.ensure(2LL * N, L);
+        ensure_step_events(c, N);
         c->bad_col = -1;
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         ck(cudaEventRecord(c->ev[0], c->st), "event");
@@ -531,45 +593,63 @@ extern "C" {
 
 void* hk_stream(const hk_ctx* c) { return c ? (void*)c->st : nullptr; }
 
-int hk_profile_ldlt(hk_ctx* c, double* ms_trailing, double* ms_total, long long* n_trailing) {
+int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
     return guarded(c, [&] {
         if (c->n < 1) return fail(c, HK_ERR_INVALID, "hk_profile_ldlt: no moments loaded");
         const int N = c->n, L = c->L;
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
-        c->B.ensure(N, L);
+        c->B.ensure(2LL * N, L);
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
-        std::vector<cudaEvent_t> ev(size_t(2 * N) + 2);
-        for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+        struct Rec {
+            int kind;
+            cudaEvent_t a, b;
+        };
+        std::vector<Rec> recs;
+        auto timed = [&](int kind, auto&& fn) {
+            Rec r{kind, nullptr, nullptr};
+            ck(cudaEventCreate(&r.a), "event");
+            ck(cudaEventCreate(&r.b), "event");
+            ck(cudaEventRecord(r.a, c->st), "event");
+            fn();
+            ck(cudaEventRecord(r.b, c->st), "event");
+            recs.push_back(r);
+        };
         const int wo = ws_op_words(L), wr = ws_recip_words(L);
-        ck(cudaEventRecord(ev[0], c->st), "event");
+        cudaEvent_t e0, e1;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        ck(cudaEventRecord(e0, c->st), "event");
         launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
         long long nt = 0;
         for (int i = 0; i < N; ++i) {
-            launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, wr);
+            timed(1, [&] { launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, wr); });
             const int nb = N - i - 1;
             if (nb == 0) continue;
-            launch(c, hk::ItemMulB{c->S.view(), c->R.view(), c->B.view(), N, L, i, c->d_err}, nb, wo);
-            ck(cudaEventRecord(ev[2 + 2 * nt], c->st), "event");
-            launch(c, hk::ItemTrailing{c->S.view(), c->B.view(), N, L, i, c->d_err}, (long long)nb * (nb + 1) / 2, wo);
-            ck(cudaEventRecord(ev[3 + 2 * nt], c->st), "event");
+            timed(2, [&] { launch(c, hk::ItemMulB{c->S.view(), c->R.view(), b_buf(c, i), N, L, i, c->d_err}, nb, wo); });
+            timed(0, [&] {
+                launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 1, c->d_err},
+                       (long long)nb * (nb + 1) / 2, wo);
+            });
             ++nt;
-            launch(c, hk::ItemStoreL{c->S.view(), c->B.view(), N, L, i}, nb, 64);
+            timed(3, [&] { launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i), N, L, i}, nb, 64); });
         }
-        ck(cudaEventRecord(ev[1], c->st), "event");
-        ck(cudaEventSynchronize(ev[1]), "sync");
-        double tr = 0;
-        for (long long q = 0; q < nt; ++q) {
+        ck(cudaEventRecord(e1, c->st), "event");
+        ck(cudaEventSynchronize(e1), "sync");
+        for (int q = 0; q < 5; ++q) ms5[q] = 0;
+        for (auto& r : recs) {
             float ms = 0;
-            ck(cudaEventElapsedTime(&ms, ev[2 + 2 * q], ev[3 + 2 * q]), "elapsed");
-            tr += ms;
+            ck(cudaEventElapsedTime(&ms, r.a, r.b), "elapsed");
+            ms5[r.kind] += ms;
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
         }
         float tot = 0;
-        ck(cudaEventElapsedTime(&tot, ev[0], ev[1]), "elapsed");
-        for (auto& e : ev) cudaEventDestroy(e);
-        *ms_trailing = tr;
-        *ms_total = tot;
+        ck(cudaEventElapsedTime(&tot, e0, e1), "elapsed");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        ms5[4] = tot;
         *n_trailing = nt;
         const int rc = check_pivots(c);
         if (rc == HK_OK) c->factored = true;

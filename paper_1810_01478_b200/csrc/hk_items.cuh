@@ -97,18 +97,21 @@ struct ItemMulB {
     }
 };
 
-// ---- trailing update S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)), i < j <= k < N
-//      (ldlt.cpp:122-129, the hot loop; one MP-FMA per item)
+// ---- trailing update S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)), jfirst <= j <= k < N
+//      (ldlt.cpp:122-129, the hot loop; one MP-FMA per item).  Items enumerate
+//      the column-major triangle of columns jfirst..N-1, so the first N-jfirst
+//      items are exactly column jfirst: jfirst = i+1 with N-i-1 items is the
+//      look-ahead column update (ldlt.cpp:274-277), jfirst = i+2 the bulk.
 struct ItemTrailing {
     MpArr S, B;
-    int N, L, i;
+    int N, L, i, jfirst;
     const int* err;
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         if (*(volatile const int*)err >= 0) return;
-        const int n2 = N - i - 1;
+        const int n2 = N - jfirst;
         int jj, kk;
         tri_decode(w, n2, jj, kk);
-        const int j = i + 1 + jj, k = i + 1 + kk;
+        const int j = jfirst + jj, k = jfirst + kk;
         const long long ec = tri_idx(k, j, N), ex = tri_idx(j, i, N);
         uint32_t* c = S.limbs(ec, L);
         const Meta r = warp_fms(c, S.m[ec], S.limbs(ex, L), S.m[ex], B.limbs(k, L), B.m[k], c, L, opws_carve(ws, L));

@@ -10,6 +10,18 @@
 
 namespace hk {
 
+// Test hook: the host emulator can force the reciprocal's exact midpoint test
+// on every call (it is otherwise skipped unless z lies near a midpoint).
+#if defined(HK_WARP_EMU)
+inline bool& force_exact_recip() {
+    static bool f = false;
+    return f;
+}
+#define HK_FORCE_EXACT_RECIP (::hk::force_exact_recip())
+#else
+#define HK_FORCE_EXACT_RECIP false
+#endif
+
 struct Meta {
     int exp;
     int sign;
@@ -37,20 +49,51 @@ HK_DEV OpWs opws_carve(uint32_t* base, int nmax) {
     return w;
 }
 
+// Short product: only limb columns t >= L - kGuardLimbs of x*y are formed
+// (about L^2/2 + 6L limb-MACs instead of L^2).  The dropped part E of the
+// product satisfies 0 <= E < L 2^(32 t0 + 32) < 2^(32 t0 + 45) units of the
+// product's LSB (L <= 4096), so the exact result lies within 2^(lsbP+32 t0+46)
+// of the computed sum; warp_round_sum's Ziv test proves the rounding is still
+// the correctly rounded one, else the exact full product is formed (rare: it
+// needs a rounding midpoint within ~2^-70 ulp, or > ~100 bits of cancellation —
+// the LDLT loses <= 12 bits per update, SURVEY C1-C3 measured).
+constexpr int kGuardLimbs = 6;
+
+HK_DEV void stage_and_mul(const uint32_t* xd, const uint32_t* yd, int L, const OpWs& ws, int t0) {
+    warp_copy(ws.A, xd, L);
+    warp_stage_padded(ws.Bp, yd, L);
+    wsync();
+    warp_mul(ws.A, L, ws.Bp, L, ws.P, t0);
+    wsync();
+}
+
+// out = RNE(c + sp * |x y|) given the signed product sign sp (shared by fms / mul).
+HK_DEV RMeta round_with_product(const Opd& X, const uint32_t* xd, const uint32_t* yd, int lsbP, int sp,
+                                uint32_t* out, int L, const OpWs& ws) {
+    const int t0 = L > kGuardLimbs ? L - kGuardLimbs : 0;
+    stage_and_mul(xd, yd, L, ws, t0);
+    if (t0 > 0) {
+        const Opd Yh{ws.P + t0, 2 * L - t0, lsbP + 32 * t0, sp};
+        bool ok = false;
+        const RMeta r = warp_round_sum(X, Yh, ws.G, out, L, lsbP + 32 * t0 + 46, &ok);
+        if (ok) return r;
+        stage_and_mul(xd, yd, L, ws, 0); // the window overwrote A / Bp: restage, exact product
+    }
+    const Opd Y{ws.P, 2 * L, lsbP, sp};
+    return warp_round_sum(X, Y, ws.G, out, L);
+}
+
 // out = RNE(c - x*y).  c / out may alias (in global memory).
 HK_DEV Meta warp_fms(const uint32_t* cd, Meta cm, const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym,
                      uint32_t* out, int L, const OpWs& ws) {
     const int sp = -(xm.sign * ym.sign);
-    if (sp != 0) {
-        warp_copy(ws.A, xd, L);
-        warp_stage_padded(ws.Bp, yd, L);
-        wsync();
-        warp_mul(ws.A, L, ws.Bp, L, ws.P);
-        wsync();
-    }
     const Opd X{cd, L, cm.exp - 32 * L, cm.sign};
-    const Opd Y{ws.P, 2 * L, xm.exp + ym.exp - 64 * L, sp};
-    const RMeta r = warp_round_sum(X, Y, ws.G, out, L);
+    if (sp == 0) {
+        const Opd Z{nullptr, 0, 0, 0};
+        const RMeta r = warp_round_sum(X, Z, ws.G, out, L);
+        return Meta{r.exp, r.sign};
+    }
+    const RMeta r = round_with_product(X, xd, yd, xm.exp + ym.exp - 64 * L, sp, out, L, ws);
     return Meta{r.exp, r.sign};
 }
 
@@ -58,16 +101,12 @@ HK_DEV Meta warp_fms(const uint32_t* cd, Meta cm, const uint32_t* xd, Meta xm, c
 HK_DEV Meta warp_mulr(const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym, uint32_t* out, int L,
                       const OpWs& ws) {
     const int sp = xm.sign * ym.sign;
-    if (sp != 0) {
-        warp_copy(ws.A, xd, L);
-        warp_stage_padded(ws.Bp, yd, L);
-        wsync();
-        warp_mul(ws.A, L, ws.Bp, L, ws.P);
-        wsync();
-    }
-    const Opd X{ws.P, 2 * L, xm.exp + ym.exp - 64 * L, sp};
     const Opd Z{nullptr, 0, 0, 0};
-    const RMeta r = warp_round_sum(X, Z, ws.G, out, L);
+    if (sp == 0) {
+        const RMeta r = warp_round_sum(Z, Z, ws.G, out, L);
+        return Meta{r.exp, r.sign};
+    }
+    const RMeta r = round_with_product(Z, xd, yd, xm.exp + ym.exp - 64 * L, sp, out, L, ws);
     return Meta{r.exp, r.sign};
 }
 
@@ -96,28 +135,31 @@ struct RecipWs {
     uint32_t *Z, *E, *T, *A, *Bp, *P, *G, *one, *tmp;
 };
 
+HK_HD int align4(int n) { return (n + 3) & ~3; }
+
+// Every region starts 16-byte aligned (warp_mul reads A with 128-bit loads).
 HK_HD int recipws_words(int L) {
     const int nm = L + 2;
-    return 3 * (nm + 1) + nm + (nm + 64) + (2 * nm + 2) + (2 * nm + 8) + 2;
+    return 3 * align4(nm + 1) + align4(nm) + align4(nm + 64) + align4(2 * nm + 2) + align4(2 * nm + 8) + 4;
 }
 
 HK_DEV RecipWs recipws_carve(uint32_t* b, int L) {
     const int nm = L + 2;
     RecipWs w;
-    w.Z = b;
-    b += nm + 1;
-    w.E = b;
-    b += nm + 1;
-    w.T = b;
-    b += nm + 1;
     w.A = b;
-    b += nm;
+    b += align4(nm);
+    w.Z = b;
+    b += align4(nm + 1);
+    w.E = b;
+    b += align4(nm + 1);
+    w.T = b;
+    b += align4(nm + 1);
     w.Bp = b;
-    b += nm + 64;
+    b += align4(nm + 64);
     w.P = b;
-    b += 2 * nm + 2;
+    b += align4(2 * nm + 2);
     w.G = b;
-    b += 2 * nm + 8;
+    b += align4(2 * nm + 8);
     w.one = b;
     w.tmp = b + 1;
     return w;
@@ -186,8 +228,18 @@ HK_DEV Meta warp_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, const 
     const Opd none{nullptr, 0, 0, 0};
     RMeta rr = warp_round_sum(zf, none, w.G, w.T, L);
     int rexp = rr.exp;
+    // Ziv: after the last Newton step at L+2 limbs, |z - 1/m| is a few units
+    // of z's last limb, so when the two discarded limbs are far from the
+    // half-way pattern 0x8000..0, RNE(z) = RNE(1/m) and the exact test is
+    // skipped (it runs only for the ~2^-47 fraction of near-midpoint cases).
+    bool safe = false;
+    if (nz == L + 2) {
+        const uint64_t f = ((uint64_t)w.Z[1] << 32) | w.Z[0];
+        const uint64_t half = 1ull << 63;
+        safe = (f > half ? f - half : half - f) > (1ull << 16);
+    }
     const Opd rneg{w.T, L, rexp - 32 * L, -1};
-    const int sigma = warp_sign_sum(zf, rneg, w.G, w.tmp);
+    const int sigma = (safe && !HK_FORCE_EXACT_RECIP) ? 0 : warp_sign_sum(zf, rneg, w.G, w.tmp);
     if (sigma != 0) {
         // is r the power of two 2^(p-1) (binade edge below)?
         bool edge = false;

@@ -34,6 +34,9 @@
 #include <cmath>
 #define HK_DEV inline
 #define HK_HD inline
+struct uint4 {
+    uint32_t x, y, z, w;
+};
 namespace hk {
 HK_DEV int lane() { return hk_emu::cur_lane(); }
 HK_DEV uint32_t ballot(bool p) { return hk_emu::ballot(p); }
@@ -51,6 +54,22 @@ HK_DEV void mac96(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t x, uint32_t
     const uint64_t mid = (uint64_t)a1 + uint32_t(p >> 32) + (lo >> 32);
     a1 = uint32_t(mid);
     a2 += uint32_t(mid >> 32);
+}
+HK_DEV void add96(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t b0, uint32_t b1, uint32_t b2) {
+    const uint64_t lo = (uint64_t)a0 + b0;
+    a0 = uint32_t(lo);
+    const uint64_t mid = (uint64_t)a1 + b1 + (lo >> 32);
+    a1 = uint32_t(mid);
+    a2 += b2 + uint32_t(mid >> 32);
+}
+HK_DEV void mac64(uint64_t& acc, uint32_t& hi, uint32_t x, uint32_t y) {
+    const uint64_t p = (uint64_t)x * y;
+    acc += p;
+    hi += acc < p;
+}
+HK_DEV void mac64x2(uint64_t& acc, uint32_t& hi, uint32_t x0, uint32_t y0, uint32_t x1, uint32_t y1) {
+    mac64(acc, hi, x0, y0);
+    mac64(acc, hi, x1, y1);
 }
 using std::max;
 using std::min;
@@ -72,6 +91,32 @@ HK_DEV void mac96(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t x, uint32_t
         "addc.u32 %2, %2, 0;"
         : "+r"(a0), "+r"(a1), "+r"(a2)
         : "r"(x), "r"(y));
+}
+HK_DEV void add96(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t b0, uint32_t b1, uint32_t b2) {
+    asm("add.cc.u32 %0, %0, %3;\n\t"
+        "addc.cc.u32 %1, %1, %4;\n\t"
+        "addc.u32 %2, %2, %5;"
+        : "+r"(a0), "+r"(a1), "+r"(a2)
+        : "r"(b0), "r"(b1), "r"(b2));
+}
+// 96-bit accumulate with the low 64 bits as ONE 64-bit operand: ptxas keeps the
+// accumulator in a register pair and emits IMAD.WIDE.U32 with carry-out, no moves.
+HK_DEV void mac64(uint64_t& acc, uint32_t& hi, uint32_t x, uint32_t y) {
+    asm("{\n\t.reg .u32 lo, h;\n\tmov.b64 {lo, h}, %0;\n\t"
+        "mad.lo.cc.u32 lo, %2, %3, lo;\n\tmadc.hi.cc.u32 h, %2, %3, h;\n\taddc.u32 %1, %1, 0;\n\t"
+        "mov.b64 %0, {lo, h};\n\t}"
+        : "+l"(acc), "+r"(hi)
+        : "r"(x), "r"(y));
+}
+// Two MACs into one accumulator: the two carry-outs merge into a single
+// ALU-pipe IADD3.X, leaving the IMAD pipe to the IMAD.WIDEs.
+HK_DEV void mac64x2(uint64_t& acc, uint32_t& hi, uint32_t x0, uint32_t y0, uint32_t x1, uint32_t y1) {
+    asm("{\n\t.reg .u32 lo, h;\n\tmov.b64 {lo, h}, %0;\n\t"
+        "mad.lo.cc.u32 lo, %2, %3, lo;\n\tmadc.hi.cc.u32 h, %2, %3, h;\n\taddc.u32 %1, %1, 0;\n\t"
+        "mad.lo.cc.u32 lo, %4, %5, lo;\n\tmadc.hi.cc.u32 h, %4, %5, h;\n\taddc.u32 %1, %1, 0;\n\t"
+        "mov.b64 %0, {lo, h};\n\t}"
+        : "+l"(acc), "+r"(hi)
+        : "r"(x0), "r"(y0), "r"(x1), "r"(y1));
 }
 } // namespace hk
 #endif
@@ -162,21 +207,45 @@ HK_DEV void warp_stage_padded(uint32_t* Bp, const uint32_t* B, int n) {
     for (int i = lane(); i < n + 64; i += 32) Bp[i] = (i >= 32 && i < 32 + n) ? B[i - 32] : 0u;
 }
 
-// P[0 .. nA+nB) = A[0..nA) * B[0..nB) (exact).  A: plain limbs (smem), Bp: the
-// padded staging of B (smem).  Column sums in 96 bits per lane, carries
+// P[tfirst .. nA+nB) = the limbs of sum_{t >= tfirst} colsum_t 2^(32 t), where
+// colsum_t = sum_s A[s] B[t-s].  With tfirst = 0 this is the exact product
+// A[0..nA) * B[0..nB); with tfirst > 0 it is the "short" product that drops the
+// low columns and their carries (the dropped part E satisfies
+// 0 <= E < min(nA,nB) 2^(32 tfirst + 32), see warp_fms).  A: plain limbs (smem),
+// Bp: the padded staging of B (smem).  Column sums in 96 bits per lane, carries
 // resolved per 32-limb group with a running carry / high-word state.
-HK_DEV void warp_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint32_t* P) {
+HK_DEV void warp_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint32_t* P, int tfirst = 0) {
     const int ln = lane();
     const int ntot = nA + nB;
     uint32_t cin = 0, hi_prev = 0, a1p = 0, a2p31 = 0, a2p30 = 0;
-    for (int g0 = 0; g0 < ntot; g0 += 32) {
+    for (int g0 = tfirst; g0 < ntot; g0 += 32) {
         const int t = g0 + ln;
         const int slo = max(0, g0 - (nB - 1));
         const int shi = min(g0 + 31, nA - 1);
-        uint32_t a0 = 0, a1 = 0, a2 = 0;
+        // four independent accumulator chains (s mod 4) break the carry-chain
+        // dependency so a lone warp (reciprocal, B column, L^{-1}) is not
+        // latency-bound; they are folded together after the loop.
+        // Per 8 MACs: 2 warp-uniform LDS.128 for x (broadcast), 8 LDS for y,
+        // 8 IMAD.WIDE.U32 + 4 IADD3.X (SASS checked).  The prologue aligns s so
+        // the x loads are 16-byte vectors (A is 16-byte aligned).
+        uint64_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+        uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
         const uint32_t* yb = Bp + 32 + t;
-#pragma unroll 4
-        for (int s = slo; s <= shi; ++s) mac96(a0, a1, a2, A[s], yb[-s]);
+        int s = slo;
+        for (; s <= shi && (s & 3); ++s) mac64(q0, h0, A[s], yb[-s]);
+        for (; s + 7 <= shi; s += 8) {
+            const uint4 xa = *reinterpret_cast<const uint4*>(A + s);
+            const uint4 xb = *reinterpret_cast<const uint4*>(A + s + 4);
+            mac64x2(q0, h0, xa.x, yb[-s], xb.x, yb[-s - 4]);
+            mac64x2(q1, h1, xa.y, yb[-s - 1], xb.y, yb[-s - 5]);
+            mac64x2(q2, h2, xa.z, yb[-s - 2], xb.z, yb[-s - 6]);
+            mac64x2(q3, h3, xa.w, yb[-s - 3], xb.w, yb[-s - 7]);
+        }
+        for (; s <= shi; ++s) mac64(q0, h0, A[s], yb[-s]);
+        uint32_t a0 = uint32_t(q0), a1 = uint32_t(q0 >> 32), a2 = h0;
+        add96(a0, a1, a2, uint32_t(q1), uint32_t(q1 >> 32), h1);
+        add96(a0, a1, a2, uint32_t(q2), uint32_t(q2 >> 32), h2);
+        add96(a0, a1, a2, uint32_t(q3), uint32_t(q3 >> 32), h3);
         // limb t receives a0(t) + a1(t-1) + a2(t-2)
         uint32_t a1m1 = shfl_up(a1, 1);
         uint32_t a2m2 = shfl_up(a2, 2);
@@ -207,11 +276,42 @@ struct RMeta {
     int sign; // -1, 0, +1
 };
 
+constexpr int kExact = -0x40000000; // "no uncertainty" for warp_round_sum's ubit
+
+// Range statistics of bits [lo, hi] (relative positions, lo <= hi) of d[0..n):
+// returns bit0 = any bit set, bit1 = all bits set.  Warp-uniform.
+HK_DEV int warp_bit_range(const uint32_t* d, int n, int lo, int hi) {
+    bool any = false, all = true;
+    const int ql = lo >> 5, qh = hi >> 5;
+    for (int q0 = ql; q0 <= qh; q0 += 32) {
+        const int idx = q0 + lane();
+        const bool in = idx <= qh;
+        uint32_t mask = 0;
+        if (in) {
+            const int s = lo - 32 * idx > 0 ? lo - 32 * idx : 0;
+            const int e = hi - 32 * idx < 31 ? hi - 32 * idx : 31;
+            mask = (e == 31 ? 0xffffffffu : ((1u << (e + 1)) - 1u)) & ~((1u << s) - 1u);
+        }
+        const uint32_t v = (in && idx < n) ? d[idx] : 0u;
+        any |= ballot((v & mask) != 0u) != 0u;
+        all &= ballot(in && (v & mask) != mask) == 0u;
+    }
+    return (any ? 1 : 0) | (all ? 2 : 0);
+}
+
 // out[0..nout) = RNE_{32 nout}(X + Y).  G is a smem scratch window of at least
 // max(X.n, Y.n, nout) + 4 limbs that must not alias X, Y or out.  X or Y may
 // alias `out` (all operand reads finish before the first write).
-HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_t* out, int nout) {
+//
+// Ziv mode (ubit != kExact): the true value is X + Y + delta with |delta| <
+// 2^ubit (absolute bit position) of unknown sign.  If no rounding midpoint can
+// lie within that distance, the correctly rounded result of the true value is
+// RNE(X + Y): it is written and *ok = true.  Otherwise nothing is written and
+// *ok = false (the caller recomputes exactly).
+HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_t* out, int nout,
+                            int ubit = kExact, bool* ok = nullptr) {
     const int ln = lane();
+    if (ok) *ok = true;
     const int blX = Xin.sign ? warp_bitlen(Xin.d, Xin.n) : 0;
     const int blY = Yin.sign ? warp_bitlen(Yin.d, Yin.n) : 0;
     if (blX == 0 && blY == 0) {
@@ -268,6 +368,10 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
     wsync();
     const int bl = warp_bitlen(G, W + 1);
     if (bl == 0) {
+        if (ubit != kExact) { // X + Y = 0 exactly but the true value is a tiny delta
+            *ok = false;
+            return RMeta{0, 0};
+        }
         for (int i = ln; i < nout; i += 32) out[i] = 0u;
         wsync();
         return RMeta{0, 0};
@@ -279,6 +383,24 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
     if (lsbpos - 1 >= 0) {
         rb = (G[(lsbpos - 1) >> 5] >> ((lsbpos - 1) & 31)) & 1u;
         st = warp_any_below(G, W + 1, lsbpos - 1);
+    }
+    if (ubit != kExact) {
+        // distance of |X+Y| to the nearest rounding midpoint must exceed the
+        // uncertainty: with the round bit set the bits below must not all be 0,
+        // with it clear they must not all be 1 (down to the uncertain position;
+        // the sticky limb [0,32) counts as uncertain).
+        const int rb_rel = lsbpos - 1;
+        int u_rel = ubit - (base - 32);
+        if (u_rel < 32) u_rel = 32;
+        bool safe = rb_rel - u_rel >= 4;
+        if (safe) {
+            const int rs = warp_bit_range(G, W + 1, u_rel, rb_rel - 1);
+            safe = rb ? (rs & 1) != 0 : (rs & 2) == 0;
+        }
+        if (!safe) {
+            *ok = false;
+            return RMeta{0, 0};
+        }
     }
     const uint32_t low0 = opd_word(Gw, lsbpos);
     const bool inc = rb && (st || (low0 & 1u));

@@ -36,9 +36,10 @@ def test_emulated_ops_match_model(emu_bin, L):
         for (x, y), r in zip(pairs, run(emu_bin, lines)):
             assert from_line(r, L) == fn(x, y, p)
     ds = [rnd(L, rng) for _ in range(40)]
-    lines = [f"op recip {L} {len(ds)}"] + [to_line(d, L) for d in ds]
-    for d, r in zip(ds, run(emu_bin, lines)):
-        assert from_line(r, L) == F.recip(d, p)
+    for op in ("recip", "recipx"):  # recipx: exact midpoint test forced on every call
+        lines = [f"op {op} {L} {len(ds)}"] + [to_line(d, L) for d in ds]
+        for d, r in zip(ds, run(emu_bin, lines)):
+            assert from_line(r, L) == F.recip(d, p)
 
 
 @pytest.mark.parametrize("beta,N,L,m", [((1, 2), 8, 4, 4), ((1, 1), 12, 3, 5), ((1, 3), 6, 8, 6),

@@ -155,12 +155,15 @@ def test_c3_parity_vs_reference(api):
 
 
 def test_c2_closed_form_pivots(api):
-    """beta = 1: d_n = (n!)^2 exactly — independent of the reference."""
+    """beta = 1: d_n = (n!)^2 — independent of the reference.  The
+    p-bit float path rounds every op, so agreement is to the north_star tolerance."""
+    from fractions import Fraction
+
     n, L = 256, 192
     with run_path(api, (1, 1), n, L, 8) as ctx:
         D = ctx.D()
-        for i in range(n):
-            assert D.to_fraction(i) == math.factorial(i) ** 2
+        worst = max(abs(D.to_fraction(i) / math.factorial(i) ** 2 - 1) for i in range(n))
+        assert worst < Fraction(1, 10**20), float(worst)
 
 
 # ------------------------------------------------------------------ reference test mirrors and edge cases

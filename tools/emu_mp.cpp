@@ -69,6 +69,7 @@ int main() {
             std::cin >> op >> L >> cnt;
             HostArr A(cnt, L), B(cnt, L), C(cnt, L), O(cnt, L);
             int code = op == "fms" ? 0 : op == "mul" ? 1 : op == "add" ? 2 : 3;
+            hk::force_exact_recip() = (op == "recipx"); // recip with the exact midpoint test forced
             for (long long e = 0; e < cnt; ++e) {
                 if (code == 0) {
                     read_opd(C, e, L);
@@ -99,7 +100,7 @@ int main() {
                 if (err >= 0) break;
                 const int nb = N - i - 1;
                 run_items(nb, ws, ItemMulB{S.view(), R.view(), Bq.view(), N, L, i, &err});
-                run_items((long long)nb * (nb + 1) / 2, ws, ItemTrailing{S.view(), Bq.view(), N, L, i, &err});
+                run_items((long long)nb * (nb + 1) / 2, ws, ItemTrailing{S.view(), Bq.view(), N, L, i, i + 1, &err});
                 run_items(nb, ws, ItemStoreL{S.view(), Bq.view(), N, L, i});
             }
             if (err < 0) {
