@@ -23,7 +23,7 @@ build/host_math.o: $(CSRC)/host_math.cpp | build
 	$(CXX) -std=c++20 -O2 -fPIC -Wall -c $< -o $@
 
 $(LIB): build/hk_api.o build/host_math.o
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl
 
 build/emu_mp: tools/emu_mp.cpp $(HDRS) $(CSRC)/warp_emu.h | build
 	$(CXX) -std=c++20 -O2 -pthread -Wall -Wno-unknown-pragmas -o $@ $<

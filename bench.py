@@ -13,9 +13,10 @@ that runs in seconds (configs[0] = C1 is the CPU-runnable oracle case).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c5]
 
-N > 1 is launched by torchrun (one rank per GPU).  The path is not sharded
-across GPUs yet in this round: every rank runs an independent replica of the
-workload ("replicas", weak scaling); timing is the max over ranks.
+N > 1 is launched by torchrun (one rank per GPU): the LDLT is column-sharded
+across the ranks (boustrophedon ownership, ncclBroadcast of the pivot column
+each step, gather to rank 0 for L^{-1}/block/eigen) — the same job split over
+N GPUs (strong scaling); timing is the max over ranks.
 """
 from __future__ import annotations
 
@@ -30,6 +31,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 
 CONFIGS = {  # BASELINE.json configs
     "c1": dict(beta=(1, 2), n=64, p=3072, k=8, K_ref=2048),
@@ -138,7 +140,7 @@ def workload_config(args, cfg, world):
     b = cfg["beta"]
     return {"workload": f"{args.config.upper()}: beta={b[0]}/{b[1]} Hankel N={cfg['n']}, p={cfg['p']} bits, "
                         f"k={cfg['k']} -> lambda_min", "n": cfg["n"], "p_bits": cfg["p"], "k": cfg["k"],
-            "beta": f"{b[0]}/{b[1]}", "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "beta": f"{b[0]}/{b[1]}", "parallelism": f"column-sharded LDLT x{world} GPUs (NCCL pivot-column broadcast)" if world > 1 else "1 GPU",
             "l2": "256 MB L2 flush before every timed step (C2 working set 25 MB would fit L2)"}
 
 
@@ -158,7 +160,16 @@ def bench_ours(args, cfg):
     s = min(3, min(k, n))
     mu, exact = api.build_hankel(cfg["beta"], n, L)
     assert exact, "moments must be exact at this precision"
-    ctx = api.Context(L, device=local)
+    if world > 1 or args.sharded:  # column-sharded LDLT over NCCL (hk_create_sharded), results on rank 0
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = api.Context(L, device=local, rank=rank, world=world, nccl_id=obj[0])
+    else:
+        ctx = api.Context(L, device=local)
     ext = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")
 
@@ -167,6 +178,8 @@ def bench_ours(args, cfg):
 
     def step():
         ctx.decompose()
+        if rank != 0:
+            return [float("nan")], [0.0], [0.0]
         ctx.invert_L_partial(min(k, n))
         ctx.assemble_truncated_inverse(min(k, n))
         return ctx.smallest_eigs_of_H(s)
@@ -197,7 +210,7 @@ def bench_ours(args, cfg):
         t = torch.tensor([ms], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * fmas(n) / (ms * 1e-3)
+    value = fmas(n) / (ms * 1e-3)  # one job split over `world` GPUs (strong scaling)
 
     # ---- e2e: the public API call with host buffers (pinned), H2D + D2H inside the timed region
     import numpy as np
@@ -233,25 +246,29 @@ def bench_ours(args, cfg):
     d2h = kk * kk * (4 * L + 8) + 3 * 3 * 8
 
     # ---- roofline of the dominant kernel (trailing update), instrumented eager run
-    prof, n_tr = ctx.profile_ldlt()
+    if rank == 0:  # eager single-GPU instrumented run on rank 0 (no communication)
+        prof, n_tr = ctx.profile_ldlt()
+    else:
+        prof, n_tr = {"trailing": 1.0, "total": 1.0}, 1
     ms_tr, ms_ldlt = prof["trailing"], prof["total"]
     alg_macs = fmas(n) * L * L  # L^2 limb-MACs per MP-FMA
     achieved = alg_macs / (ms_tr * 1e-3) / 1e12
     peak = api.peak_imad(local) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_trailing_{args.config}.json")
-    if os.path.exists(prof):
-        traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+    ncu_file = os.path.join(ROOT, "profiles", f"ncu_trailing_{args.config}.json")
+    if os.path.exists(ncu_file):
+        traffic = json.load(open(ncu_file)).get("dram_bytes_per_launch")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
         "dtype": f"mp{p} (p-bit binary float, 32-bit limbs, RNE; integer limb arithmetic)",
         "data": "exact-integer moments (deterministic, no dataset)",
         "config": workload_config(args, cfg, world),
         "time_to_lambda_ms": ms,
         "lambda_min": repr(lam[0][0] + lam[1][0]),
-        "e2e": {"value": world * fmas(n) / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        "e2e": {"value": fmas(n) / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "roofline": {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "Tlimb-MAC/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -279,7 +296,7 @@ def bench_ours(args, cfg):
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     return 0
 
@@ -292,6 +309,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the NCCL column-sharded path even on 1 GPU")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

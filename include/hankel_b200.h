@@ -134,6 +134,22 @@ int hk_profile_ldlt(hk_ctx* ctx, double* ms5, long long* n_trailing);
  * over all SMs).  The roofline denominator for the IMAD path. */
 int hk_peak_imad(int device, double* limb_macs_per_s);
 
+/* ---- multi-GPU (one process per GPU) --------------------------
+ * decompose_parallel's worker split (ldlt.hpp:97-99; W threads + slot channel,
+ * ldlt.cpp:137-395) becomes `world` GPUs: rank r owns the columns
+ * assign_columns(n, world) gives it, the pivot column is ncclBroadcast from its
+ * owner every step, and after the factorisation the columns are gathered to
+ * rank 0, which runs L^{-1} / block / eigen.  Results are bit-identical for any
+ * world size.  hk_nccl_unique_id on rank 0, shared by the caller (e.g. over
+ * torch.distributed), then hk_create_sharded on every rank (collective).
+ * With nccl_id128 == NULL all `world` ranks are emulated inside this one
+ * context on one device (broadcast = device-to-device copy): the sharded
+ * kernels and maps, testable on a single GPU; rank must then be 0.
+ * On ranks != 0, hk_compute returns HK_OK with *s_out = 0 (no lambdas). */
+int hk_nccl_unique_id(void* out128);
+int hk_create_sharded(int device, int limbs, int rank, int world, const void* nccl_id128, hk_ctx** out);
+int hk_world(const hk_ctx* ctx, int* rank, int* world);
+
 /* Balanced round-robin (boustrophedon) ownership map, assign_columns
  * (ldlt.cpp:22-35): owner[c] for c < n. */
 int hk_assign_columns(int n, int workers, int32_t* owner);

@@ -66,6 +66,9 @@ def lib():
             "hk_stream": (vp, [vp]),
             "hk_profile_ldlt": (C.c_int, [vp, f64p, C.POINTER(C.c_longlong)]),
             "hk_peak_imad": (C.c_int, [C.c_int, f64p]),
+            "hk_nccl_unique_id": (C.c_int, [C.c_char_p]),
+            "hk_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]),
+            "hk_world": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -181,17 +184,36 @@ class RunRecord:
     d2h_s: float = 0.0
 
 
-class Context:
-    """One device context at p = 32*limbs bits (hk_create / hk_destroy)."""
+def nccl_unique_id() -> bytes:
+    """ncclUniqueId (128 bytes) for hk_create_sharded; make it on rank 0 and share it."""
+    buf = C.create_string_buffer(128)
+    if lib().hk_nccl_unique_id(buf) != HK_OK:
+        raise RuntimeError("hk_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.raw
 
-    def __init__(self, limbs: int, device: int = 0):
+
+class Context:
+    """One device context at p = 32*limbs bits (hk_create / hk_destroy).
+
+    world > 1 (or virtual=True) selects the column-sharded LDLT
+    (hk_create_sharded): with `nccl_id` one process per GPU over NCCL, with
+    virtual=True all `world` ranks emulated on this one device."""
+
+    def __init__(self, limbs: int, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 virtual: bool = False):
         self.L = limbs
         h = C.c_void_p()
-        rc = lib().hk_create(device, limbs, C.byref(h))
+        if world > 1 or virtual or nccl_id is not None:
+            if nccl_id is None and not virtual:
+                raise ValueError("world > 1 needs an nccl_id (or virtual=True)")
+            rc = lib().hk_create_sharded(device, limbs, rank, world, nccl_id, C.byref(h))
+        else:
+            rc = lib().hk_create(device, limbs, C.byref(h))
         if rc != HK_OK:
             raise RuntimeError(f"hk_create failed with status {rc} (CUDA device {device} unavailable?)")
         self.h = h
         self.n = 0
+        self.rank, self.world = rank, world
 
     def close(self):
         if self.h:

@@ -12,6 +12,8 @@
 #include "hk_items.cuh"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h> // types only; libnccl.so.2 is dlopen'ed (multi-GPU section)
 
 #include <chrono>
 #include <cstdio>
@@ -95,6 +97,22 @@ struct hk_ctx {
     const void* graph_bufs[3] = {nullptr, nullptr, nullptr}; // S, R, B the graphs were captured on
     std::vector<uint32_t> h_limbs;
     std::vector<int32_t> h_e, h_s;
+    // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
+    struct Shard {
+        int rank = 0;
+        std::vector<int> owned;       // global columns owned, ascending
+        std::vector<long long> off;   // local entry offset of each owned column (+ total)
+        std::vector<int> loc;         // global column -> local index, -1 if not owned
+        DevArr S, panel, R, B;
+        int* d_erow = nullptr;
+        int* d_ecol = nullptr;
+        int* d_err = nullptr;
+    };
+    int world = 1, rank = 0;
+    bool virt = false;               // all `world` ranks emulated in this one context
+    void* nccl_comm = nullptr;       // ncclComm_t (one rank per process)
+    std::vector<Shard> shards;
+    std::vector<int> owner;          // assign_columns(n, world)
 };
 
 namespace {
@@ -260,6 +278,8 @@ int check_pivots(hk_ctx* c) {
     return HK_OK;
 }
 
+int dist_ldlt(hk_ctx* c); // multi-GPU factorisation (below)
+
 } // namespace
 
 extern "C" {
@@ -303,6 +323,17 @@ void hk_destroy(hk_ctx* c) {
     cudaSetDevice(c->device);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M}) a->release();
+    for (auto& s : c->shards) {
+        for (DevArr* a : {&s.S, &s.panel, &s.R, &s.B}) a->release();
+        if (s.d_erow) cudaFree(s.d_erow);
+        if (s.d_ecol) cudaFree(s.d_ecol);
+        if (s.d_err) cudaFree(s.d_err);
+    }
+    if (c->nccl_comm) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        auto destroy = h ? (int (*)(void*))dlsym(h, "ncclCommDestroy") : nullptr;
+        if (destroy) destroy(c->nccl_comm);
+    }
     if (c->d_err) cudaFree(c->d_err);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -344,6 +375,7 @@ int hk_load_moments(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps
 int hk_ldlt(hk_ctx* c) {
     return guarded(c, [&] {
         if (c->n < 1) return fail(c, HK_ERR_INVALID, "hk_ldlt: no moments loaded");
+        if (c->world > 1 || c->virt || c->nccl_comm) return dist_ldlt(c);
         const int N = c->n, L = c->L;
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
@@ -517,6 +549,11 @@ int hk_compute(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, con
     const int s = kk < 3 ? kk : 3;   // pipeline.cpp:64
     int rc = hk_load_moments(c, n, limbs, exps, signs);
     if (rc == HK_OK) rc = hk_ldlt(c);
+    if (rc == HK_OK && c->rank != 0) { // results live on rank 0 (columns gathered there)
+        if (s_out) *s_out = 0;
+        c->t[0] = now_s() - t0;
+        return HK_OK;
+    }
     if (rc == HK_OK) rc = hk_invert_L_partial(c, kk);
     if (rc == HK_OK) rc = hk_assemble_block(c, kk);
     if (rc == HK_OK) rc = hk_smallest_eigs(c, s, lambda_hi, lambda_lo, trunc_err);
@@ -686,6 +723,312 @@ int hk_peak_imad(int device, double* out) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return HK_ERR_RUNTIME;
     *out = best;
+    return HK_OK;
+}
+
+} // extern "C"
+
+// ====================================================================== multi-GPU
+//
+// Column-sharded LDLT: rank r owns columns {c : owner[c] == r} of
+// the boustrophedon map (ldlt.cpp:22-35).  Per step i (eager, one stream):
+//   U(i)     every rank: step-i update of its owned columns j >= i+1 (panel_i, B_i)
+//   STORE(i) owner(i): column i <- B_i (L in place)
+//   PUBLISH  owner(i+1): panel <- column i+1; ncclBroadcast(panel, root = owner(i+1))
+//            (ldlt.cpp:294-298 publish / 248 wait_complete)
+//   every rank: R_{i+1} = recip(panel[0]), B_{i+1} = panel * R_{i+1} — the
+//            identical deterministic kernels, so no second broadcast (B never
+//            travels; the reference's BroadcastPolicy chunking is moot).
+// Then all columns are gathered to rank 0 (ncclSend/Recv), which runs L^{-1},
+// the block and the eigensolve exactly as on one GPU.  Every op is correctly
+// rounded, so results are bit-identical for any world size.
+// Virtual mode runs all ranks' shards in one process on one GPU with the
+// broadcast / gather as device-to-device copies (tests the sharded kernels and
+// index maps on a single B200).
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*GetErrorString)(ncclResult_t);
+};
+
+// libnccl.so.2 is dlopen'ed: inside a torch process this resolves to the NCCL
+// torch already loaded (same SONAME), standalone to the system one.
+NcclApi* nccl_api() {
+    static NcclApi api;
+    static bool tried = false, ok = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            ok = (api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId")) &&
+                 (api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank")) &&
+                 (api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy")) &&
+                 (api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast")) &&
+                 (api.Send = (decltype(api.Send))dlsym(h, "ncclSend")) &&
+                 (api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv")) &&
+                 (api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart")) &&
+                 (api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd")) &&
+                 (api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString"));
+        }
+    }
+    return ok ? &api : nullptr;
+}
+
+void nk(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw HkError{HK_ERR_RUNTIME, std::string(what) + ": " + (nccl_api() ? nccl_api()->GetErrorString(r) : "?")};
+}
+
+using Shard = hk_ctx::Shard;
+
+void shard_setup(hk_ctx* c, Shard& s, int N) {
+    s.owned.clear();
+    s.loc.assign(size_t(N), -1);
+    s.off.assign(1, 0);
+    std::vector<int> erow, ecol;
+    for (int j = 0; j < N; ++j) {
+        if (c->owner[size_t(j)] != s.rank) continue;
+        s.loc[size_t(j)] = int(s.owned.size());
+        s.owned.push_back(j);
+        for (int k = j; k < N; ++k) {
+            erow.push_back(k);
+            ecol.push_back(j);
+        }
+        s.off.push_back((long long)erow.size());
+    }
+    const long long tot = (long long)erow.size();
+    s.S.ensure(tot > 0 ? tot : 1, c->L);
+    s.panel.ensure(N, c->L);
+    s.R.ensure(N, c->L);
+    s.B.ensure(N, c->L);
+    if (s.d_erow) cudaFree(s.d_erow);
+    if (s.d_ecol) cudaFree(s.d_ecol);
+    ck(cudaMalloc(&s.d_erow, size_t(tot > 0 ? tot : 1) * sizeof(int)), "malloc erow");
+    ck(cudaMalloc(&s.d_ecol, size_t(tot > 0 ? tot : 1) * sizeof(int)), "malloc ecol");
+    if (tot > 0) {
+        ck(cudaMemcpyAsync(s.d_erow, erow.data(), size_t(tot) * sizeof(int), cudaMemcpyHostToDevice, c->st), "H2D erow");
+        ck(cudaMemcpyAsync(s.d_ecol, ecol.data(), size_t(tot) * sizeof(int), cudaMemcpyHostToDevice, c->st), "H2D ecol");
+    }
+    if (!s.d_err) ck(cudaMalloc(&s.d_err, sizeof(int)), "malloc err");
+    ck(cudaMemsetAsync(s.d_err, 0xff, sizeof(int), c->st), "memset err");
+    ck(cudaStreamSynchronize(c->st), "sync");
+}
+
+// entries of `s` belonging to owned columns >= j0 form a suffix of the local storage
+long long suffix_start(const Shard& s, int j0) {
+    size_t q = 0;
+    while (q < s.owned.size() && s.owned[q] < j0) ++q;
+    return s.off[q];
+}
+
+// make every shard's panel hold column `col` rows col..N-1 (N - col entries)
+void publish(hk_ctx* c, int col) {
+    const int N = c->n, L = c->L, root = c->owner[size_t(col)];
+    const long long cnt = N - col;
+    if (c->virt) {
+        Shard& o = c->shards[size_t(root)];
+        const long long src = o.off[size_t(o.loc[size_t(col)])];
+        launch(c, hk::ItemCopy{o.panel.view(), o.S.view(), 0, src, L}, cnt, 64);
+        for (auto& s : c->shards) {
+            if (s.rank == root) continue;
+            ck(cudaMemcpyAsync(s.panel.d, o.panel.d, size_t(cnt) * L * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st),
+               "panel copy");
+            ck(cudaMemcpyAsync(s.panel.m, o.panel.m, size_t(cnt) * sizeof(Meta), cudaMemcpyDeviceToDevice, c->st),
+               "panel meta copy");
+        }
+        return;
+    }
+    Shard& s = c->shards[0];
+    if (s.rank == root) {
+        const long long src = s.off[size_t(s.loc[size_t(col)])];
+        launch(c, hk::ItemCopy{s.panel.view(), s.S.view(), 0, src, L}, cnt, 64);
+    }
+    NcclApi* A = nccl_api();
+    ncclComm_t comm = (ncclComm_t)c->nccl_comm;
+    nk(A->GroupStart(), "group start");
+    nk(A->Broadcast(s.panel.d, s.panel.d, size_t(cnt) * L, ncclUint32, root, comm, c->st), "bcast limbs");
+    nk(A->Broadcast(s.panel.m, s.panel.m, size_t(cnt) * 2, ncclInt32, root, comm, c->st), "bcast meta");
+    nk(A->GroupEnd(), "group end");
+}
+
+void derive(hk_ctx* c, Shard& s, int i) {
+    const int N = c->n, L = c->L;
+    launch(c, hk::ItemDRecip{s.panel.view(), s.R.view(), L, i, s.d_err}, 1, ws_recip_words(L));
+    if (N - i - 1 > 0)
+        launch(c, hk::ItemDMulB{s.panel.view(), s.R.view(), s.B.view(), L, i, s.d_err}, N - i - 1, ws_op_words(L));
+}
+
+// gather all columns into the standard jagged S on rank 0 (+ R)
+void gather_to_root(hk_ctx* c) {
+    const int N = c->n, L = c->L;
+    const long long ntri = (long long)N * (N + 1) / 2;
+    if (c->rank == 0) {
+        c->S.ensure(ntri, L);
+        c->R.ensure(N, L);
+    }
+    if (c->virt) {
+        for (int j = 0; j < N; ++j) {
+            Shard& o = c->shards[size_t(c->owner[size_t(j)])];
+            const long long src = o.off[size_t(o.loc[size_t(j)])], dst = hk::tri_idx(j, j, N), cnt = N - j;
+            ck(cudaMemcpyAsync(c->S.d + dst * L, o.S.d + src * L, size_t(cnt) * L * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, c->st), "gather");
+            ck(cudaMemcpyAsync(c->S.m + dst, o.S.m + src, size_t(cnt) * sizeof(Meta), cudaMemcpyDeviceToDevice, c->st),
+               "gather meta");
+        }
+        Shard& s0 = c->shards[0];
+        ck(cudaMemcpyAsync(c->R.d, s0.R.d, size_t(N) * L * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st), "R");
+        ck(cudaMemcpyAsync(c->R.m, s0.R.m, size_t(N) * sizeof(Meta), cudaMemcpyDeviceToDevice, c->st), "R meta");
+        return;
+    }
+    Shard& s = c->shards[0];
+    NcclApi* A = nccl_api();
+    ncclComm_t comm = (ncclComm_t)c->nccl_comm;
+    const int batch = 128;
+    for (int j0 = 0; j0 < N; j0 += batch) {
+        nk(A->GroupStart(), "group start");
+        for (int j = j0; j < N && j < j0 + batch; ++j) {
+            const int o = c->owner[size_t(j)];
+            const long long cnt = N - j;
+            if (c->rank == 0) {
+                const long long dst = hk::tri_idx(j, j, N);
+                if (o == 0) {
+                    const long long src = s.off[size_t(s.loc[size_t(j)])];
+                    ck(cudaMemcpyAsync(c->S.d + dst * L, s.S.d + src * L, size_t(cnt) * L * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToDevice, c->st), "gather");
+                    ck(cudaMemcpyAsync(c->S.m + dst, s.S.m + src, size_t(cnt) * sizeof(Meta), cudaMemcpyDeviceToDevice,
+                                       c->st), "gather meta");
+                } else {
+                    nk(A->Recv(c->S.d + dst * L, size_t(cnt) * L, ncclUint32, o, comm, c->st), "recv");
+                    nk(A->Recv(c->S.m + dst, size_t(cnt) * 2, ncclInt32, o, comm, c->st), "recv meta");
+                }
+            } else if (o == c->rank) {
+                const long long src = s.off[size_t(s.loc[size_t(j)])];
+                nk(A->Send(s.S.d + src * L, size_t(cnt) * L, ncclUint32, 0, comm, c->st), "send");
+                nk(A->Send(s.S.m + src, size_t(cnt) * 2, ncclInt32, 0, comm, c->st), "send meta");
+            }
+        }
+        nk(A->GroupEnd(), "group end");
+    }
+    if (c->rank == 0) {
+        ck(cudaMemcpyAsync(c->R.d, s.R.d, size_t(N) * L * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st), "R");
+        ck(cudaMemcpyAsync(c->R.m, s.R.m, size_t(N) * sizeof(Meta), cudaMemcpyDeviceToDevice, c->st), "R meta");
+    }
+}
+
+int dist_ldlt(hk_ctx* c) {
+    const int N = c->n, L = c->L;
+    c->owner.assign(size_t(N), 0);
+    hk_assign_columns(N, c->world, c->owner.data());
+    for (auto& s : c->shards) shard_setup(c, s, N);
+    const int wo = ws_op_words(L);
+    ck(cudaEventRecord(c->ev[0], c->st), "event");
+    for (auto& s : c->shards) {
+        const long long tot = s.off.back();
+        launch(c, hk::ItemDInit{s.S.view(), c->mu.view(), s.d_erow, s.d_ecol, L}, tot, 64);
+    }
+    publish(c, 0);
+    for (auto& s : c->shards) derive(c, s, 0);
+    for (int i = 0; i < N; ++i) {
+        for (auto& s : c->shards) {
+            const long long e0 = suffix_start(s, i + 1), n = s.off.back() - e0;
+            launch(c, hk::ItemDTrailing{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0, s.d_err},
+                   n, wo);
+            if (c->owner[size_t(i)] == s.rank && N - i - 1 > 0) {
+                const long long dst = s.off[size_t(s.loc[size_t(i)])] + 1;
+                launch(c, hk::ItemCopy{s.S.view(), s.B.view(), dst, i + 1, L}, N - i - 1, 64);
+            }
+        }
+        if (i + 1 < N) {
+            publish(c, i + 1);
+            for (auto& s : c->shards) derive(c, s, i + 1);
+        }
+    }
+    // pivot errors: every rank computed the same reciprocals, so the flags agree
+    int bad = -1;
+    for (auto& s : c->shards) {
+        int e = -1;
+        ck(cudaMemcpyAsync(&e, s.d_err, sizeof(int), cudaMemcpyDeviceToHost, c->st), "D2H err");
+        ck(cudaStreamSynchronize(c->st), "sync");
+        if (e >= 0 && (bad < 0 || e < bad)) bad = e;
+    }
+    if (bad >= 0) {
+        c->bad_col = bad;
+        c->factored = false;
+        return fail(c, HK_ERR_PRECISION,
+                    "LDLT pivot <= 0 at column " + std::to_string(bad) + ": matrix not positive definite at p=" +
+                        std::to_string(32 * L) + " bits, increase the precision");
+    }
+    gather_to_root(c);
+    ck(cudaEventRecord(c->ev[1], c->st), "event");
+    ck(cudaEventSynchronize(c->ev[1]), "sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
+    c->t[1] = ms * 1e-3;
+    c->factored = c->rank == 0;
+    c->inverted = c->assembled = false;
+    return HK_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int hk_nccl_unique_id(void* out128) {
+    NcclApi* A = nccl_api();
+    if (!A || !out128) return HK_ERR_RUNTIME;
+    ncclUniqueId id;
+    if (A->GetUniqueId(&id) != ncclSuccess) return HK_ERR_RUNTIME;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out128, &id, 128);
+    return HK_OK;
+}
+
+int hk_create_sharded(int device, int limbs, int rank, int world, const void* nccl_id128, hk_ctx** out) {
+    if (!out || world < 1 || rank < 0 || rank >= world) return HK_ERR_INVALID;
+    const int rc = hk_create(device, limbs, out);
+    if (rc != HK_OK) return rc;
+    hk_ctx* c = *out;
+    c->world = world;
+    c->rank = rank;
+    c->virt = nccl_id128 == nullptr;
+    const int r2 = guarded(c, [&] {
+        if (c->virt) {
+            if (rank != 0) return fail(c, HK_ERR_INVALID, "virtual mode emulates all ranks: rank must be 0");
+            c->shards.resize(size_t(world));
+            for (int r = 0; r < world; ++r) c->shards[size_t(r)].rank = r;
+        } else {
+            NcclApi* A = nccl_api();
+            if (!A) return fail(c, HK_ERR_RUNTIME, "libnccl.so.2 not loadable");
+            ncclUniqueId id;
+            memcpy(&id, nccl_id128, 128);
+            ncclComm_t comm;
+            nk(A->CommInitRank(&comm, world, id, rank), "ncclCommInitRank");
+            c->nccl_comm = comm;
+            c->shards.resize(1);
+            c->shards[0].rank = rank;
+        }
+        return HK_OK;
+    });
+    if (r2 != HK_OK) {
+        hk_destroy(c);
+        *out = nullptr;
+    }
+    return r2;
+}
+
+int hk_world(const hk_ctx* c, int* rank, int* world) {
+    if (!c) return HK_ERR_INVALID;
+    if (rank) *rank = c->rank;
+    if (world) *world = c->world;
     return HK_OK;
 }
 

@@ -263,6 +263,88 @@ struct ItemBlockOut {
     }
 };
 
+// ======================================================================
+// Sharded (multi-GPU) LDLT: rank r stores only the columns it owns under the
+// boustrophedon map (ldlt.cpp:22-35), concatenated; entry e of the local
+// storage is (row erow[e], column ecol[e]).  The pivot column i is held by
+// every rank in `panel` (rows i..N-1 at panel[0..N-i)), published by its owner
+// each step (ldlt.cpp:294-298 / 248 -> ncclBroadcast).
+
+// local S <- Hankel(mu)
+struct ItemDInit {
+    MpArr S, mu;
+    const int* erow;
+    const int* ecol;
+    int L;
+    HK_DEV void operator()(long long e, uint32_t*) const {
+        const int k = erow[e], j = ecol[e];
+        copy_entry(S.limbs(e, L), S.m + e, mu.limbs(k + j, L), mu.m + (k + j), L);
+    }
+};
+
+// step-i update of local entries [e0, e0 + n): S(k,j) -= panel_i(j) B_i(k)
+struct ItemDTrailing {
+    MpArr S, panel, B;
+    const int* erow;
+    const int* ecol;
+    int L, i;
+    long long e0;
+    const int* err;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const long long e = e0 + w;
+        const int k = erow[e], j = ecol[e];
+        uint32_t* c = S.limbs(e, L);
+        const Meta r = warp_fms(c, S.m[e], panel.limbs(j - i, L), panel.m[j - i], B.limbs(k, L), B.m[k], c, L,
+                                opws_carve(ws, L));
+        if (lane() == 0) S.m[e] = r;
+        wsync();
+    }
+};
+
+// R_i = RNE(1/panel[0]) with the pivot test
+struct ItemDRecip {
+    MpArr panel, R;
+    int L, i;
+    int* err;
+    HK_DEV void operator()(long long, uint32_t* ws) const {
+        if (*(volatile int*)err >= 0) return;
+        const Meta dm = panel.m[0];
+        if (dm.sign <= 0) {
+            if (lane() == 0) ItemRecip::atomicCAS_emu(err, i);
+            return;
+        }
+        const Meta r = warp_recip(panel.limbs(0, L), dm, R.limbs(i, L), L, recipws_carve(ws, L));
+        if (lane() == 0) R.m[i] = r;
+        wsync();
+    }
+};
+
+// B_i(k) = RNE(panel_i(k) R_i), k = i+1+t
+struct ItemDMulB {
+    MpArr panel, R, B;
+    int L, i;
+    const int* err;
+    HK_DEV void operator()(long long t, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int k = i + 1 + int(t);
+        const Meta r = warp_mulr(panel.limbs(k - i, L), panel.m[k - i], R.limbs(i, L), R.m[i], B.limbs(k, L), L,
+                                 opws_carve(ws, L));
+        if (lane() == 0) B.m[k] = r;
+        wsync();
+    }
+};
+
+// contiguous entry copy dst[d0 + t] <- src[s0 + t]
+struct ItemCopy {
+    MpArr dst, src;
+    long long d0, s0;
+    int L;
+    HK_DEV void operator()(long long t, uint32_t*) const {
+        copy_entry(dst.limbs(d0 + t, L), dst.m + d0 + t, src.limbs(s0 + t, L), src.m + s0 + t, L);
+    }
+};
+
 // ---- generic batch ops (parity tests of the arithmetic itself)
 struct ItemBatch {
     MpArr A, B, C, O;

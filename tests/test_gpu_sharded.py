@@ -1,0 +1,83 @@
+"""GPU: the column-sharded (multi-GPU) LDLT path.  Only one GPU is available to
+the tests, so (a) all ranks are emulated in one context on one device
+(virtual mode: the broadcast / gather become device-to-device copies, the
+sharded kernels and index maps are the real ones) and (b) a real NCCL
+communicator of world size 1 exercises the ncclBroadcast / ncclSend / ncclRecv
+calls.  Results must be bit-identical to the single-GPU path (every op is
+correctly rounded), as the reference requires across worker counts
+(ldlt.hpp:92-96, test_ldlt.cpp:147-154, acceptance.cpp:176-218)."""
+import json
+import os
+
+import pytest
+
+from tests.mpf_helpers import from_arr
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1810_01478_b200 import api as a
+
+    return a
+
+
+def results(ctx, mu, k):
+    rec = ctx.compute(mu, k)
+    return rec, from_arr(ctx.D()), from_arr(ctx.Linv()), from_arr(ctx.block())
+
+
+@pytest.fixture(scope="module")
+def single(api):
+    out = {}
+    for beta, n, L, k in [((1, 2), 40, 32, 8), ((1, 1), 50, 24, 8), ((1, 3), 24, 40, 12)]:
+        mu, _ = api.build_hankel(beta, n, L)
+        with api.Context(L) as ctx:
+            out[(beta, n, L, k)] = (mu, results(ctx, mu, k))
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_virtual_sharded_bit_identical(api, single, world):
+    for (beta, n, L, k), (mu, (r0, D0, X0, M0)) in single.items():
+        with api.Context(L, world=world, virtual=True) as ctx:
+            r1, D1, X1, M1 = results(ctx, mu, k)
+        assert D1 == D0 and X1 == X0 and M1 == M0, (beta, n, world)
+        assert r1.lambda_hi == r0.lambda_hi and r1.lambda_lo == r0.lambda_lo
+
+
+def test_nccl_world1_bit_identical(api, single):
+    nid = api.nccl_unique_id()
+    (beta, n, L, k), (mu, (r0, D0, X0, M0)) = next(iter(single.items()))
+    with api.Context(L, rank=0, world=1, nccl_id=nid) as ctx:
+        r1, D1, X1, M1 = results(ctx, mu, k)
+    assert D1 == D0 and X1 == X0 and M1 == M0
+
+
+def test_virtual_sharded_c2_matches_model_digest(api):
+    from tests.test_gpu_parity import digest
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "model_c2.json")))
+    n, L, k = g["n"], g["p"] // 32, g["k"]
+    mu, _ = api.build_hankel((1, 1), n, L)
+    with api.Context(L, world=8, virtual=True) as ctx:
+        ctx.compute(mu, k)
+        assert digest(from_arr(ctx.D())) == g["D_sha256"]
+        assert digest(from_arr(ctx.block())) == g["block_sha256"]
+
+
+def test_virtual_sharded_precision_error(api):
+    n, L = 16, 1
+    mu, _ = api.build_hankel((1, 1), n, L)
+    with api.Context(L) as ref:
+        ref.load_moments(mu)
+        with pytest.raises(api.PrecisionError):
+            ref.decompose()
+        want = ref.bad_column
+    with api.Context(L, world=3, virtual=True) as ctx:
+        ctx.load_moments(mu)
+        with pytest.raises(api.PrecisionError):
+            ctx.decompose()
+        assert ctx.bad_column == want
