@@ -43,6 +43,7 @@ extern "C" {
 #define HK_OP_MUL 1   /* out = RNE(a*b)      — operator*, fixedpoint.cpp:67-69 (exact there) */
 #define HK_OP_ADD 2   /* out = RNE(a+b)      — operator+, fixedpoint.cpp:55-59 (exact there) */
 #define HK_OP_RECIP 3 /* out = RNE(1/a)      — FixScalar::div's role, fixedpoint.cpp:71-84 */
+#define HK_OP_CTA 16  /* or-flag: run FMS / MUL / RECIP with the CTA-cooperative kernels */
 
 typedef struct hk_ctx hk_ctx;
 

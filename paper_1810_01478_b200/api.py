@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libhankel_b200.so")
 
 HK_OK, HK_ERR_RUNTIME, HK_ERR_PRECISION, HK_ERR_INVALID = 0, 1, 2, 3
 OP_FMS, OP_MUL, OP_ADD, OP_RECIP = 0, 1, 2, 3
+OP_CTA = 16  # or-flag: CTA-cooperative kernels (critical-path variants)
 
 
 class PrecisionError(RuntimeError):

@@ -149,6 +149,41 @@ void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = 
     ++c->launches;
 }
 
+// One item per CTA (all warps cooperate on it): the critical-path ops.
+template <class F>
+__global__ void __launch_bounds__(256) k_cta_items(long long n, F f) {
+    extern __shared__ __align__(16) uint32_t cta_smem[];
+    for (long long it = blockIdx.x; it < n; it += gridDim.x) {
+        f(it, cta_smem);
+        __syncthreads();
+    }
+}
+
+constexpr int kCtaThreads = 256;
+
+template <class F>
+void launch_cta(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = nullptr) {
+    if (n <= 0) return;
+    if (!st) st = c->st;
+    const size_t smem = size_t(ws_words) * sizeof(uint32_t);
+    static std::map<const void*, size_t> configured;
+    const void* key = (const void*)&k_cta_items<F>;
+    auto it = configured.find(key);
+    if (it == configured.end() || it->second < smem) {
+        const size_t v = smem < 48 * 1024 ? 48 * 1024 : smem;
+        ck(cudaFuncSetAttribute(k_cta_items<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v)),
+           "cudaFuncSetAttribute");
+        configured[key] = v;
+    }
+    const long long blocks = n < (1LL << 30) ? n : (1LL << 30);
+    k_cta_items<F><<<unsigned(blocks), kCtaThreads, smem, st>>>(n, f);
+    ck(cudaGetLastError(), "kernel launch");
+    ++c->launches;
+}
+
+int ws_cta_words(int L) { return hk::ctaws_words(L); }
+int ws_cta_recip_words(int L) { return hk::ctarecipws_words(L); }
+
 int fail(hk_ctx* c, int code, const std::string& msg) {
     if (c) c->err = msg;
     return code;
@@ -229,8 +264,10 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     std::vector<cudaEvent_t>& evR = c->evR;
     ck(cudaEventRecord(c->evFork, bulk), "fork");
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
-    launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, 0, c->d_err}, 1, wr, la);
-    launch(c, hk::ItemMulB{c->S.view(), c->R.view(), b_buf(c, 0), N, L, 0, c->d_err}, N - 1, wo, la);
+    const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
+    (void)wr;
+    launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, 0, c->d_err}, 1, wcr, la);
+    launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, 0), N, L, 0, c->d_err}, N - 1, wc, la);
     ck(cudaEventRecord(evP[0], la), "evP");
     for (int i = 0; i < N; ++i) {
         ck(cudaStreamWaitEvent(bulk, evP[i], 0), "wait P");
@@ -238,10 +275,10 @@ void enqueue_ldlt_steps(hk_ctx* c) {
         launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 2, c->d_err}, nu, wo, bulk);
         if (i + 1 < N) {
             if (i > 0) ck(cudaStreamWaitEvent(la, evR[i - 1], 0), "wait R");
-            launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 1, c->d_err}, N - i - 1, wo, la);
-            launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wr, la);
-            launch(c, hk::ItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err}, N - i - 2, wo,
-                   la);
+            launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err}, N - i - 1, wc, la);
+            launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la);
+            launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err}, N - i - 2,
+                       wc, la);
             ck(cudaEventRecord(evP[i + 1], la), "evP");
             ck(cudaStreamWaitEvent(bulk, evP[i + 1], 0), "wait P next");
         }
@@ -572,7 +609,10 @@ int hk_mp_batch(hk_ctx* c, int op, long long count, const uint32_t* a_l, const i
                 const uint32_t* b_l, const int32_t* b_e, const int32_t* b_s, const uint32_t* c_l, const int32_t* c_e,
                 const int32_t* c_s, uint32_t* o_l, int32_t* o_e, int32_t* o_s) {
     return guarded(c, [&] {
-        if (op < 0 || op > 3 || count < 1) return fail(c, HK_ERR_INVALID, "hk_mp_batch: bad op/count");
+        const bool cta = (op & HK_OP_CTA) != 0;
+        op &= ~HK_OP_CTA;
+        if (op < 0 || op > 3 || count < 1 || (cta && op == HK_OP_ADD))
+            return fail(c, HK_ERR_INVALID, "hk_mp_batch: bad op/count");
         if ((op != HK_OP_RECIP && (!b_l || !b_e || !b_s)) || (op == HK_OP_FMS && (!c_l || !c_e || !c_s)))
             return fail(c, HK_ERR_INVALID, "hk_mp_batch: missing operand");
         const int L = c->L;
@@ -582,7 +622,11 @@ int hk_mp_batch(hk_ctx* c, int op, long long count, const uint32_t* a_l, const i
         if (op == HK_OP_FMS) h2d_soa(c, C, count, c_l, c_e, c_s);
         O.ensure(count, L);
         const int ws = op == HK_OP_RECIP ? ws_recip_words(L) : ws_op_words(L);
-        launch(c, hk::ItemBatch{A.view(), B.view(), C.view(), O.view(), L, op}, count, ws);
+        if (cta)
+            launch_cta(c, hk::CItemBatch{A.view(), B.view(), C.view(), O.view(), L, op == HK_OP_RECIP ? 2 : op}, count,
+                       op == HK_OP_RECIP ? ws_cta_recip_words(L) : ws_cta_words(L));
+        else
+            launch(c, hk::ItemBatch{A.view(), B.view(), C.view(), O.view(), L, op}, count, ws);
         ck(cudaStreamSynchronize(c->st), "sync");
         d2h_range(c, O, 0, count, o_l, o_e, o_s);
         A.release();
@@ -661,10 +705,15 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
         launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
         long long nt = 0;
         for (int i = 0; i < N; ++i) {
-            timed(1, [&] { launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, wr); });
+            timed(1, [&] {
+                launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, ws_cta_recip_words(L));
+            });
             const int nb = N - i - 1;
             if (nb == 0) continue;
-            timed(2, [&] { launch(c, hk::ItemMulB{c->S.view(), c->R.view(), b_buf(c, i), N, L, i, c->d_err}, nb, wo); });
+            timed(2, [&] {
+                launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i), N, L, i, c->d_err}, nb,
+                           ws_cta_words(L));
+            });
             timed(0, [&] {
                 launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 1, c->d_err},
                        (long long)nb * (nb + 1) / 2, wo);
@@ -862,9 +911,10 @@ void publish(hk_ctx* c, int col) {
 
 void derive(hk_ctx* c, Shard& s, int i) {
     const int N = c->n, L = c->L;
-    launch(c, hk::ItemDRecip{s.panel.view(), s.R.view(), L, i, s.d_err}, 1, ws_recip_words(L));
+    launch_cta(c, hk::CItemDRecip{s.panel.view(), s.R.view(), L, i, s.d_err}, 1, ws_cta_recip_words(L));
     if (N - i - 1 > 0)
-        launch(c, hk::ItemDMulB{s.panel.view(), s.R.view(), s.B.view(), L, i, s.d_err}, N - i - 1, ws_op_words(L));
+        launch_cta(c, hk::CItemDMulB{s.panel.view(), s.R.view(), s.B.view(), L, i, s.d_err}, N - i - 1,
+                   ws_cta_words(L));
 }
 
 // gather all columns into the standard jagged S on rank 0 (+ R)

@@ -345,6 +345,101 @@ struct ItemCopy {
     }
 };
 
+// ======================================================================
+// CTA-cooperative items (one item per CTA) for the latency-bound critical path
+// of the look-ahead: column update -> reciprocal -> B column.
+
+HK_DEV void cta_meta_store(Meta* dst, Meta v) {
+    if (cta_tid() == 0) *dst = v;
+    cta_sync();
+}
+
+struct CItemRecip { // R_i = RNE(1/S_ii) with the pivot sign test
+    MpArr S, R;
+    int N, L, i;
+    int* err;
+    HK_DEV void operator()(long long, uint32_t* ws) const {
+        if (*(volatile int*)err >= 0) return;
+        const long long e = tri_idx(i, i, N);
+        const Meta dm = S.m[e];
+        if (dm.sign <= 0) {
+            if (cta_tid() == 0) ItemRecip::atomicCAS_emu(err, i);
+            return;
+        }
+        cta_meta_store(R.m + i, cta_recip(S.limbs(e, L), dm, R.limbs(i, L), L, ws));
+    }
+};
+
+struct CItemMulB { // B_i(k) = RNE(S(k,i) R_i), k = i+1+t
+    MpArr S, R, B;
+    int N, L, i;
+    const int* err;
+    HK_DEV void operator()(long long t, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int k = i + 1 + int(t);
+        const long long e = tri_idx(k, i, N);
+        cta_meta_store(B.m + k, cta_mulr(S.limbs(e, L), S.m[e], R.limbs(i, L), R.m[i], B.limbs(k, L), L,
+                                         ctaws_carve(ws, L)));
+    }
+};
+
+struct CItemColUpd { // look-ahead column j = i+1: S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)), k = j+t
+    MpArr S, B;
+    int N, L, i;
+    const int* err;
+    HK_DEV void operator()(long long t, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int j = i + 1, k = j + int(t);
+        const long long ec = tri_idx(k, j, N), ex = tri_idx(j, i, N);
+        uint32_t* c = S.limbs(ec, L);
+        cta_meta_store(S.m + ec, cta_fms(c, S.m[ec], S.limbs(ex, L), S.m[ex], B.limbs(k, L), B.m[k], c, L,
+                                         ctaws_carve(ws, L)));
+    }
+};
+
+struct CItemDRecip { // sharded: R_i from the panel
+    MpArr panel, R;
+    int L, i;
+    int* err;
+    HK_DEV void operator()(long long, uint32_t* ws) const {
+        if (*(volatile int*)err >= 0) return;
+        const Meta dm = panel.m[0];
+        if (dm.sign <= 0) {
+            if (cta_tid() == 0) ItemRecip::atomicCAS_emu(err, i);
+            return;
+        }
+        cta_meta_store(R.m + i, cta_recip(panel.limbs(0, L), dm, R.limbs(i, L), L, ws));
+    }
+};
+
+struct CItemDMulB { // sharded: B_i(k) = RNE(panel_i(k) R_i)
+    MpArr panel, R, B;
+    int L, i;
+    const int* err;
+    HK_DEV void operator()(long long t, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int k = i + 1 + int(t);
+        cta_meta_store(B.m + k, cta_mulr(panel.limbs(k - i, L), panel.m[k - i], R.limbs(i, L), R.m[i], B.limbs(k, L),
+                                         L, ctaws_carve(ws, L)));
+    }
+};
+
+struct CItemBatch { // the CTA ops on batches (tests)
+    MpArr A, B, C, O;
+    int L, op;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        Meta r;
+        if (op == 0)
+            r = cta_fms(C.limbs(w, L), C.m[w], A.limbs(w, L), A.m[w], B.limbs(w, L), B.m[w], O.limbs(w, L), L,
+                        ctaws_carve(ws, L));
+        else if (op == 1)
+            r = cta_mulr(A.limbs(w, L), A.m[w], B.limbs(w, L), B.m[w], O.limbs(w, L), L, ctaws_carve(ws, L));
+        else
+            r = cta_recip(A.limbs(w, L), A.m[w], O.limbs(w, L), L, ws);
+        cta_meta_store(O.m + w, r);
+    }
+};
+
 // ---- generic batch ops (parity tests of the arithmetic itself)
 struct ItemBatch {
     MpArr A, B, C, O;

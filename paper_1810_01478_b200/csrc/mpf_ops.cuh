@@ -139,12 +139,12 @@ HK_HD int align4(int n) { return (n + 3) & ~3; }
 
 // Every region starts 16-byte aligned (warp_mul reads A with 128-bit loads).
 HK_HD int recipws_words(int L) {
-    const int nm = L + 2;
+    const int nm = L + 3;
     return 3 * align4(nm + 1) + align4(nm) + align4(nm + 64) + align4(2 * nm + 2) + align4(2 * nm + 8) + 4;
 }
 
 HK_DEV RecipWs recipws_carve(uint32_t* b, int L) {
-    const int nm = L + 2;
+    const int nm = L + 3;
     RecipWs w;
     w.A = b;
     b += align4(nm);
@@ -178,6 +178,8 @@ HK_DEV void warp_mul_staged(const uint32_t* x, int nx, const uint32_t* y, int ny
     warp_mul(w.A, nx, w.Bp, ny, w.P);
     wsync();
 }
+
+HK_DEV int recip_finish(const uint32_t* Md, int L, int nz, int zlsb, const RecipWs& w);
 
 HK_DEV Meta warp_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, const RecipWs& w) {
     const int ln = lane();
@@ -223,7 +225,17 @@ HK_DEV Meta warp_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, const 
         nz = nk;
         zlsb = rz.exp - 32 * nk;
     }
-    // 3. r = RNE_L(z), then one exact midpoint test
+    const int rexp = recip_finish(Md, L, nz, zlsb, w);
+    for (int i = ln; i < L; i += 32) out[i] = w.T[i];
+    wsync();
+    return Meta{rexp - dm.exp, dm.sign};
+}
+
+// Step 3 of the reciprocal (one warp): r = RNE_L(z) into w.T, then the Ziv /
+// exact midpoint test.  Returns r's exponent (r ~ 1/m in [1, 2]).
+HK_DEV int recip_finish(const uint32_t* Md, int L, int nz, int zlsb, const RecipWs& w) {
+    const int ln = lane();
+    const Opd one{w.one, 1, 0, 1};
     const Opd zf{w.Z, nz, zlsb, 1};
     const Opd none{nullptr, 0, 0, 0};
     RMeta rr = warp_round_sum(zf, none, w.G, w.T, L);
@@ -305,9 +317,241 @@ HK_DEV Meta warp_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, const 
         }
         wsync();
     }
-    // 4. write out, exponent 1/d = (1/m) 2^-e
-    for (int i = ln; i < L; i += 32) out[i] = w.T[i];
-    wsync();
+    return rexp;
+}
+
+// ---------------------------------------------------------------- CTA-cooperative ops
+//
+// Latency matters on the LDLT's critical path (look-ahead column -> reciprocal
+// -> B column, one op after the other): there one op gets a whole CTA.  All
+// warps compute product column groups (cta_mul); warp 0 does the rounding and
+// publishes the result metadata through shared memory.  Results are bit-identical
+// to the warp versions (same correctly rounded operations).
+struct CtaWs {
+    OpWs op;
+    uint32_t* CS;
+    int* sh; // shared flags / metadata broadcast
+};
+
+HK_HD int ctaws_words(int L) { return opws_words(L) + cta_cs_words(2 * L) + 8; }
+
+HK_DEV CtaWs ctaws_carve(uint32_t* b, int L) {
+    CtaWs w;
+    w.op = opws_carve(b, L);
+    w.CS = b + opws_words(L);
+    w.sh = reinterpret_cast<int*>(w.CS + cta_cs_words(2 * L));
+    return w;
+}
+
+HK_DEV void cta_stage_and_mul(const uint32_t* xd, const uint32_t* yd, int L, const CtaWs& w, int t0) {
+    cta_copy(w.op.A, xd, L);
+    cta_stage_padded(w.op.Bp, yd, L);
+    cta_sync();
+    cta_mul(w.op.A, L, w.op.Bp, L, w.op.P, t0, w.CS);
+}
+
+// warp 0's RMeta (and ok flag) to every thread of the CTA
+HK_DEV RMeta cta_bcast_meta(const CtaWs& w, RMeta r, bool ok, bool* ok_out) {
+    if (warp_id() == 0 && lane() == 0) {
+        w.sh[0] = r.exp;
+        w.sh[1] = r.sign;
+        w.sh[2] = ok ? 1 : 0;
+    }
+    cta_sync();
+    const RMeta o{w.sh[0], w.sh[1]};
+    if (ok_out) *ok_out = w.sh[2] != 0;
+    cta_sync();
+    return o;
+}
+
+HK_DEV Meta cta_round_with_product(const Opd& X, const uint32_t* xd, const uint32_t* yd, int lsbP, int sp,
+                                   uint32_t* out, int L, const CtaWs& w) {
+    const int t0 = L > kGuardLimbs ? L - kGuardLimbs : 0;
+    cta_stage_and_mul(xd, yd, L, w, t0);
+    if (t0 > 0) {
+        RMeta r{0, 0};
+        bool ok = false;
+        if (warp_id() == 0) {
+            const Opd Yh{w.op.P + t0, 2 * L - t0, lsbP + 32 * t0, sp};
+            r = warp_round_sum(X, Yh, w.op.G, out, L, lsbP + 32 * t0 + 46, &ok);
+        }
+        r = cta_bcast_meta(w, r, ok, &ok);
+        if (ok) return Meta{r.exp, r.sign};
+        cta_stage_and_mul(xd, yd, L, w, 0); // exact product (the window overwrote A / Bp)
+    }
+    RMeta r{0, 0};
+    if (warp_id() == 0) {
+        const Opd Y{w.op.P, 2 * L, lsbP, sp};
+        r = warp_round_sum(X, Y, w.op.G, out, L);
+    }
+    r = cta_bcast_meta(w, r, true, nullptr);
+    return Meta{r.exp, r.sign};
+}
+
+HK_DEV Meta cta_fms(const uint32_t* cd, Meta cm, const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym,
+                    uint32_t* out, int L, const CtaWs& w) {
+    const int sp = -(xm.sign * ym.sign);
+    const Opd X{cd, L, cm.exp - 32 * L, cm.sign};
+    if (sp == 0) {
+        RMeta r{0, 0};
+        if (warp_id() == 0) r = warp_round_sum(X, Opd{nullptr, 0, 0, 0}, w.op.G, out, L);
+        r = cta_bcast_meta(w, r, true, nullptr);
+        return Meta{r.exp, r.sign};
+    }
+    return cta_round_with_product(X, xd, yd, xm.exp + ym.exp - 64 * L, sp, out, L, w);
+}
+
+HK_DEV Meta cta_mulr(const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym, uint32_t* out, int L,
+                     const CtaWs& w) {
+    const int sp = xm.sign * ym.sign;
+    const Opd Z{nullptr, 0, 0, 0};
+    if (sp == 0) {
+        RMeta r{0, 0};
+        if (warp_id() == 0) r = warp_round_sum(Z, Z, w.op.G, out, L);
+        r = cta_bcast_meta(w, r, true, nullptr);
+        return Meta{r.exp, r.sign};
+    }
+    return cta_round_with_product(Z, xd, yd, xm.exp + ym.exp - 64 * L, sp, out, L, w);
+}
+
+// ---- CTA reciprocal, fixed-point Newton.
+//
+// z ~ 1/m in fixed point: Z[0..nf] (nf fraction limbs + one integer limb),
+// value Z / 2^(32 nf).  One level to nk fraction limbs (all truncating):
+//   T = top_mn(M) * Z                (mn = min(L, nk) limbs of m; CTA product)
+//   |e|_nk = top nk fraction limbs of (T - 1)  if T >= 1   (e = 1 - m z <= 0)
+//          = top nk fraction limbs of ~T       otherwise   (one's complement:
+//            off by at most one unit, inside the truncation budget)
+//   D = Z * |e|_nk, keep 2^-32nk and above     (CTA product)
+//   Z <- (Z << 32(nk - nf)) -/+ D              (one carry pass)
+// Every step truncates, so after the last level (nk = L+2) |z - 1/m| is a few
+// units of 2^-32(L+2).  r = RNE_L(z) by one round; the Ziv test on the 65-66
+// discarded bits certifies it, otherwise recip_finish's exact midpoint test
+// runs.  Output is RNE(1/d), identical to warp_recip / oracle/mpfloat.recip.
+struct FxRecipWs {
+    RecipWs rw;       // A / Bp / P / Z (= z) / E (= |e|) double as the Newton buffers
+    uint32_t *CS, *Z2;
+    int* sh;
+};
+
+// ~64 L + 1 KB bytes: fits the 227 KB per-CTA limit up to L = 3600 (p = 115200).
+HK_HD int ctarecipws_words(int L) {
+    return recipws_words(L) + cta_cs_words(2 * (L + 4)) + align4(L + 4) + 8;
+}
+
+HK_DEV FxRecipWs fxrecipws_carve(uint32_t* b, int L) {
+    FxRecipWs w;
+    w.rw = recipws_carve(b, L);
+    b += recipws_words(L);
+    w.CS = b;
+    b += cta_cs_words(2 * (L + 4));
+    w.Z2 = b;
+    b += align4(L + 4);
+    w.sh = reinterpret_cast<int*>(b);
+    return w;
+}
+
+HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_t* wsb) {
+    FxRecipWs w = fxrecipws_carve(wsb, L);
+    const bool w0 = warp_id() == 0;
+    // seed: z0 = 1/m_hi in binary64, as a fixed-point value with 2 fraction limbs
+    const uint64_t mh = ((uint64_t)Md[L - 1] << 32) | (L >= 2 ? Md[L - 2] : 0u);
+    const double zd = 1.0 / ldexp((double)mh, -64);
+    int ex;
+    const uint64_t mant = (uint64_t)ldexp(frexp(zd, &ex), 53); // zd = mant 2^(ex-53), ex in {1, 2}
+    if (cta_tid() == 0) {
+        const int sh = ex + 11; // Z = mant << (64 + ex - 53), a 66-bit value
+        const uint64_t lo = mant << sh;
+        w.rw.Z[0] = uint32_t(lo);
+        w.rw.Z[1] = uint32_t(lo >> 32);
+        w.rw.Z[2] = uint32_t(mant >> (64 - sh));
+        w.rw.Z[3] = 0u;
+    }
+    if (cta_tid() == 1) w.rw.one[0] = 1u;
+    cta_sync();
+    int nf = 2;
+    int sched[32];
+    int ns = 0;
+    for (int n = L + 2;; n = (n + 1) / 2 + 1) {
+        sched[ns++] = n;
+        if (n <= 3) break;
+    }
+    uint32_t* Z = w.rw.Z;
+    uint32_t* Zn = w.Z2;
+    for (int si = ns - 1; si >= 0; --si) {
+        const int nk = sched[si];
+        const int mn = nk >= L ? L : nk;
+        // T = m_top * z
+        cta_copy(w.rw.A, Md + (L - mn), mn);
+        cta_stage_padded(w.rw.Bp, Z, nf + 1);
+        cta_sync();
+        cta_mul(w.rw.A, mn, w.rw.Bp, nf + 1, w.rw.P, 0, w.CS);
+        const int FT = mn + nf; // fraction limbs of T
+        const bool neg = w.rw.P[FT] != 0u; // T >= 1  ->  e <= 0
+        for (int q = cta_tid(); q < nk; q += cta_threads()) {
+            const uint32_t v = w.rw.P[FT - nk + q];
+            w.rw.E[q] = neg ? v : ~v;
+        }
+        cta_sync();
+        // D = z * |e|
+        cta_copy(w.rw.A, Z, nf + 1);
+        cta_stage_padded(w.rw.Bp, w.rw.E, nk);
+        cta_sync();
+        cta_mul(w.rw.A, nf + 1, w.rw.Bp, nk, w.rw.P, 0, w.CS);
+        // Z' = (Z << 32 (nk - nf)) -/+ (D >> 32 nf), over nk + 1 limbs
+        if (w0) {
+            const int shl = nk - nf;
+            uint32_t c = 0;
+            for (int b0 = 0; b0 <= nk; b0 += 32) {
+                const int q = b0 + lane();
+                const uint32_t zv = (q <= nk && q >= shl) ? Z[q - shl] : 0u;
+                const uint32_t dv = q <= nk ? w.rw.P[nf + q] : 0u;
+                uint32_t r;
+                if (neg) {
+                    r = zv - dv;
+                    c = seg_borrow(r, zv < dv, c);
+                } else {
+                    r = zv + dv;
+                    c = seg_carry(r, r < zv, c);
+                }
+                if (q <= nk) Zn[q] = r;
+            }
+        }
+        cta_sync();
+        uint32_t* t = Z;
+        Z = Zn;
+        Zn = t;
+        nf = nk;
+    }
+    // r = RNE_L(z), Ziv test on the discarded bits, exact test if needed
+    if (w0) {
+        const int nz = L + 3; // nf = L + 2 fraction limbs + integer limb
+        const Opd zf{Z, nz, -32 * (L + 2), 1};
+        const RMeta rr = warp_round_sum(zf, Opd{nullptr, 0, 0, 0}, w.rw.G, w.rw.T, L);
+        int rexp = rr.exp;
+        // discarded bits: k = bitlen(Z) - 32 L (65 or 66); distance to the half
+        const int kbits = (32 * (L + 2) + (Z[L + 2] >= 2u ? 2 : 1)) - 32 * L;
+        const uint64_t lo64 = ((uint64_t)Z[1] << 32) | Z[0];
+        const uint32_t top = Z[2] & ((1u << (kbits - 64)) - 1u); // 1 or 2 bits above the low 64
+        // value f = top 2^64 + lo64, half = 2^(kbits-1)
+        bool safe;
+        if (kbits == 65)
+            safe = top ? lo64 > (1ull << 16) : lo64 < ~0ull - (1ull << 16);
+        else // kbits == 66: half = 2^65 = top 2 (binary 10) with lo64 = 0
+            safe = top == 2u ? lo64 > (1ull << 16) : (top == 1u ? lo64 < ~0ull - (1ull << 16) : true);
+        if (!safe || HK_FORCE_EXACT_RECIP) {
+            if (Z != w.rw.Z) {
+                for (int q = lane(); q < nz; q += 32) w.rw.Z[q] = Z[q];
+                wsync();
+            }
+            rexp = recip_finish(Md, L, nz, -32 * (L + 2), w.rw);
+        }
+        if (lane() == 0) w.sh[0] = rexp;
+    }
+    cta_sync();
+    const int rexp = w.sh[0];
+    cta_copy(out, w.rw.T, L);
+    cta_sync();
     return Meta{rexp - dm.exp, dm.sign};
 }
 

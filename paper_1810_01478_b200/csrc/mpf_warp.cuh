@@ -214,60 +214,134 @@ HK_DEV void warp_stage_padded(uint32_t* Bp, const uint32_t* B, int n) {
 // 0 <= E < min(nA,nB) 2^(32 tfirst + 32), see warp_fms).  A: plain limbs (smem),
 // Bp: the padded staging of B (smem).  Column sums in 96 bits per lane, carries
 // resolved per 32-limb group with a running carry / high-word state.
-HK_DEV void warp_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint32_t* P, int tfirst = 0) {
-    const int ln = lane();
-    const int ntot = nA + nB;
-    uint32_t cin = 0, hi_prev = 0, a1p = 0, a2p31 = 0, a2p30 = 0;
-    for (int g0 = tfirst; g0 < ntot; g0 += 32) {
-        const int t = g0 + ln;
-        const int slo = max(0, g0 - (nB - 1));
-        const int shi = min(g0 + 31, nA - 1);
-        // four independent accumulator chains (s mod 4) break the carry-chain
-        // dependency so a lone warp (reciprocal, B column, L^{-1}) is not
-        // latency-bound; they are folded together after the loop.
-        // Per 8 MACs: 2 warp-uniform LDS.128 for x (broadcast), 8 LDS for y,
-        // 8 IMAD.WIDE.U32 + 4 IADD3.X (SASS checked).  The prologue aligns s so
-        // the x loads are 16-byte vectors (A is 16-byte aligned).
-        uint64_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-        uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
-        const uint32_t* yb = Bp + 32 + t;
-        int s = slo;
-        for (; s <= shi && (s & 3); ++s) mac64(q0, h0, A[s], yb[-s]);
-        for (; s + 7 <= shi; s += 8) {
-            const uint4 xa = *reinterpret_cast<const uint4*>(A + s);
-            const uint4 xb = *reinterpret_cast<const uint4*>(A + s + 4);
-            mac64x2(q0, h0, xa.x, yb[-s], xb.x, yb[-s - 4]);
-            mac64x2(q1, h1, xa.y, yb[-s - 1], xb.y, yb[-s - 5]);
-            mac64x2(q2, h2, xa.z, yb[-s - 2], xb.z, yb[-s - 6]);
-            mac64x2(q3, h3, xa.w, yb[-s - 3], xb.w, yb[-s - 7]);
-        }
-        for (; s <= shi; ++s) mac64(q0, h0, A[s], yb[-s]);
-        uint32_t a0 = uint32_t(q0), a1 = uint32_t(q0 >> 32), a2 = h0;
-        add96(a0, a1, a2, uint32_t(q1), uint32_t(q1 >> 32), h1);
-        add96(a0, a1, a2, uint32_t(q2), uint32_t(q2 >> 32), h2);
-        add96(a0, a1, a2, uint32_t(q3), uint32_t(q3 >> 32), h3);
-        // limb t receives a0(t) + a1(t-1) + a2(t-2)
-        uint32_t a1m1 = shfl_up(a1, 1);
-        uint32_t a2m2 = shfl_up(a2, 2);
-        if (ln == 0) {
-            a1m1 = a1p;
-            a2m2 = a2p30;
-        } else if (ln == 1) {
-            a2m2 = a2p31;
-        }
-        const uint64_t s64 = (uint64_t)a0 + a1m1 + a2m2;
-        const uint32_t lo = uint32_t(s64), hi = uint32_t(s64 >> 32);
-        uint32_t him1 = shfl_up(hi, 1);
-        if (ln == 0) him1 = hi_prev;
-        uint32_t w = lo + him1;
-        const bool gen = w < lo;
-        cin = seg_carry(w, gen, cin);
-        if (t < ntot) P[t] = w;
-        a1p = shfl(a1, 31);
-        a2p31 = shfl(a2, 31);
-        a2p30 = shfl(a2, 30);
-        hi_prev = shfl(hi, 31);
+// 96-bit column sum of column t = g0 + lane: sum_s A[s] B[t-s] over the
+// group's union s-range.  Four independent accumulator chains break the carry
+// dependency (a lone warp is latency-bound otherwise).  Per 8 MACs: 2
+// warp-uniform LDS.128 for x (broadcast), 8 LDS for y, 8 IMAD.WIDE.U32 + 4
+// IADD3.X (SASS checked).  The prologue aligns s so the x loads are 16-byte
+// vectors (A must be 16-byte aligned).
+HK_DEV void colsum_group(const uint32_t* A, int nA, const uint32_t* Bp, int nB, int g0, uint32_t& a0, uint32_t& a1,
+                         uint32_t& a2) {
+    const int t = g0 + lane();
+    const int slo = max(0, g0 - (nB - 1));
+    const int shi = min(g0 + 31, nA - 1);
+    uint64_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+    uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+    const uint32_t* yb = Bp + 32 + t;
+    int s = slo;
+    for (; s <= shi && (s & 3); ++s) mac64(q0, h0, A[s], yb[-s]);
+    for (; s + 7 <= shi; s += 8) {
+        const uint4 xa = *reinterpret_cast<const uint4*>(A + s);
+        const uint4 xb = *reinterpret_cast<const uint4*>(A + s + 4);
+        mac64x2(q0, h0, xa.x, yb[-s], xb.x, yb[-s - 4]);
+        mac64x2(q1, h1, xa.y, yb[-s - 1], xb.y, yb[-s - 5]);
+        mac64x2(q2, h2, xa.z, yb[-s - 2], xb.z, yb[-s - 6]);
+        mac64x2(q3, h3, xa.w, yb[-s - 3], xb.w, yb[-s - 7]);
     }
+    for (; s <= shi; ++s) mac64(q0, h0, A[s], yb[-s]);
+    a0 = uint32_t(q0);
+    a1 = uint32_t(q0 >> 32);
+    a2 = h0;
+    add96(a0, a1, a2, uint32_t(q1), uint32_t(q1 >> 32), h1);
+    add96(a0, a1, a2, uint32_t(q2), uint32_t(q2 >> 32), h2);
+    add96(a0, a1, a2, uint32_t(q3), uint32_t(q3 >> 32), h3);
+}
+
+// Running state of the column-sum -> limb carry resolution (warp-uniform).
+struct CarryState {
+    uint32_t cin = 0, hi_prev = 0, a1p = 0, a2p31 = 0, a2p30 = 0;
+};
+
+// Limb t = g0 + lane of the product from the group's column sums: limb t
+// receives a0(t) + a1(t-1) + a2(t-2) + carries, resolved with the lookahead.
+HK_DEV uint32_t carry_group(CarryState& cs, uint32_t a0, uint32_t a1, uint32_t a2) {
+    const int ln = lane();
+    uint32_t a1m1 = shfl_up(a1, 1);
+    uint32_t a2m2 = shfl_up(a2, 2);
+    if (ln == 0) {
+        a1m1 = cs.a1p;
+        a2m2 = cs.a2p30;
+    } else if (ln == 1) {
+        a2m2 = cs.a2p31;
+    }
+    const uint64_t s64 = (uint64_t)a0 + a1m1 + a2m2;
+    const uint32_t lo = uint32_t(s64), hi = uint32_t(s64 >> 32);
+    uint32_t him1 = shfl_up(hi, 1);
+    if (ln == 0) him1 = cs.hi_prev;
+    uint32_t w = lo + him1;
+    const bool gen = w < lo;
+    cs.cin = seg_carry(w, gen, cs.cin);
+    cs.a1p = shfl(a1, 31);
+    cs.a2p31 = shfl(a2, 31);
+    cs.a2p30 = shfl(a2, 30);
+    cs.hi_prev = shfl(hi, 31);
+    return w;
+}
+
+HK_DEV void warp_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint32_t* P, int tfirst = 0) {
+    const int ntot = nA + nB;
+    CarryState cs;
+    for (int g0 = tfirst; g0 < ntot; g0 += 32) {
+        uint32_t a0, a1, a2;
+        colsum_group(A, nA, Bp, nB, g0, a0, a1, a2);
+        const uint32_t w = carry_group(cs, a0, a1, a2);
+        const int t = g0 + lane();
+        if (t < ntot) P[t] = w;
+    }
+}
+
+// ---- CTA cooperation for latency-bound single ops (the LDLT's critical path:
+// reciprocal, B column, look-ahead column).  On the host emulator a "CTA" is
+// one warp, so the same code is exercised with num_warps() == 1.
+#if defined(HK_WARP_EMU)
+HK_DEV int warp_id() { return 0; }
+HK_DEV int num_warps() { return 1; }
+HK_DEV void cta_sync() { wsync(); }
+HK_DEV int cta_tid() { return lane(); }
+HK_DEV int cta_threads() { return 32; }
+#else
+HK_DEV int warp_id() { return int(threadIdx.x >> 5); }
+HK_DEV int num_warps() { return int(blockDim.x >> 5); }
+HK_DEV void cta_sync() { __syncthreads(); }
+HK_DEV int cta_tid() { return int(threadIdx.x); }
+HK_DEV int cta_threads() { return int(blockDim.x); }
+#endif
+
+HK_HD int cta_cs_words(int ntot) { return 96 * ((ntot + 31) / 32); }
+
+// Product (from column tfirst) by all warps of the CTA: warps take 32-column
+// groups round-robin and park the 96-bit sums in CS, then warp 0 resolves the
+// carries group by group (cheap: one lookahead per group).  A, Bp staged.
+HK_DEV void cta_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint32_t* P, int tfirst, uint32_t* CS) {
+    const int ntot = nA + nB, ng = (ntot - tfirst + 31) / 32;
+    const int w = warp_id(), nw = num_warps();
+    for (int g = w; g < ng; g += nw) {
+        uint32_t a0, a1, a2;
+        colsum_group(A, nA, Bp, nB, tfirst + 32 * g, a0, a1, a2);
+        uint32_t* c = CS + 96 * g + lane();
+        c[0] = a0;
+        c[32] = a1;
+        c[64] = a2;
+    }
+    cta_sync();
+    if (w == 0) {
+        CarryState cs;
+        for (int g = 0; g < ng; ++g) {
+            const uint32_t* c = CS + 96 * g + lane();
+            const uint32_t v = carry_group(cs, c[0], c[32], c[64]);
+            const int t = tfirst + 32 * g + lane();
+            if (t < ntot) P[t] = v;
+        }
+    }
+    cta_sync();
+}
+
+// CTA-strided copies (all threads)
+HK_DEV void cta_copy(uint32_t* dst, const uint32_t* src, int n) {
+    for (int i = cta_tid(); i < n; i += cta_threads()) dst[i] = src[i];
+}
+HK_DEV void cta_stage_padded(uint32_t* Bp, const uint32_t* B, int n) {
+    for (int i = cta_tid(); i < n + 64; i += cta_threads()) Bp[i] = (i >= 32 && i < 32 + n) ? B[i - 32] : 0u;
 }
 
 // Result metadata of a rounded operation.

@@ -72,3 +72,23 @@ def test_emulated_path_reports_first_bad_pivot(emu_bin):
     except ArithmeticError as e:
         model_col = int(str(e).rsplit(" ", 1)[1])
     assert col == model_col and col > 0
+
+
+@pytest.mark.parametrize("L", [1, 3, 8, 33])
+def test_emulated_cta_ops_match_model(emu_bin, L):
+    """The CTA-cooperative critical-path ops (as a 1-warp CTA on the host)."""
+    rng = random.Random(2000 + L)
+    p = 32 * L
+    cases = fms_cases(L, rng, 40)
+    lines = [f"op cfms {L} {len(cases)}"] + [to_line(v, L) for t in cases for v in t]
+    for (c, x, y), r in zip(cases, run(emu_bin, lines)):
+        assert from_line(r, L) == F.fms(c, x, y, p), (c, x, y)
+    pairs = [(rnd(L, rng), rnd(L, rng)) for _ in range(30)]
+    lines = [f"op cmul {L} {len(pairs)}"] + [to_line(v, L) for t in pairs for v in t]
+    for (x, y), r in zip(pairs, run(emu_bin, lines)):
+        assert from_line(r, L) == F.mul(x, y, p)
+    ds = [rnd(L, rng) for _ in range(30)]
+    for op in ("crecip", "crecipx"):
+        lines = [f"op {op} {L} {len(ds)}"] + [to_line(d, L) for d in ds]
+        for d, r in zip(ds, run(emu_bin, lines)):
+            assert from_line(r, L) == F.recip(d, p)

@@ -57,6 +57,13 @@ def test_mp_ops_bit_exact(api, L, count):
         nrec = min(count, 24)
         got = from_arr(ctx.mp_batch(api.OP_RECIP, to_arr(xs_l[:nrec], L)))
         assert got == [F.recip(x, p) for x in xs_l[:nrec]]
+        # CTA-cooperative variants (the look-ahead / critical-path kernels)
+        got = from_arr(ctx.mp_batch(api.OP_FMS | api.OP_CTA, xs, ys, cs))
+        assert got == [F.fms(c, x, y, p) for c, x, y in cases]
+        got = from_arr(ctx.mp_batch(api.OP_MUL | api.OP_CTA, to_arr(xs_l, L), ys))
+        assert got == [F.mul(x, t[2], p) for x, t in zip(xs_l, cases)]
+        got = from_arr(ctx.mp_batch(api.OP_RECIP | api.OP_CTA, to_arr(xs_l[:nrec], L)))
+        assert got == [F.recip(x, p) for x in xs_l[:nrec]]
 
 
 # ------------------------------------------------------------------ the path, bit-exact vs the model

@@ -68,8 +68,11 @@ int main() {
             long long cnt;
             std::cin >> op >> L >> cnt;
             HostArr A(cnt, L), B(cnt, L), C(cnt, L), O(cnt, L);
-            int code = op == "fms" ? 0 : op == "mul" ? 1 : op == "add" ? 2 : 3;
-            hk::force_exact_recip() = (op == "recipx"); // recip with the exact midpoint test forced
+            // c-prefixed ops run the CTA-cooperative variants (a 1-warp CTA here)
+            const bool cta = op.size() > 1 && op[0] == 'c';
+            const std::string base = cta ? op.substr(1) : op;
+            int code = base == "fms" ? 0 : base == "mul" ? 1 : base == "add" ? 2 : 3;
+            hk::force_exact_recip() = (base == "recipx"); // recip with the exact midpoint test forced
             for (long long e = 0; e < cnt; ++e) {
                 if (code == 0) {
                     read_opd(C, e, L);
@@ -82,8 +85,12 @@ int main() {
                     read_opd(B, e, L);
                 }
             }
-            ItemBatch it{A.view(), B.view(), C.view(), O.view(), L, code};
-            run_items(cnt, ws_words_for(L), it);
+            if (cta) {
+                const int ws = ctaws_words(L) > ctarecipws_words(L) ? ctaws_words(L) : ctarecipws_words(L);
+                run_items(cnt, ws, CItemBatch{A.view(), B.view(), C.view(), O.view(), L, code == 3 ? 2 : code});
+            } else {
+                run_items(cnt, ws_words_for(L), ItemBatch{A.view(), B.view(), C.view(), O.view(), L, code});
+            }
             for (long long e = 0; e < cnt; ++e) print_opd(O, e, L);
         } else if (cmd == "path") {
             int L, N, m;
