@@ -43,6 +43,7 @@ CONFIGS = {
     "c1": dict(beta=(1, 2), n=64, p=3072, k=8, Ks=(2048, 3072)),
     "c2": dict(beta=(1, 1), n=256, p=6144, k=8, Ks=(2048, 3072)),
     "c3": dict(beta=(1, 3), n=512, p=36864, k=12, Ks=(3072, 4096)),
+    "c4": dict(beta=(1, 2), n=1024, p=49152, k=16, Ks=(4096, 5120)),
 }
 
 
