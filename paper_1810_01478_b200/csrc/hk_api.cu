@@ -95,6 +95,9 @@ struct hk_ctx {
     std::map<int, cudaGraphExec_t> graphs;
     std::map<int, long long> graph_launches;
     const void* graph_bufs[3] = {nullptr, nullptr, nullptr}; // S, R, B the graphs were captured on
+    std::map<long long, cudaGraphExec_t> inv_graphs;         // L^{-1} step graphs keyed by (n, m)
+    std::map<long long, long long> inv_graph_launches;
+    const void* inv_bufs[2] = {nullptr, nullptr};            // S, X they were captured on
     std::vector<uint32_t> h_limbs;
     std::vector<int32_t> h_e, h_s;
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
@@ -139,6 +142,9 @@ void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = 
     if (it == configured.end() || it->second < smem) {
         ck(cudaFuncSetAttribute(k_items<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem < 48 * 1024 ? 48 * 1024 : smem)),
            "cudaFuncSetAttribute");
+        // all of the unified L1/shared array as shared memory: residency is then
+        // register-bound (5 x 256-thread blocks at <= 48 registers)
+        ck(cudaFuncSetAttribute(k_items<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         configured[key] = smem < 48 * 1024 ? 48 * 1024 : smem;
     }
     long long blocks = (n + wpb - 1) / wpb;
@@ -359,6 +365,7 @@ void hk_destroy(hk_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : c->inv_graphs) cudaGraphExecDestroy(kv.second);
     for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M}) a->release();
     for (auto& s : c->shards) {
         for (DevArr* a : {&s.S, &s.panel, &s.R, &s.B}) a->release();
@@ -486,14 +493,40 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
         if (m < 1 || m > N) return fail(c, HK_ERR_INVALID, "invert_L_partial: need 1 <= m <= n");
         c->m = m;
         c->X.ensure((long long)N * m, L);
-        const int wo = ws_op_words(L);
-        ck(cudaEventRecord(c->ev[0], c->st), "event");
-        launch(c, hk::ItemInvInit{c->S.view(), c->X.view(), N, L, m}, (long long)N * m, 64);
-        for (int i = 0; i < N; ++i) {
-            const int b = i < m ? i : m;
-            const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
-            launch(c, hk::ItemInvStep{c->S.view(), c->X.view(), N, L, m, i}, items, wo);
+        // N latency-bound steps: one CTA per FMA, all steps in one cached graph
+        if (c->inv_bufs[0] != c->S.d || c->inv_bufs[1] != c->X.d) {
+            for (auto& kv : c->inv_graphs) cudaGraphExecDestroy(kv.second);
+            c->inv_graphs.clear();
+            c->inv_bufs[0] = c->S.d;
+            c->inv_bufs[1] = c->X.d;
         }
+        const long long key = ((long long)N << 20) | m;
+        auto it = c->inv_graphs.find(key);
+        if (it == c->inv_graphs.end()) {
+            const long long before = c->launches;
+            cudaGraph_t g;
+            ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            launch(c, hk::ItemInvInit{c->S.view(), c->X.view(), N, L, m}, (long long)N * m, 64);
+            for (int i = 0; i < N; ++i) {
+                const int b = i < m ? i : m;
+                const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
+                // few items: a CTA per FMA (latency); many: a warp per FMA (one wave)
+                if (items <= 4LL * c->sm_count)
+                    launch_cta(c, hk::CItemInvStep{c->S.view(), c->X.view(), N, L, m, i}, items, ws_cta_words(L));
+                else
+                    launch(c, hk::ItemInvStep{c->S.view(), c->X.view(), N, L, m, i}, items, ws_op_words(L));
+            }
+            ck(cudaStreamEndCapture(c->st, &g), "end capture");
+            cudaGraphExec_t ge;
+            ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            it = c->inv_graphs.emplace(key, ge).first;
+            c->inv_graph_launches[key] = c->launches - before;
+            c->launches = before;
+        }
+        ck(cudaEventRecord(c->ev[0], c->st), "event");
+        ck(cudaGraphLaunch(it->second, c->st), "graph launch");
+        c->launches += c->inv_graph_launches[key];
         ck(cudaEventRecord(c->ev[1], c->st), "event");
         ck(cudaEventSynchronize(c->ev[1]), "sync");
         float ms = 0;

@@ -424,6 +424,32 @@ struct CItemDMulB { // sharded: B_i(k) = RNE(panel_i(k) R_i)
     }
 };
 
+// L^{-1} step i with one CTA per item (the step is latency-bound: N sequential
+// steps of at most (N-i-1) min(m,i) independent FMAs) — same ops as ItemInvStep.
+struct CItemInvStep {
+    MpArr S, X;
+    int N, L, m, i;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const int b = i < m ? i : m;
+        const long long nfma = (long long)(N - i - 1) * b;
+        if (w < nfma) {
+            const int j = i + 1 + int(w / b), c = int(w % b);
+            const long long el = tri_idx(j, i, N);
+            const long long xc = (long long)j * m + c, xi = (long long)i * m + c;
+            uint32_t* o = X.limbs(xc, L);
+            cta_meta_store(X.m + xc, cta_fms(o, X.m[xc], S.limbs(el, L), S.m[el], X.limbs(xi, L), X.m[xi], o, L,
+                                             ctaws_carve(ws, L)));
+        } else {
+            const int j = i + 1 + int(w - nfma);
+            const long long el = tri_idx(j, i, N);
+            const long long xd = (long long)j * m + i;
+            for (int q = cta_tid(); q < L; q += cta_threads()) X.limbs(xd, L)[q] = S.limbs(el, L)[q];
+            if (cta_tid() == 0) X.m[xd] = Meta{S.m[el].exp, -S.m[el].sign};
+            cta_sync();
+        }
+    }
+};
+
 struct CItemBatch { // the CTA ops on batches (tests)
     MpArr A, B, C, O;
     int L, op;
