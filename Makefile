@@ -6,7 +6,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 CXX ?= g++
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v -DHK_TRAILING2_MINB=3
 CSRC := paper_1810_01478_b200/csrc
 HDRS := $(wildcard $(CSRC)/*.cuh) include/hankel_b200.h
 LIB := paper_1810_01478_b200/libhankel_b200.so

@@ -155,6 +155,41 @@ void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = 
     ++c->launches;
 }
 
+// The paired bulk update (hot kernel) with a residency bound on registers.
+template <class F>
+__global__ void __launch_bounds__(256, HK_TRAILING2_MINB) k_items_hot(long long n, int ws_words, F f) {
+    extern __shared__ uint32_t smem[];
+    const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    uint32_t* ws = smem + (size_t)wib * ws_words;
+    const long long nw = (long long)gridDim.x * wpb;
+    for (long long it = (long long)blockIdx.x * wpb + wib; it < n; it += nw) f(it, ws);
+}
+
+template <class F>
+void launch_hot(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = nullptr) {
+    if (n <= 0) return;
+    if (!st) st = c->st;
+    const size_t per_warp = size_t(ws_words) * sizeof(uint32_t);
+    int wpb = int((96 * 1024) / per_warp);
+    if (wpb > 8) wpb = 8;
+    if (wpb < 1) wpb = 1;
+    if ((long long)wpb > n) wpb = int(n);
+    const size_t smem = per_warp * wpb;
+    static std::map<const void*, size_t> configured;
+    const void* key = (const void*)&k_items_hot<F>;
+    auto it = configured.find(key);
+    if (it == configured.end() || it->second < smem) {
+        const size_t v = smem < 48 * 1024 ? 48 * 1024 : smem;
+        ck(cudaFuncSetAttribute(k_items_hot<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v)), "attr");
+        ck(cudaFuncSetAttribute(k_items_hot<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        configured[key] = v;
+    }
+    const long long blocks = (n + wpb - 1) / wpb;
+    k_items_hot<F><<<unsigned(blocks), unsigned(32 * wpb), smem, st>>>(n, ws_words, f);
+    ck(cudaGetLastError(), "kernel launch");
+    ++c->launches;
+}
+
 // One item per CTA (all warps cooperate on it): the critical-path ops.
 template <class F>
 __global__ void __launch_bounds__(256) k_cta_items(long long n, F f) {
@@ -278,7 +313,9 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     for (int i = 0; i < N; ++i) {
         ck(cudaStreamWaitEvent(bulk, evP[i], 0), "wait P");
         const long long nu = (long long)(N - i - 2) * (N - i - 1) / 2;
-        launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 2, c->d_err}, nu, wo, bulk);
+        (void)nu;
+        launch_hot(c, hk::ItemTrailing2{c->S.view(), b_buf(c, i), N, L, i, i + 2, c->d_err}, hk::trailing2_items(N, i + 2),
+               hk::opws2_words(L), bulk);
         if (i + 1 < N) {
             if (i > 0) ck(cudaStreamWaitEvent(la, evR[i - 1], 0), "wait R");
             launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err}, N - i - 1, wc, la);
@@ -748,8 +785,8 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
                            ws_cta_words(L));
             });
             timed(0, [&] {
-                launch(c, hk::ItemTrailing{c->S.view(), b_buf(c, i), N, L, i, i + 1, c->d_err},
-                       (long long)nb * (nb + 1) / 2, wo);
+                launch_hot(c, hk::ItemTrailing2{c->S.view(), b_buf(c, i), N, L, i, i + 1, c->d_err},
+                       hk::trailing2_items(N, i + 1), hk::opws2_words(L));
             });
             ++nt;
             timed(3, [&] { launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i), N, L, i}, nb, 64); });

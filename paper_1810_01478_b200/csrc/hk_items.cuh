@@ -120,6 +120,64 @@ struct ItemTrailing {
     }
 };
 
+// ---- the same bulk update with entries paired by row: columns j0, j0+1
+//      (j0 = jfirst + 2q) share y = B_i(k) for k >= j0+1, so one warp does
+//      both FMAs with one y stream (warp_fms2).  Items of pair q: index 0 is the
+//      diagonal single (j0, j0), index r >= 1 the row k = j0 + r; an odd last
+//      column (only row N-1) is one single item.  Same ops as ItemTrailing.
+HK_HD long long pair_items(int n0, int q) { return (long long)q * n0 - (long long)q * (q - 1); }
+HK_HD long long trailing2_items(int N, int jfirst) {
+    const int n0 = N - jfirst;
+    if (n0 <= 0) return 0;
+    return pair_items(n0, n0 / 2) + (n0 & 1);
+}
+
+struct ItemTrailing2 {
+    MpArr S, B;
+    int N, L, i, jfirst;
+    const int* err;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int n0 = N - jfirst, np = n0 / 2;
+        int q = 0;
+        if (w >= pair_items(n0, np)) {
+            q = np; // odd last column: (N-1, N-1)
+        } else {
+            const double b = n0 + 1.0;
+            q = int((b - sqrt(b * b - 4.0 * double(w))) * 0.5);
+            if (q < 0) q = 0;
+            if (q > np - 1) q = np - 1;
+            while (q > 0 && pair_items(n0, q) > w) --q;
+            while (q + 1 < np && pair_items(n0, q + 1) <= w) ++q;
+        }
+        const int j0 = jfirst + 2 * q;
+        const int r = int(w - pair_items(n0, q));
+        const long long ex0 = tri_idx(j0, i, N);
+        if (q == np || r == 0) { // single: (j0, j0) or the odd last column
+            const int k = j0;
+            const long long ec = tri_idx(k, j0, N);
+            uint32_t* c = S.limbs(ec, L);
+            const Meta m = warp_fms(c, S.m[ec], S.limbs(ex0, L), S.m[ex0], B.limbs(k, L), B.m[k], c, L,
+                                    opws_carve(ws, L));
+            if (lane() == 0) S.m[ec] = m;
+            wsync();
+            return;
+        }
+        const int k = j0 + r;
+        const long long ec0 = tri_idx(k, j0, N), ec1 = tri_idx(k, j0 + 1, N), ex1 = tri_idx(j0 + 1, i, N);
+        uint32_t* c0 = S.limbs(ec0, L);
+        uint32_t* c1 = S.limbs(ec1, L);
+        Meta m0, m1;
+        warp_fms2(c0, S.m[ec0], S.limbs(ex0, L), S.m[ex0], c1, S.m[ec1], S.limbs(ex1, L), S.m[ex1], B.limbs(k, L),
+                  B.m[k], c0, c1, m0, m1, L, ws);
+        if (lane() == 0) {
+            S.m[ec0] = m0;
+            S.m[ec1] = m1;
+        }
+        wsync();
+    }
+};
+
 // ---- column i of S <- B_i (L(k,i) stored in place), k = i+1+t
 struct ItemStoreL {
     MpArr S, B;

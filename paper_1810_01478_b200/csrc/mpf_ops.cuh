@@ -110,6 +110,45 @@ HK_DEV Meta warp_mulr(const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym, 
     return Meta{r.exp, r.sign};
 }
 
+// ---- paired FMA: out_q = RNE(c_q - x_q y) for q = 0, 1 with a shared y.
+// Scratch (words): A0 [L] | A1 [L] | Bp [L+64] | P0 [2L] | P1 [2L]  (7L + 64);
+// the rounding window reuses A0.. (>= L + 10 words needed), and a Ziv fallback
+// of member 0 (single-FMA path, which clobbers [0, 4L+64)) leaves P1 intact.
+HK_HD int opws2_words(int L) { return 7 * L + 64; }
+
+HK_DEV void warp_fms2(const uint32_t* c0, Meta cm0, const uint32_t* x0, Meta xm0, const uint32_t* c1, Meta cm1,
+                      const uint32_t* x1, Meta xm1, const uint32_t* yd, Meta ym, uint32_t* out0, uint32_t* out1,
+                      Meta& r0, Meta& r1, int L, uint32_t* ws) {
+    uint32_t* A0 = ws;
+    uint32_t* A1 = ws + L;
+    uint32_t* Bp = ws + 2 * L;
+    uint32_t* P0 = ws + 3 * L + 64;
+    uint32_t* P1 = ws + 5 * L + 64;
+    const int t0 = L > kGuardLimbs ? L - kGuardLimbs : 0;
+    const int sp0 = -(xm0.sign * ym.sign), sp1 = -(xm1.sign * ym.sign);
+    if (t0 == 0 || sp0 == 0 || sp1 == 0 || (reinterpret_cast<uintptr_t>(A1) & 15)) { // rare / tiny: single path
+        r0 = warp_fms(c0, cm0, x0, xm0, yd, ym, out0, L, opws_carve(ws, L));
+        r1 = warp_fms(c1, cm1, x1, xm1, yd, ym, out1, L, opws_carve(ws, L));
+        return;
+    }
+    warp_copy(A0, x0, L);
+    warp_copy(A1, x1, L);
+    warp_stage_padded(Bp, yd, L);
+    wsync();
+    warp_mul2(A0, A1, L, Bp, L, P0, P1, t0);
+    wsync();
+    const int lsb0 = xm0.exp + ym.exp - 64 * L, lsb1 = xm1.exp + ym.exp - 64 * L;
+    bool ok = false;
+    RMeta a = warp_round_sum(Opd{c0, L, cm0.exp - 32 * L, cm0.sign}, Opd{P0 + t0, 2 * L - t0, lsb0 + 32 * t0, sp0},
+                             ws, out0, L, lsb0 + 32 * t0 + 46, &ok);
+    if (ok) r0 = Meta{a.exp, a.sign};
+    else r0 = warp_fms(c0, cm0, x0, xm0, yd, ym, out0, L, opws_carve(ws, L));
+    a = warp_round_sum(Opd{c1, L, cm1.exp - 32 * L, cm1.sign}, Opd{P1 + t0, 2 * L - t0, lsb1 + 32 * t0, sp1}, ws, out1,
+                       L, lsb1 + 32 * t0 + 46, &ok);
+    if (ok) r1 = Meta{a.exp, a.sign};
+    else r1 = warp_fms(c1, cm1, x1, xm1, yd, ym, out1, L, opws_carve(ws, L));
+}
+
 // out = RNE(x + y); x, y may alias out.
 HK_DEV Meta warp_addr(const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym, uint32_t* out, int L,
                       const OpWs& ws) {

@@ -247,6 +247,47 @@ HK_DEV void colsum_group(const uint32_t* A, int nA, const uint32_t* Bp, int nB, 
     add96(a0, a1, a2, uint32_t(q3), uint32_t(q3 >> 32), h3);
 }
 
+// Two column sums sharing the y operand: columns t = g0 + lane of A0*B and
+// A1*B.  Each per-lane y load feeds two MACs (the bulk LDLT update pairs the
+// entries (k, j) and (k, j+1), which share y = B_i(k)).
+HK_DEV void colsum_group2(const uint32_t* A0, const uint32_t* A1, int nA, const uint32_t* Bp, int nB, int g0,
+                          uint32_t (&r0)[3], uint32_t (&r1)[3]) {
+    const int t = g0 + lane();
+    const int slo = max(0, g0 - (nB - 1));
+    const int shi = min(g0 + 31, nA - 1);
+    uint64_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;
+    uint32_t hp0 = 0, hp1 = 0, hq0 = 0, hq1 = 0;
+    const uint32_t* yb = Bp + 32 + t;
+    int s = slo;
+    for (; s <= shi && (s & 3); ++s) {
+        const uint32_t y = yb[-s];
+        mac64(p0, hp0, A0[s], y);
+        mac64(q0, hq0, A1[s], y);
+    }
+    for (; s + 3 <= shi; s += 4) {
+        const uint4 xa = *reinterpret_cast<const uint4*>(A0 + s);
+        const uint4 xb = *reinterpret_cast<const uint4*>(A1 + s);
+        const uint32_t y0 = yb[-s], y1 = yb[-s - 1], y2 = yb[-s - 2], y3 = yb[-s - 3];
+        mac64x2(p0, hp0, xa.x, y0, xa.z, y2);
+        mac64x2(p1, hp1, xa.y, y1, xa.w, y3);
+        mac64x2(q0, hq0, xb.x, y0, xb.z, y2);
+        mac64x2(q1, hq1, xb.y, y1, xb.w, y3);
+    }
+    for (; s <= shi; ++s) {
+        const uint32_t y = yb[-s];
+        mac64(p0, hp0, A0[s], y);
+        mac64(q0, hq0, A1[s], y);
+    }
+    r0[0] = uint32_t(p0);
+    r0[1] = uint32_t(p0 >> 32);
+    r0[2] = hp0;
+    add96(r0[0], r0[1], r0[2], uint32_t(p1), uint32_t(p1 >> 32), hp1);
+    r1[0] = uint32_t(q0);
+    r1[1] = uint32_t(q0 >> 32);
+    r1[2] = hq0;
+    add96(r1[0], r1[1], r1[2], uint32_t(q1), uint32_t(q1 >> 32), hq1);
+}
+
 // Running state of the column-sum -> limb carry resolution (warp-uniform).
 struct CarryState {
     uint32_t cin = 0, hi_prev = 0, a1p = 0, a2p31 = 0, a2p30 = 0;
@@ -287,6 +328,24 @@ HK_DEV void warp_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint
         const uint32_t w = carry_group(cs, a0, a1, a2);
         const int t = g0 + lane();
         if (t < ntot) P[t] = w;
+    }
+}
+
+// P0 = A0*B, P1 = A1*B (from column tfirst), sharing the staged B.
+HK_DEV void warp_mul2(const uint32_t* A0, const uint32_t* A1, int nA, const uint32_t* Bp, int nB, uint32_t* P0,
+                      uint32_t* P1, int tfirst) {
+    const int ntot = nA + nB;
+    CarryState c0, c1;
+    for (int g0 = tfirst; g0 < ntot; g0 += 32) {
+        uint32_t r0[3], r1[3];
+        colsum_group2(A0, A1, nA, Bp, nB, g0, r0, r1);
+        const uint32_t w0 = carry_group(c0, r0[0], r0[1], r0[2]);
+        const uint32_t w1 = carry_group(c1, r1[0], r1[1], r1[2]);
+        const int t = g0 + lane();
+        if (t < ntot) {
+            P0[t] = w0;
+            P1[t] = w1;
+        }
     }
 }
 

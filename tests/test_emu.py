@@ -42,7 +42,7 @@ def test_emulated_ops_match_model(emu_bin, L):
             assert from_line(r, L) == F.recip(d, p)
 
 
-@pytest.mark.parametrize("beta,N,L,m", [((1, 2), 8, 4, 4), ((1, 1), 12, 3, 5), ((1, 3), 6, 8, 6),
+@pytest.mark.parametrize("beta,N,L,m", [((1, 2), 8, 4, 4), ((1, 1), 12, 3, 5), ((1, 3), 6, 8, 6), ((1, 2), 11, 8, 4),
                                         ((1, 2), 3, 4, 3), ((1, 2), 1, 2, 1)])
 def test_emulated_path_matches_model(emu_bin, beta, N, L, m):
     p = 32 * L

@@ -107,7 +107,9 @@ int main() {
                 if (err >= 0) break;
                 const int nb = N - i - 1;
                 run_items(nb, ws, ItemMulB{S.view(), R.view(), Bq.view(), N, L, i, &err});
-                run_items((long long)nb * (nb + 1) / 2, ws, ItemTrailing{S.view(), Bq.view(), N, L, i, i + 1, &err});
+                // paired bulk kernel (ItemTrailing2) as the device path runs it
+                const int ws2 = opws2_words(L) > ws ? opws2_words(L) : ws;
+                run_items(trailing2_items(N, i + 1), ws2, ItemTrailing2{S.view(), Bq.view(), N, L, i, i + 1, &err});
                 run_items(nb, ws, ItemStoreL{S.view(), Bq.view(), N, L, i});
             }
             if (err < 0) {

@@ -9,6 +9,6 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 if [ "${NCU:-1}" = "1" ]; then
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-$CMD > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:ItemTrailing -s 20 -c 2 -o gpurun_out/prof_trailing $CMD > gpurun_out/ncu_full.log 2>&1
+$CMD > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:ItemTrailing2 -s 20 -c 2 -o gpurun_out/prof_trailing $CMD > gpurun_out/ncu_full.log 2>&1
 fi
 echo done
