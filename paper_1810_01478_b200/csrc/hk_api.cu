@@ -10,6 +10,7 @@
 // item sees it and returns, and the host maps it to HK_ERR_PRECISION.
 #include "../../include/hankel_b200.h"
 #include "hk_items.cuh"
+#include "tc_bulk.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -95,11 +96,16 @@ struct hk_ctx {
     std::map<int, cudaGraphExec_t> graphs;
     std::map<int, long long> graph_launches;
     const void* graph_bufs[3] = {nullptr, nullptr, nullptr}; // S, R, B the graphs were captured on
+    const void* graph_tcp = nullptr;                         // tc scratch they were captured on
+    bool graph_tc = false;
     std::map<long long, cudaGraphExec_t> inv_graphs;         // L^{-1} step graphs keyed by (n, m)
     std::map<long long, long long> inv_graph_launches;
     const void* inv_bufs[2] = {nullptr, nullptr};            // S, X they were captured on
     std::vector<uint32_t> h_limbs;
     std::vector<int32_t> h_e, h_s;
+    // ---- tensor-core bulk products (large p): scratch of short products
+    uint32_t* tc_P = nullptr;
+    size_t tc_P_words = 0;
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
     struct Shard {
         int rank = 0;
@@ -297,6 +303,51 @@ MpArr b_buf(hk_ctx* c, int i) {
 // U(i) needs B_i (end of P(i)); P(i+1) needs column i+1 after step i-1 (end of
 // U(i-1)+STORE(i-1)); STORE(i) needs P(i+1) to have read S(i+1,i).  So P(i+1)
 // overlaps U(i) and the critical path per step is max(U(i), P(i+1)).
+// Tensor-core products for the bulk update?  Default: when p >= 8192 bits and
+// the per-CTA shared memory fits; HK_TC=0/1 forces it off/on (tests, sweeps).
+bool use_tc(const hk_ctx* c) {
+    const int L = c->L;
+    if (L % 4 != 0 || hk::tc_smem_bytes(L) > 220 * 1024) return false;
+    if (const char* e = getenv("HK_TC")) return e[0] == '1';
+    return L >= 256;
+}
+
+// Step-i update of columns jfirst..N-1 (bulk): IMAD paired warp FMAs, or the
+// tcgen05 product kernel followed by the certified rounding pass.
+void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
+    const int N = c->n, L = c->L;
+    const int ncols = N - jfirst;
+    if (ncols <= 0) return;
+    if (!use_tc(c)) {
+        launch_hot(c, hk::ItemTrailing2{c->S.view(), b_buf(c, i), N, L, i, jfirst, c->d_err},
+                   hk::trailing2_items(N, jfirst), hk::opws2_words(L), st);
+        return;
+    }
+    const size_t smem = hk::tc_smem_bytes(L);
+    static bool configured = false;
+    if (!configured) {
+        ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");
+        configured = true;
+    }
+    hk::TcBulkArgs a{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err};
+    const dim3 grid(unsigned(ncols), unsigned((ncols + hk::kTcRows - 1) / hk::kTcRows));
+    hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
+    ck(cudaGetLastError(), "tc bulk launch");
+    ++c->launches;
+    launch(c, hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err},
+           (long long)ncols * (ncols + 1) / 2, ws_op_words(L), st);
+}
+
+void ensure_tc_scratch(hk_ctx* c) {
+    if (!use_tc(c)) return;
+    const size_t need = (size_t)c->n * (c->n + 1) / 2 * hk::tc_scratch_limbs(c->L);
+    if (c->tc_P_words >= need) return;
+    if (c->tc_P) cudaFree(c->tc_P);
+    c->tc_P = nullptr;
+    ck(cudaMalloc(&c->tc_P, need * sizeof(uint32_t)), "cudaMalloc tc scratch");
+    c->tc_P_words = need;
+}
+
 void enqueue_ldlt_steps(hk_ctx* c) {
     const int N = c->n, L = c->L;
     const int wo = ws_op_words(L), wr = ws_recip_words(L);
@@ -314,8 +365,7 @@ void enqueue_ldlt_steps(hk_ctx* c) {
         ck(cudaStreamWaitEvent(bulk, evP[i], 0), "wait P");
         const long long nu = (long long)(N - i - 2) * (N - i - 1) / 2;
         (void)nu;
-        launch_hot(c, hk::ItemTrailing2{c->S.view(), b_buf(c, i), N, L, i, i + 2, c->d_err}, hk::trailing2_items(N, i + 2),
-               hk::opws2_words(L), bulk);
+        enqueue_bulk(c, i, i + 2, bulk);
         if (i + 1 < N) {
             if (i > 0) ck(cudaStreamWaitEvent(la, evR[i - 1], 0), "wait R");
             launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err}, N - i - 1, wc, la);
@@ -416,6 +466,7 @@ void hk_destroy(hk_ctx* c) {
         if (destroy) destroy(c->nccl_comm);
     }
     if (c->d_err) cudaFree(c->d_err);
+    if (c->tc_P) cudaFree(c->tc_P);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);
@@ -462,12 +513,16 @@ int hk_ldlt(hk_ctx* c) {
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
         c->B.ensure(2LL * N, L);
+        ensure_tc_scratch(c);
         ensure_step_events(c, N);
         c->bad_col = -1;
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         ck(cudaEventRecord(c->ev[0], c->st), "event");
         launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
-        if (c->graph_bufs[0] != c->S.d || c->graph_bufs[1] != c->R.d || c->graph_bufs[2] != c->B.d) {
+        if (c->graph_bufs[0] != c->S.d || c->graph_bufs[1] != c->R.d || c->graph_bufs[2] != c->B.d ||
+            c->graph_tcp != c->tc_P || c->graph_tc != use_tc(c)) {
+            c->graph_tcp = c->tc_P;
+            c->graph_tc = use_tc(c);
             for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
             c->graphs.clear();
             c->graph_bufs[0] = c->S.d;
@@ -752,6 +807,7 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
         c->B.ensure(2LL * N, L);
+        ensure_tc_scratch(c);
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         struct Rec {
             int kind;
@@ -785,8 +841,7 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
                            ws_cta_words(L));
             });
             timed(0, [&] {
-                launch_hot(c, hk::ItemTrailing2{c->S.view(), b_buf(c, i), N, L, i, i + 1, c->d_err},
-                       hk::trailing2_items(N, i + 1), hk::opws2_words(L));
+                enqueue_bulk(c, i, i + 1, c->st);
             });
             ++nt;
             timed(3, [&] { launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i), N, L, i}, nb, 64); });

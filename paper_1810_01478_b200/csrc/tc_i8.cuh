@@ -1,0 +1,89 @@
+// tc_i8.cuh — thin sm_100a wrappers for 5th-gen tensor-core int8 MMAs
+// (tcgen05.mma.cta_group::1.kind::i8, u8 x u8 -> s32 in TMEM), used for the
+// limb products of large-p MP-FMAs.  Descriptor bit layouts follow the PTX ISA
+// (mirrored in CUTLASS cute/arch/mma_sm100_desc.hpp: SmemDescriptor,
+// InstrDescriptor); only SWIZZLE_NONE ("interleaved") canonical layouts are used:
+//   K-major  : core matrix = 8 rows x 16 B (rows 16 B apart, 128 B contiguous);
+//              SBO = byte stride between 8-row groups, LBO = between 16 B K-chunks.
+//   MN-major : core matrix = 8 K-rows x 16 B of MN (K-rows 16 B apart);
+//              SBO = byte stride between 16-element MN blocks, LBO = between
+//              8-row K groups.
+#pragma once
+
+#include <cstdint>
+
+namespace hk {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// SWIZZLE_NONE shared-memory matrix descriptor (version 1 = Blackwell).
+__device__ __forceinline__ uint64_t sdesc(const void* smem, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    const uint64_t a = (smem_u32(smem) >> 4) & 0x3fffu;
+    const uint64_t l = (lbo_bytes >> 4) & 0x3fffu;
+    const uint64_t s = (sbo_bytes >> 4) & 0x3fffu;
+    return a | (l << 16) | (s << 32) | (1ull << 46); // base_offset 0, lbo_mode 0, layout 0
+}
+
+// Instruction descriptor: u8 x u8 -> s32, dense, M x N, A/B majorness.
+__host__ __device__ constexpr uint32_t idesc_u8(int M, int N, bool a_mn_major, bool b_mn_major) {
+    return (2u << 4)                                  // c_format = S32
+           | (0u << 7) | (0u << 10)                   // a/b format = unsigned 8-bit
+           | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+           (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// warp-wide: allocate `ncols` TMEM columns (power of two >= 32), address -> *dst (smem)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// warp-wide: 8 consecutive 32-bit columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+} // namespace tc
+} // namespace hk
