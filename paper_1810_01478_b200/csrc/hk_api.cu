@@ -106,6 +106,8 @@ struct hk_ctx {
     // ---- tensor-core bulk products (large p): scratch of short products
     uint32_t* tc_P = nullptr;
     size_t tc_P_words = 0;
+    int* tc_fb_count = nullptr;   // uncertified items of the current step
+    long long* tc_fb = nullptr;
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
     struct Shard {
         int rank = 0;
@@ -334,8 +336,21 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
     hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
     ck(cudaGetLastError(), "tc bulk launch");
     ++c->launches;
-    launch(c, hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err},
-           (long long)ncols * (ncols + 1) / 2, ws_op_words(L), st);
+    ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
+    launch(c,
+           hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count, c->tc_fb},
+           (long long)ncols * (ncols + 1) / 2, hk::tcround_words(L), st);
+    const int wo = ws_op_words(L);
+    const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
+    static bool fix_cfg = false;
+    if (!fix_cfg) {
+        ck(cudaFuncSetAttribute(hk::k_tc_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "fix attr");
+        fix_cfg = true;
+    }
+    hk::k_tc_fix<<<unsigned(c->sm_count), unsigned(32 * wpb), size_t(wo) * 4 * wpb, st>>>(
+        c->S.view(), b_buf(c, i), N, L, i, jfirst, c->tc_fb_count, c->tc_fb, wo);
+    ck(cudaGetLastError(), "tc fix launch");
+    ++c->launches;
 }
 
 void ensure_tc_scratch(hk_ctx* c) {
@@ -343,8 +358,12 @@ void ensure_tc_scratch(hk_ctx* c) {
     const size_t need = (size_t)c->n * (c->n + 1) / 2 * hk::tc_scratch_limbs(c->L);
     if (c->tc_P_words >= need) return;
     if (c->tc_P) cudaFree(c->tc_P);
+    if (c->tc_fb) cudaFree(c->tc_fb);
+    if (!c->tc_fb_count) ck(cudaMalloc(&c->tc_fb_count, sizeof(int)), "cudaMalloc fb count");
     c->tc_P = nullptr;
+    c->tc_fb = nullptr;
     ck(cudaMalloc(&c->tc_P, need * sizeof(uint32_t)), "cudaMalloc tc scratch");
+    ck(cudaMalloc(&c->tc_fb, (size_t)c->n * (c->n + 1) / 2 * sizeof(long long)), "cudaMalloc fb list");
     c->tc_P_words = need;
 }
 
@@ -467,6 +486,8 @@ void hk_destroy(hk_ctx* c) {
     }
     if (c->d_err) cudaFree(c->d_err);
     if (c->tc_P) cudaFree(c->tc_P);
+    if (c->tc_fb) cudaFree(c->tc_fb);
+    if (c->tc_fb_count) cudaFree(c->tc_fb_count);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);

@@ -30,12 +30,14 @@ constexpr int kTcN = 256;        // N per MMA (TMEM columns)
 constexpr int kTcK = 32;         // K per MMA (bytes)
 constexpr int kTcGuard = 8;      // short product from limb L - 8
 constexpr int kTcThreads = 128;  // 4 warps: one thread per row / TMEM lane
+constexpr int kTcKB = 4;         // MMAs (K-steps) per staged A block
+constexpr int kTcABuf = 4096 * kTcKB; // bytes per A buffer (2 buffers)
 
 HK_HD int tc_nb(int L) { return 4 * L; }
 HK_HD int tc_ncell(int L) { return tc_nb(L) + 352; }        // cells p in [-31, nb + 321)
 HK_HD int tc_sx_words(int L) { return (tc_nb(L) + 512) / 4; }
 HK_HD size_t tc_smem_bytes(int L) {
-    return 4096 + 16 * (size_t)tc_ncell(L) + 4 * (size_t)tc_sx_words(L) + 64;
+    return 2 * (size_t)kTcABuf + 16 * (size_t)tc_ncell(L) + 4 * (size_t)tc_sx_words(L) + 64;
 }
 HK_HD int tc_scratch_limbs(int L) { return L + kTcGuard; }  // limbs [L-8, 2L)
 
@@ -49,7 +51,7 @@ struct TcBulkArgs {
 // blockIdx.x: column offset (j = jfirst + x); blockIdx.y: row tile (k0 = j + 128 y)
 __global__ void __launch_bounds__(kTcThreads) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbarb[2];
     __shared__ uint32_t taddr_s;
     if (*(volatile const int*)a.err >= 0) return;
     const int N = a.N, L = a.L, nb = tc_nb(L);
@@ -57,8 +59,8 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_bulk(TcBulkArgs a) {
     const int k0 = j + kTcRows * int(blockIdx.y);
     if (j >= N || k0 >= N) return;
     const int tid = threadIdx.x, warp = tid >> 5;
-    uint8_t* sA = tsm;                                   // 4 KB: 128 rows x 32 B, K-major core matrices
-    uint8_t* sE = tsm + 4096;                            // expanded x cells
+    uint8_t* sA = tsm;                                   // 2 x 16 KB: A blocks (4 K-major 128 x 32 B tiles)
+    uint8_t* sE = tsm + 2 * kTcABuf;                     // expanded x cells
     uint32_t* sX = reinterpret_cast<uint32_t*>(sE + 16 * (size_t)tc_ncell(L)); // x bytes, 32-byte zero pad
     const int pmin = -31;
 
@@ -81,13 +83,15 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_bulk(TcBulkArgs a) {
         *reinterpret_cast<uint4*>(sE + 16 * (size_t)c) = v;
     }
     if (warp == 0) tc::tmem_alloc(&taddr_s, kTcN);
-    if (tid == 0) tc::mbar_init(&mbar, 1);
+    if (tid == 0) {
+        tc::mbar_init(&mbarb[0], 1);
+        tc::mbar_init(&mbarb[1], 1);
+    }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = taddr_s;
     const uint32_t idesc = tc::idesc_u8(kTcRows, kTcN, false, true);
-    uint32_t phase = 0;
 
     const int r = tid;            // this thread's row / TMEM lane
     const int k = k0 + r;
@@ -97,39 +101,67 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_bulk(TcBulkArgs a) {
     uint32_t* Pout = a.P + item * (long long)tc_scratch_limbs(L);
     const uint32_t* yl_row = a.B.limbs(row_ok ? k : k0, L);
     uint64_t carry = 0;
+    uint32_t bph[2] = {0u, 0u}; // per-buffer mbarrier phases
+
+    // stage the A K-block `blk` (kTcKB MMAs = 128 rows x 128 B) into buffer `buf`
+    auto stage = [&](int blk, int buf, int ksteps) {
+        uint8_t* dst = sA + buf * kTcABuf;
+        for (int q = tid; q < kTcRows * 2 * kTcKB; q += kTcThreads) {
+            const int sub = q / (kTcRows * 2), qq = q % (kTcRows * 2);
+            const int rr = qq >> 1, h = qq & 1;
+            const int ks = blk * kTcKB + sub;
+            const int u0 = ks * kTcK + 16 * h;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (ks < ksteps && k0 + rr < N && u0 < nb) {
+                // Yr[u0 .. u0+15] = Y[nb-1-u0 .. nb-16-u0] = reversed limbs [L-4-u0/4, L-u0/4)
+                const uint4 g = *reinterpret_cast<const uint4*>(a.B.limbs(k0 + rr, L) + (L - 4 - u0 / 4));
+                v.x = __byte_perm(g.w, 0u, 0x0123);
+                v.y = __byte_perm(g.z, 0u, 0x0123);
+                v.z = __byte_perm(g.y, 0u, 0x0123);
+                v.w = __byte_perm(g.x, 0u, 0x0123);
+            }
+            *reinterpret_cast<uint4*>(dst + sub * 4096 + (rr >> 3) * 256 + h * 128 + (rr & 7) * 16) = v;
+        }
+        tc::fence_async_smem();
+    };
 
     for (int tc0 = -31, ch = 0; tc0 < nb + 1; tc0 += kTcN, ++ch) {
         const int u_hi = tc0 < 0 ? nb : nb - tc0;             // u' < u_hi contribute
         const int ksteps = (u_hi + kTcK - 1) / kTcK;
-        for (int ks = 0; ks < ksteps; ++ks) {
-            // stage A: rows k0.., bytes u' in [32 ks, 32 ks + 32) of reversed y
-            for (int q = tid; q < kTcRows * 2; q += kTcThreads) {
-                const int rr = q >> 1, h = q & 1;
-                const int u0 = ks * kTcK + 16 * h;
-                uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                if (k0 + rr < N && u0 < nb) {
-                    // Yr[u0 .. u0+15] = Y[nb-1-u0 .. nb-16-u0] = reversed limbs [L-4-u0/4, L-u0/4)
-                    const uint4 g = *reinterpret_cast<const uint4*>(a.B.limbs(k0 + rr, L) + (L - 4 - u0 / 4));
-                    v.x = __byte_perm(g.w, 0u, 0x0123);
-                    v.y = __byte_perm(g.z, 0u, 0x0123);
-                    v.z = __byte_perm(g.y, 0u, 0x0123);
-                    v.w = __byte_perm(g.x, 0u, 0x0123);
-                }
-                *reinterpret_cast<uint4*>(sA + (rr >> 3) * 256 + h * 128 + (rr & 7) * 16) = v;
-            }
-            tc::fence_async_smem();
-            __syncthreads();
+        const int nblk = (ksteps + kTcKB - 1) / kTcKB;
+        // double-buffered pipeline: MMAs of block b run while block b+1 is staged
+        stage(0, 0, ksteps);
+        __syncthreads();
+        for (int b = 0; b < nblk; ++b) {
+            const int buf = b & 1;
             if (tid == 0) {
                 tc::fence_after();
-                const uint64_t ad = tc::sdesc(sA, 128, 256);
-                const uint64_t bd = tc::sdesc(sE + 16 * (size_t)(tc0 + ks * kTcK - pmin), 128, 256);
-                tc::mma_i8(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
-                tc::commit(&mbar);
+                for (int sub = 0; sub < kTcKB; ++sub) {
+                    const int ks = b * kTcKB + sub;
+                    if (ks >= ksteps) break;
+                    const uint64_t ad = tc::sdesc(sA + buf * kTcABuf + sub * 4096, 128, 256);
+                    const uint64_t bd = tc::sdesc(sE + 16 * (size_t)(tc0 + ks * kTcK - pmin), 128, 256);
+                    tc::mma_i8(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
+                }
+                tc::commit(&mbarb[buf]);
             }
-            tc::mbar_wait(&mbar, phase);
-            phase ^= 1;
-            tc::fence_after();
+            if (b + 1 < nblk) {
+                if (b >= 1) { // buffer (b+1)&1 was last read by block b-1's MMAs
+                    tc::mbar_wait(&mbarb[(b + 1) & 1], bph[(b + 1) & 1]);
+                    bph[(b + 1) & 1] ^= 1u;
+                }
+                stage(b + 1, (b + 1) & 1, ksteps);
+            }
+            __syncthreads();
         }
+        // drain: the last block's commit (and the one before, if not yet awaited)
+        if (nblk >= 2) {
+            tc::mbar_wait(&mbarb[(nblk - 2) & 1], bph[(nblk - 2) & 1]);
+            bph[(nblk - 2) & 1] ^= 1u;
+        }
+        tc::mbar_wait(&mbarb[(nblk - 1) & 1], bph[(nblk - 1) & 1]);
+        bph[(nblk - 1) & 1] ^= 1u;
+        tc::fence_after();
         // epilogue: this row's 256 byte-column sums -> 64 limbs (exact carries)
         for (int c8 = 0; c8 < kTcN; c8 += 8) {
             uint32_t v[8];
@@ -157,11 +189,18 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_bulk(TcBulkArgs a) {
 // Second pass: S(k,j) = RNE(S(k,j) - x_j y_k) from the scratch product, with the
 // Ziv certificate; exact warp FMA when it cannot certify.  Items enumerate the
 // column-major triangle of columns jfirst..N-1 (as ItemTrailing / the scratch).
+// The window needs max(L, L+8, L) + 4 words; the rare items the certificate
+// cannot settle are appended to `fb` and redone exactly by k_tc_fix (so this
+// pass runs at high occupancy with a window-sized workspace).
+HK_HD int tcround_words(int L) { return (L + 16 + 3) & ~3; }
+
 struct ItemTcRound {
     MpArr S, B;
     const uint32_t* P;
     int N, L, i, jfirst;
     const int* err;
+    int* fb_count;
+    long long* fb;
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         if (*(volatile const int*)err >= 0) return;
         const int n2 = N - jfirst;
@@ -172,22 +211,48 @@ struct ItemTcRound {
         const Meta cm = S.m[ec], xm = S.m[ex], ym = B.m[k];
         uint32_t* c = S.limbs(ec, L);
         const int sp = -(xm.sign * ym.sign);
+        if (sp == 0) return; // x or y zero: RNE(c - 0) = c, nothing to write
         const int t0 = L - kTcGuard;
         const int lsbP = xm.exp + ym.exp - 64 * L;
-        Meta r;
-        if (sp != 0) {
-            const Opd X{c, L, cm.exp - 32 * L, cm.sign};
-            const Opd Y{P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L), lsbP + 32 * t0, sp};
-            bool ok = false;
-            const RMeta rr = warp_round_sum(X, Y, ws, c, L, lsbP + 32 * t0 + 46, &ok);
-            if (ok) r = Meta{rr.exp, rr.sign};
-            else r = warp_fms(c, cm, S.limbs(ex, L), xm, B.limbs(k, L), ym, c, L, opws_carve(ws, L));
-        } else {
-            r = cm; // x or y zero: c unchanged (RNE(c) = c)
+        const Opd X{c, L, cm.exp - 32 * L, cm.sign};
+        const Opd Y{P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L), lsbP + 32 * t0, sp};
+        bool ok = false;
+        const RMeta rr = warp_round_sum(X, Y, ws, c, L, lsbP + 32 * t0 + 46, &ok);
+        if (lane() == 0) {
+            if (ok) {
+                S.m[ec] = Meta{rr.exp, rr.sign};
+            } else {
+#if defined(HK_WARP_EMU)
+                fb[(*fb_count)++] = w;
+#else
+                fb[atomicAdd(fb_count, 1)] = w;
+#endif
+            }
         }
-        if (lane() == 0) S.m[ec] = r;
         wsync();
     }
 };
+
+#if !defined(HK_WARP_EMU)
+// Exact redo of the uncertified items: S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)).
+__global__ void __launch_bounds__(256) k_tc_fix(MpArr S, MpArr B, int N, int L, int i, int jfirst,
+                                                const int* fb_count, const long long* fb, int ws_words) {
+    extern __shared__ uint32_t fsm[];
+    const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    uint32_t* ws = fsm + (size_t)wib * ws_words;
+    const int cnt = *fb_count;
+    for (long long q = (long long)blockIdx.x * wpb + wib; q < cnt; q += (long long)gridDim.x * wpb) {
+        const long long w = fb[q];
+        int jj, kk;
+        tri_decode(w, N - jfirst, jj, kk);
+        const int j = jfirst + jj, k = jfirst + kk;
+        const long long ec = tri_idx(k, j, N), ex = tri_idx(j, i, N);
+        uint32_t* c = S.limbs(ec, L);
+        const Meta m = warp_fms(c, S.m[ec], S.limbs(ex, L), S.m[ex], B.limbs(k, L), B.m[k], c, L, opws_carve(ws, L));
+        if (lane() == 0) S.m[ec] = m;
+        wsync();
+    }
+}
+#endif
 
 } // namespace hk
