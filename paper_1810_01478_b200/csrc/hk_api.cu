@@ -106,6 +106,7 @@ struct hk_ctx {
     // ---- tensor-core bulk products (large p): scratch of short products
     uint32_t* tc_P = nullptr;
     size_t tc_P_words = 0;
+    uint8_t* tc_A = nullptr;      // preformatted A operand of the current step
     int* tc_fb_count = nullptr;   // uncertified items of the current step
     long long* tc_fb = nullptr;
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
@@ -325,14 +326,20 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
                    hk::trailing2_items(N, jfirst), hk::opws2_words(L), st);
         return;
     }
-    const size_t smem = hk::tc_smem_bytes(L);
+    // one CTA per SM (it owns all 512 TMEM columns)
+    const size_t smem = std::max(hk::tc_smem_bytes(L), size_t(120 * 1024));
     static bool configured = false;
     if (!configured) {
         ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");
         configured = true;
     }
-    hk::TcBulkArgs a{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err};
-    const dim3 grid(unsigned(ncols), unsigned((ncols + hk::kTcRows - 1) / hk::kTcRows));
+    const long long nprep = (long long)(hk::tc_apre_bytes(N, L) / 16);
+    hk::k_tc_prep<<<unsigned((nprep + 255) / 256), 256, 0, st>>>(hk::ItemTcPrep{b_buf(c, i), c->tc_A, N, L, i},
+                                                                 nprep);
+    ck(cudaGetLastError(), "tc prep launch");
+    ++c->launches;
+    hk::TcBulkArgs a{c->S.view(), c->tc_A, c->tc_P, N, L, i, jfirst, c->d_err};
+    const dim3 grid(unsigned(ncols), unsigned(hk::tc_ntiles(N) - jfirst / hk::kTcRows));
     hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
     ck(cudaGetLastError(), "tc bulk launch");
     ++c->launches;
@@ -359,6 +366,8 @@ void ensure_tc_scratch(hk_ctx* c) {
     if (c->tc_P_words >= need) return;
     if (c->tc_P) cudaFree(c->tc_P);
     if (c->tc_fb) cudaFree(c->tc_fb);
+    if (c->tc_A) cudaFree(c->tc_A);
+    ck(cudaMalloc(&c->tc_A, hk::tc_apre_bytes(c->n, c->L)), "cudaMalloc tc A");
     if (!c->tc_fb_count) ck(cudaMalloc(&c->tc_fb_count, sizeof(int)), "cudaMalloc fb count");
     c->tc_P = nullptr;
     c->tc_fb = nullptr;
@@ -488,6 +497,7 @@ void hk_destroy(hk_ctx* c) {
     if (c->tc_P) cudaFree(c->tc_P);
     if (c->tc_fb) cudaFree(c->tc_fb);
     if (c->tc_fb_count) cudaFree(c->tc_fb_count);
+    if (c->tc_A) cudaFree(c->tc_A);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);

@@ -26,49 +26,99 @@
 namespace hk {
 
 constexpr int kTcRows = 128;     // M per tile (TMEM lanes)
-constexpr int kTcN = 256;        // N per MMA (TMEM columns)
+constexpr int kTcN = 256;        // N per MMA (TMEM columns per accumulator)
 constexpr int kTcK = 32;         // K per MMA (bytes)
 constexpr int kTcGuard = 8;      // short product from limb L - 8
-constexpr int kTcThreads = 128;  // 4 warps: one thread per row / TMEM lane
-constexpr int kTcKB = 4;         // MMAs (K-steps) per staged A block
-constexpr int kTcABuf = 4096 * kTcKB; // bytes per A buffer (2 buffers)
+constexpr int kTcThreads = 256;  // warp 0: TMA + MMA issue; warps 4-7: epilogue (TMEM lanes 32 (w % 4)..)
+constexpr int kTcKB = 4;         // MMAs (K-steps) per A block
+constexpr int kTcBlk = 4096 * kTcKB; // bytes per A block (one bulk copy)
+constexpr int kTcStages = 4;     // A ring depth
 
 HK_HD int tc_nb(int L) { return 4 * L; }
 HK_HD int tc_ncell(int L) { return tc_nb(L) + 352; }        // cells p in [-31, nb + 321)
 HK_HD int tc_sx_words(int L) { return (tc_nb(L) + 512) / 4; }
+HK_HD int tc_nks(int L) { return (tc_nb(L) + kTcK - 1) / kTcK; }
+HK_HD int tc_nblk(int L) { return (tc_nks(L) + kTcKB - 1) / kTcKB; }
+HK_HD int tc_ntiles(int N) { return (N + kTcRows - 1) / kTcRows; }
+HK_HD int tc_nchunks(int L) { return (tc_nb(L) + 32 + kTcN - 1) / kTcN; }
 HK_HD size_t tc_smem_bytes(int L) {
-    return 2 * (size_t)kTcABuf + 16 * (size_t)tc_ncell(L) + 4 * (size_t)tc_sx_words(L) + 64;
+    return (size_t)kTcStages * kTcBlk + 16 * (size_t)tc_ncell(L) + 4 * (size_t)tc_sx_words(L) + 64;
 }
 HK_HD int tc_scratch_limbs(int L) { return L + kTcGuard; }  // limbs [L-8, 2L)
+// preformatted A operand of one step: [row tile][A block][4 K-steps x 128 rows x 32 B]
+HK_HD size_t tc_apre_bytes(int N, int L) { return (size_t)tc_ntiles(N) * tc_nblk(L) * kTcBlk; }
+
+// A operand of step i in the MMA's K-major SWIZZLE_NONE layout: row k = 128 tile
+// + rr, K-step ks holds reversed bytes Yr[32 ks .. 32 ks + 31] of y_k = B_i(k)
+// (zero for k <= i, k >= N or past nb).  16 B per thread, coalesced writes.
+struct ItemTcPrep {
+    MpArr B;
+    uint8_t* A;
+    int N, L, i;
+    HK_DEV void operator()(long long u) const {
+        const int nb = tc_nb(L);
+        const long long per_tile = (long long)tc_nblk(L) * kTcKB * 256;
+        const int tile = int(u / per_tile);
+        const int rem = int(u % per_tile);
+        const int ks = rem >> 8, w = rem & 255;
+        const int rr = (w >> 4) * 8 + (w & 7), h = (w >> 3) & 1;
+        const int k = tile * kTcRows + rr;
+        const int u0 = ks * kTcK + 16 * h;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (k > i && k < N && u0 < nb) {
+            const uint4 g = *reinterpret_cast<const uint4*>(B.limbs(k, L) + (L - 4 - u0 / 4));
+            v.x = __byte_perm(g.w, 0u, 0x0123);
+            v.y = __byte_perm(g.z, 0u, 0x0123);
+            v.z = __byte_perm(g.y, 0u, 0x0123);
+            v.w = __byte_perm(g.x, 0u, 0x0123);
+        }
+        reinterpret_cast<uint4*>(A)[u] = v;
+    }
+};
+
+#if !defined(HK_WARP_EMU)
+__global__ void __launch_bounds__(256) k_tc_prep(ItemTcPrep f, long long n) {
+    const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) f(u);
+}
+#endif
 
 struct TcBulkArgs {
-    MpArr S, B;                  // S (jagged), B_i
+    MpArr S;                     // S (jagged)
+    const uint8_t* A;            // preformatted A (ItemTcPrep)
     uint32_t* P;                 // scratch: item -> tc_scratch_limbs(L) limbs
     int N, L, i, jfirst;
     const int* err;
 };
 
-// blockIdx.x: column offset (j = jfirst + x); blockIdx.y: row tile (k0 = j + 128 y)
-__global__ void __launch_bounds__(kTcThreads) k_tc_bulk(TcBulkArgs a) {
+#if !defined(HK_WARP_EMU)
+// blockIdx.x: column offset (j = jfirst + x); blockIdx.y: row tile offset (tile = j / 128 + y).
+// Rows k of the tile with j <= k < N are this CTA's items (k, j).
+//
+// Pipeline: thread 0 streams A blocks through a kTcStages ring with bulk copies
+// (full[s]: TMA bytes landed; empty[s]: the MMAs reading slot s retired, via
+// tcgen05.commit) and issues the MMAs of output chunk c into TMEM accumulator
+// c & 1; warps 4-7 drain accumulator c & 1 (carry the int32 byte-column sums
+// into limbs) while chunk c + 1 accumulates into the other one (accF / accE).
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    __shared__ uint64_t mbarb[2];
+    __shared__ uint64_t full[kTcStages], empty[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
     if (*(volatile const int*)a.err >= 0) return;
     const int N = a.N, L = a.L, nb = tc_nb(L);
     const int j = a.jfirst + int(blockIdx.x);
-    const int k0 = j + kTcRows * int(blockIdx.y);
-    if (j >= N || k0 >= N) return;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    uint8_t* sA = tsm;                                   // 2 x 16 KB: A blocks (4 K-major 128 x 32 B tiles)
-    uint8_t* sE = tsm + 2 * kTcABuf;                     // expanded x cells
+    const int tile = j / kTcRows + int(blockIdx.y);
+    if (j >= N || tile * kTcRows >= N) return;
+    const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
+    uint8_t* sA = tsm;                                     // kTcStages x 16 KB A ring
+    uint8_t* sE = tsm + (size_t)kTcStages * kTcBlk;        // expanded x cells
     uint32_t* sX = reinterpret_cast<uint32_t*>(sE + 16 * (size_t)tc_ncell(L)); // x bytes, 32-byte zero pad
     const int pmin = -31;
 
-    // x_j = S(j, i) bytes into sX (word 8 = byte 32 holds X[0])
+    // x_j = S(j, i) bytes into sX (word 8 = byte 32 holds X[0]); cells p = pmin + c: X[p .. p+15]
     const uint32_t* xl = a.S.limbs(tri_idx(j, a.i, N), L);
     for (int w = tid; w < tc_sx_words(L); w += kTcThreads) sX[w] = (w >= 8 && w < 8 + L) ? xl[w - 8] : 0u;
     __syncthreads();
-    // cells p = pmin + c: X[p .. p+15] (zero outside [0, nb))
     for (int c = tid; c < tc_ncell(L); c += kTcThreads) {
         const int off = 32 + pmin + c; // byte offset in sX (>= 1)
         const int w0 = off >> 2, sh = (off & 3) * 8;
@@ -82,109 +132,127 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_bulk(TcBulkArgs a) {
         v.w = __funnelshift_r(W[3], W[4], sh);
         *reinterpret_cast<uint4*>(sE + 16 * (size_t)c) = v;
     }
-    if (warp == 0) tc::tmem_alloc(&taddr_s, kTcN);
+    tc::fence_async_smem(); // generic-proxy writes of sE -> visible to the tensor core
+    if (warp == 0) tc::tmem_alloc(&taddr_s, 2 * kTcN);
     if (tid == 0) {
-        tc::mbar_init(&mbarb[0], 1);
-        tc::mbar_init(&mbarb[1], 1);
+        for (int s = 0; s < kTcStages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&accF[b], 1);
+            tc::mbar_init(&accE[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = taddr_s;
-    const uint32_t idesc = tc::idesc_u8(kTcRows, kTcN, false, true);
+    const int nch = tc_nchunks(L);
 
-    const int r = tid;            // this thread's row / TMEM lane
-    const int k = k0 + r;
-    const bool row_ok = k < N;
-    const long long n2 = N - a.jfirst;
-    const long long item = row_ok ? col_off(j - a.jfirst, int(n2)) + (k - j) : 0;
-    uint32_t* Pout = a.P + item * (long long)tc_scratch_limbs(L);
-    const uint32_t* yl_row = a.B.limbs(row_ok ? k : k0, L);
-    uint64_t carry = 0;
-    uint32_t bph[2] = {0u, 0u}; // per-buffer mbarrier phases
-
-    // stage the A K-block `blk` (kTcKB MMAs = 128 rows x 128 B) into buffer `buf`
-    auto stage = [&](int blk, int buf, int ksteps) {
-        uint8_t* dst = sA + buf * kTcABuf;
-        for (int q = tid; q < kTcRows * 2 * kTcKB; q += kTcThreads) {
-            const int sub = q / (kTcRows * 2), qq = q % (kTcRows * 2);
-            const int rr = qq >> 1, h = qq & 1;
-            const int ks = blk * kTcKB + sub;
-            const int u0 = ks * kTcK + 16 * h;
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (ks < ksteps && k0 + rr < N && u0 < nb) {
-                // Yr[u0 .. u0+15] = Y[nb-1-u0 .. nb-16-u0] = reversed limbs [L-4-u0/4, L-u0/4)
-                const uint4 g = *reinterpret_cast<const uint4*>(a.B.limbs(k0 + rr, L) + (L - 4 - u0 / 4));
-                v.x = __byte_perm(g.w, 0u, 0x0123);
-                v.y = __byte_perm(g.z, 0u, 0x0123);
-                v.z = __byte_perm(g.y, 0u, 0x0123);
-                v.w = __byte_perm(g.x, 0u, 0x0123);
-            }
-            *reinterpret_cast<uint4*>(dst + sub * 4096 + (rr >> 3) * 256 + h * 128 + (rr & 7) * 16) = v;
-        }
-        tc::fence_async_smem();
-    };
-
-    for (int tc0 = -31, ch = 0; tc0 < nb + 1; tc0 += kTcN, ++ch) {
-        const int u_hi = tc0 < 0 ? nb : nb - tc0;             // u' < u_hi contribute
-        const int ksteps = (u_hi + kTcK - 1) / kTcK;
-        const int nblk = (ksteps + kTcKB - 1) / kTcKB;
-        // double-buffered pipeline: MMAs of block b run while block b+1 is staged
-        stage(0, 0, ksteps);
-        __syncthreads();
-        for (int b = 0; b < nblk; ++b) {
-            const int buf = b & 1;
-            if (tid == 0) {
+    if (warp == 0) {
+        if (ln == 0) {
+            const uint32_t idesc = tc::idesc_u8(kTcRows, kTcN, false, true);
+            const uint8_t* Abase = a.A + (size_t)tile * tc_nblk(L) * kTcBlk;
+            auto nblk_of = [&](int c) {
+                const int tc0 = -31 + kTcN * c;
+                const int u_hi = tc0 < 0 ? nb : nb - tc0; // u' < u_hi contribute
+                return (((u_hi + kTcK - 1) / kTcK) + kTcKB - 1) / kTcKB;
+            };
+            int Q = 0;
+            for (int c = 0; c < nch; ++c) Q += nblk_of(c);
+            // producer cursor: global block index qt -> (chunk pc, block pb)
+            int qt = 0, pc = 0, pb = 0, pcn = nblk_of(0);
+            auto issue_tma = [&]() {
+                const int s = qt % kTcStages;
+                if (qt >= kTcStages) tc::mbar_wait(&empty[s], uint32_t((qt / kTcStages) - 1) & 1u);
+                tc::mbar_expect_tx(&full[s], kTcBlk);
+                tc::bulk_g2s(sA + (size_t)s * kTcBlk, Abase + (size_t)pb * kTcBlk, kTcBlk, &full[s]);
+                ++qt;
+                if (++pb == pcn && ++pc < nch) {
+                    pb = 0;
+                    pcn = nblk_of(pc);
+                }
+            };
+            while (qt < Q && qt < kTcStages - 1) issue_tma();
+            int q = 0;
+            for (int c = 0; c < nch; ++c) {
+                const int ab = c & 1;
+                if (c >= 2) tc::mbar_wait(&accE[ab], uint32_t((c - 2) >> 1) & 1u);
                 tc::fence_after();
-                for (int sub = 0; sub < kTcKB; ++sub) {
-                    const int ks = b * kTcKB + sub;
-                    if (ks >= ksteps) break;
-                    const uint64_t ad = tc::sdesc(sA + buf * kTcABuf + sub * 4096, 128, 256);
-                    const uint64_t bd = tc::sdesc(sE + 16 * (size_t)(tc0 + ks * kTcK - pmin), 128, 256);
-                    tc::mma_i8(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
-                }
-                tc::commit(&mbarb[buf]);
-            }
-            if (b + 1 < nblk) {
-                if (b >= 1) { // buffer (b+1)&1 was last read by block b-1's MMAs
-                    tc::mbar_wait(&mbarb[(b + 1) & 1], bph[(b + 1) & 1]);
-                    bph[(b + 1) & 1] ^= 1u;
-                }
-                stage(b + 1, (b + 1) & 1, ksteps);
-            }
-            __syncthreads();
-        }
-        // drain: the last block's commit (and the one before, if not yet awaited)
-        if (nblk >= 2) {
-            tc::mbar_wait(&mbarb[(nblk - 2) & 1], bph[(nblk - 2) & 1]);
-            bph[(nblk - 2) & 1] ^= 1u;
-        }
-        tc::mbar_wait(&mbarb[(nblk - 1) & 1], bph[(nblk - 1) & 1]);
-        bph[(nblk - 1) & 1] ^= 1u;
-        tc::fence_after();
-        // epilogue: this row's 256 byte-column sums -> 64 limbs (exact carries)
-        for (int c8 = 0; c8 < kTcN; c8 += 8) {
-            uint32_t v[8];
-            tc::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c8, v);
-            tc::tmem_ld_wait();
+                const int tc0 = -31 + kTcN * c;
+                const int u_hi = tc0 < 0 ? nb : nb - tc0;
+                const int ksteps = (u_hi + kTcK - 1) / kTcK;
+                const int nblk = nblk_of(c);
+                for (int b = 0; b < nblk; ++b, ++q) {
+                    const int s = q % kTcStages;
+                    tc::mbar_wait(&full[s], uint32_t(q / kTcStages) & 1u);
+                    tc::fence_after();
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint64_t s = carry + (uint64_t)v[4 * h] + ((uint64_t)v[4 * h + 1] << 8) +
-                             ((uint64_t)v[4 * h + 2] << 16) + ((uint64_t)v[4 * h + 3] << 24);
-                const int lq = ch * 64 + (c8 >> 2) + h; // limb index relative to L - 8
-                if (row_ok && lq < tc_scratch_limbs(L)) Pout[lq] = uint32_t(s);
-                carry = s >> 32;
+                    for (int sub = 0; sub < kTcKB; ++sub) {
+                        const int ks = b * kTcKB + sub;
+                        if (ks < ksteps) {
+                            const uint64_t ad = tc::sdesc(sA + (size_t)s * kTcBlk + sub * 4096, 128, 256);
+                            const uint64_t bd = tc::sdesc(sE + 16 * (size_t)(tc0 + ks * kTcK - pmin), 128, 256);
+                            tc::mma_i8(tmem + uint32_t(ab * kTcN), ad, bd, idesc, ks > 0 ? 1u : 0u);
+                        }
+                    }
+                    tc::commit(&empty[s]);
+                    if (qt < Q) issue_tma(); // refills the slot block q - 1 used
+                }
+                tc::commit(&accF[ab]);
             }
         }
-        tc::fence_before();
-        __syncthreads(); // TMEM reads done before the next chunk's MMAs overwrite it
-        tc::fence_after();
+        __syncwarp();
+    } else if (warp >= 4) {
+        const int r = 32 * (warp & 3) + ln; // this thread's row / TMEM lane
+        const int k = tile * kTcRows + r;
+        const bool row_ok = k >= j && k < N;
+        const long long n2 = N - a.jfirst;
+        const long long item = row_ok ? col_off(j - a.jfirst, int(n2)) + (k - j) : 0;
+        uint32_t* Pout = a.P + item * (long long)tc_scratch_limbs(L);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+        uint64_t carry = 0;
+        for (int c = 0; c < nch; ++c) {
+            const int ab = c & 1;
+            tc::mbar_wait(&accF[ab], uint32_t(c >> 1) & 1u);
+            tc::fence_after();
+            for (int c32 = 0; c32 < kTcN; c32 += 32) {
+                uint32_t v[32];
+                tc::tmem_ld32(lane_base + uint32_t(ab * kTcN + c32), v);
+                tc::tmem_ld_wait();
+                uint32_t o[8];
+#pragma unroll
+                for (int h = 0; h < 8; ++h) {
+                    const uint64_t s = carry + (uint64_t)v[4 * h] + ((uint64_t)v[4 * h + 1] << 8) +
+                                       ((uint64_t)v[4 * h + 2] << 16) + ((uint64_t)v[4 * h + 3] << 24);
+                    o[h] = uint32_t(s);
+                    carry = s >> 32;
+                }
+                const int lq = c * 64 + (c32 >> 2); // limb index relative to L - 8 (multiple of 8)
+                if (row_ok) {
+                    if (lq + 8 <= tc_scratch_limbs(L)) {
+                        reinterpret_cast<uint4*>(Pout + lq)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                        reinterpret_cast<uint4*>(Pout + lq)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 8; ++h)
+                            if (lq + h < tc_scratch_limbs(L)) Pout[lq + h] = o[h];
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (ln == 0) tc::mbar_arrive(&accE[ab]);
+        }
     }
-    (void)yl_row;
     tc::fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tmem, kTcN);
+    tc::fence_after();
+    if (warp == 0) tc::tmem_dealloc(tmem, 2 * kTcN);
 }
+#endif
 
 // Second pass: S(k,j) = RNE(S(k,j) - x_j y_k) from the scratch product, with the
 // Ziv certificate; exact warp FMA when it cannot certify.  Items enumerate the

@@ -161,6 +161,12 @@ def test_c3_parity_vs_reference(api):
     check_vs_golden(api, "c3")
 
 
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLD, "c4.json")), reason="c4 golden not generated")
+def test_c4_parity_vs_reference(api):
+    # BASELINE configs[3]: N = 1024, p = 49152 bits (about 20 s on one B200)
+    check_vs_golden(api, "c4")
+
+
 def test_c2_closed_form_pivots(api):
     """beta = 1: d_n = (n!)^2 — independent of the reference.  The
     p-bit float path rounds every op, so agreement is to the north_star tolerance."""
