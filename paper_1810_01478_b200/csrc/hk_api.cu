@@ -100,7 +100,7 @@ struct hk_ctx {
     bool graph_tc = false;
     std::map<long long, cudaGraphExec_t> inv_graphs;         // L^{-1} step graphs keyed by (n, m)
     std::map<long long, long long> inv_graph_launches;
-    const void* inv_bufs[2] = {nullptr, nullptr};            // S, X they were captured on
+    const void* inv_bufs[3] = {nullptr, nullptr, nullptr};   // S, X, TC scratch they were captured on
     std::vector<uint32_t> h_limbs;
     std::vector<int32_t> h_e, h_s;
     // ---- tensor-core bulk products (large p): scratch of short products
@@ -306,13 +306,58 @@ MpArr b_buf(hk_ctx* c, int i) {
 // U(i) needs B_i (end of P(i)); P(i+1) needs column i+1 after step i-1 (end of
 // U(i-1)+STORE(i-1)); STORE(i) needs P(i+1) to have read S(i+1,i).  So P(i+1)
 // overlaps U(i) and the critical path per step is max(U(i), P(i+1)).
-// Tensor-core products for the bulk update?  Default: when p >= 8192 bits and
+// Tensor-core products for the bulk update?  Default: when p >= 4096 bits and
 // the per-CTA shared memory fits; HK_TC=0/1 forces it off/on (tests, sweeps).
+// L^-1 steps are narrower (b <= m columns per step): there the tensor cores pay
+// from p >= 12288 bits (measured: C2 5.1 ms IMAD vs 7.4 ms TC, C3 459 vs 107 ms).
 bool use_tc(const hk_ctx* c) {
     const int L = c->L;
     if (L % 4 != 0 || hk::tc_smem_bytes(L) > 220 * 1024) return false;
     if (const char* e = getenv("HK_TC")) return e[0] == '1';
-    return L >= 256;
+    return L >= 128;
+}
+bool use_tc_inv(const hk_ctx* c) {
+    if (!use_tc(c)) return false;
+    if (getenv("HK_TC")) return true;
+    return c->L >= 384;
+}
+
+// A operand preformat + the tcgen05 product kernel (one CTA per SM: it owns all
+// 512 TMEM columns).  `rows` is the row-operand source (ItemTcPrep).
+void tc_products(hk_ctx* c, const hk::TcBulkArgs& a, hk::MpArr rows, unsigned gx, cudaStream_t st) {
+    const int N = c->n, L = c->L;
+    const size_t smem = std::max(hk::tc_smem_bytes(L), size_t(120 * 1024));
+    static bool configured = false;
+    if (!configured) {
+        ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");
+        configured = true;
+    }
+    const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
+    const long long nprep = prep.count();
+    hk::k_tc_prep<<<unsigned((nprep + 255) / 256), 256, 0, st>>>(prep, nprep);
+    ck(cudaGetLastError(), "tc prep launch");
+    ++c->launches;
+    const int first_row = a.mode == 0 ? a.jfirst : a.i + 1;
+    const dim3 grid(gx, unsigned(hk::tc_ntiles(N) - first_row / hk::kTcRows));
+    hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
+    ck(cudaGetLastError(), "tc bulk launch");
+    ++c->launches;
+}
+
+// Exact redo of the items the rounding pass could not certify (device-side count).
+template <class F>
+void launch_fix(hk_ctx* c, const F& f, cudaStream_t st) {
+    const int wo = ws_op_words(c->L);
+    const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
+    static bool cfg = false;
+    if (!cfg) {
+        ck(cudaFuncSetAttribute(hk::k_tc_fix<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "fix attr");
+        cfg = true;
+    }
+    hk::k_tc_fix<F><<<unsigned(c->sm_count), unsigned(32 * wpb), size_t(wo) * 4 * wpb, st>>>(f, c->tc_fb_count,
+                                                                                            c->tc_fb, wo);
+    ck(cudaGetLastError(), "tc fix launch");
+    ++c->launches;
 }
 
 // Step-i update of columns jfirst..N-1 (bulk): IMAD paired warp FMAs, or the
@@ -326,43 +371,34 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
                    hk::trailing2_items(N, jfirst), hk::opws2_words(L), st);
         return;
     }
-    // one CTA per SM (it owns all 512 TMEM columns)
-    const size_t smem = std::max(hk::tc_smem_bytes(L), size_t(120 * 1024));
-    static bool configured = false;
-    if (!configured) {
-        ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");
-        configured = true;
-    }
-    const long long nprep = (long long)(hk::tc_apre_bytes(N, L) / 16);
-    hk::k_tc_prep<<<unsigned((nprep + 255) / 256), 256, 0, st>>>(hk::ItemTcPrep{b_buf(c, i), c->tc_A, N, L, i},
-                                                                 nprep);
-    ck(cudaGetLastError(), "tc prep launch");
-    ++c->launches;
-    hk::TcBulkArgs a{c->S.view(), c->tc_A, c->tc_P, N, L, i, jfirst, c->d_err};
-    const dim3 grid(unsigned(ncols), unsigned(hk::tc_ntiles(N) - jfirst / hk::kTcRows));
-    hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
-    ck(cudaGetLastError(), "tc bulk launch");
-    ++c->launches;
+    tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
+                b_buf(c, i), unsigned(ncols), st);
     ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
     launch(c,
            hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count, c->tc_fb},
            (long long)ncols * (ncols + 1) / 2, hk::tcround_words(L), st);
-    const int wo = ws_op_words(L);
-    const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
-    static bool fix_cfg = false;
-    if (!fix_cfg) {
-        ck(cudaFuncSetAttribute(hk::k_tc_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "fix attr");
-        fix_cfg = true;
-    }
-    hk::k_tc_fix<<<unsigned(c->sm_count), unsigned(32 * wpb), size_t(wo) * 4 * wpb, st>>>(
-        c->S.view(), b_buf(c, i), N, L, i, jfirst, c->tc_fb_count, c->tc_fb, wo);
-    ck(cudaGetLastError(), "tc fix launch");
-    ++c->launches;
+    launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st);
 }
 
-void ensure_tc_scratch(hk_ctx* c) {
+// L^-1 step i on the tensor cores (same product kernel, mode 1).
+void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
+    const int N = c->n, L = c->L, m = c->m;
+    const int b = i < m ? i : m;
+    if (i + 1 >= N) return;
+    if (b > 0)
+        tc_products(c, hk::TcBulkArgs{c->S.view(), c->X.view(), c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err},
+                    c->S.view(), unsigned(b), st);
+    ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
+    const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
+    launch(c, hk::ItemTcRoundInv{c->S.view(), c->X.view(), c->tc_P, N, L, m, i, b, c->tc_fb_count, c->tc_fb},
+           items, hk::tcround_words(L), st);
+    if (b > 0) launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st);
+}
+
+void ensure_tc_scratch(hk_ctx* c, int m = 0) {
     if (!use_tc(c)) return;
-    const size_t need = (size_t)c->n * (c->n + 1) / 2 * hk::tc_scratch_limbs(c->L);
+    const size_t items = std::max((size_t)c->n * (c->n + 1) / 2, (size_t)c->n * m);
+    const size_t need = items * hk::tc_scratch_limbs(c->L);
     if (c->tc_P_words >= need) return;
     if (c->tc_P) cudaFree(c->tc_P);
     if (c->tc_fb) cudaFree(c->tc_fb);
@@ -372,7 +408,7 @@ void ensure_tc_scratch(hk_ctx* c) {
     c->tc_P = nullptr;
     c->tc_fb = nullptr;
     ck(cudaMalloc(&c->tc_P, need * sizeof(uint32_t)), "cudaMalloc tc scratch");
-    ck(cudaMalloc(&c->tc_fb, (size_t)c->n * (c->n + 1) / 2 * sizeof(long long)), "cudaMalloc fb list");
+    ck(cudaMalloc(&c->tc_fb, items * sizeof(long long)), "cudaMalloc fb list");
     c->tc_P_words = need;
 }
 
@@ -616,12 +652,15 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
         if (m < 1 || m > N) return fail(c, HK_ERR_INVALID, "invert_L_partial: need 1 <= m <= n");
         c->m = m;
         c->X.ensure((long long)N * m, L);
-        // N latency-bound steps: one CTA per FMA, all steps in one cached graph
-        if (c->inv_bufs[0] != c->S.d || c->inv_bufs[1] != c->X.d) {
+        const bool tc = use_tc_inv(c);
+        ensure_tc_scratch(c, m);
+        // all N steps in one cached graph (invalidated when a buffer moves)
+        if (c->inv_bufs[0] != c->S.d || c->inv_bufs[1] != c->X.d || c->inv_bufs[2] != c->tc_P) {
             for (auto& kv : c->inv_graphs) cudaGraphExecDestroy(kv.second);
             c->inv_graphs.clear();
             c->inv_bufs[0] = c->S.d;
             c->inv_bufs[1] = c->X.d;
+            c->inv_bufs[2] = c->tc_P;
         }
         const long long key = ((long long)N << 20) | m;
         auto it = c->inv_graphs.find(key);
@@ -633,6 +672,10 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
             for (int i = 0; i < N; ++i) {
                 const int b = i < m ? i : m;
                 const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
+                if (tc) {
+                    enqueue_inv_tc(c, i, c->st);
+                    continue;
+                }
                 // few items: a CTA per FMA (latency); many: a warp per FMA (one wave)
                 if (items <= 4LL * c->sm_count)
                     launch_cta(c, hk::CItemInvStep{c->S.view(), c->X.view(), N, L, m, i}, items, ws_cta_words(L));

@@ -49,15 +49,18 @@ HK_HD int tc_scratch_limbs(int L) { return L + kTcGuard; }  // limbs [L-8, 2L)
 HK_HD size_t tc_apre_bytes(int N, int L) { return (size_t)tc_ntiles(N) * tc_nblk(L) * kTcBlk; }
 
 // A operand of step i in the MMA's K-major SWIZZLE_NONE layout: row k = 128 tile
-// + rr, K-step ks holds reversed bytes Yr[32 ks .. 32 ks + 31] of y_k = B_i(k)
-// (zero for k <= i, k >= N or past nb).  16 B per thread, coalesced writes.
+// + rr, K-step ks holds reversed bytes Yr[32 ks .. 32 ks + 31] of the row operand
+// (LDLT: y_k = B_i(k); L^-1: L(k, i) = S(k, i)), zero for k <= i, k >= N or past
+// nb.  Tiles from tile0 = (i + 1) / 128 on.  16 B per thread, coalesced writes.
 struct ItemTcPrep {
-    MpArr B;
+    MpArr R;   // LDLT: B_i (row k at k);  L^-1: S (row k at tri_idx(k, i))
     uint8_t* A;
-    int N, L, i;
+    int N, L, i, mode;
     HK_DEV void operator()(long long u) const {
         const int nb = tc_nb(L);
         const long long per_tile = (long long)tc_nblk(L) * kTcKB * 256;
+        const int tile0 = (i + 1) / kTcRows;
+        u += tile0 * per_tile;
         const int tile = int(u / per_tile);
         const int rem = int(u % per_tile);
         const int ks = rem >> 8, w = rem & 255;
@@ -66,13 +69,17 @@ struct ItemTcPrep {
         const int u0 = ks * kTcK + 16 * h;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (k > i && k < N && u0 < nb) {
-            const uint4 g = *reinterpret_cast<const uint4*>(B.limbs(k, L) + (L - 4 - u0 / 4));
+            const uint32_t* row = mode == 0 ? R.limbs(k, L) : R.limbs(tri_idx(k, i, N), L);
+            const uint4 g = *reinterpret_cast<const uint4*>(row + (L - 4 - u0 / 4));
             v.x = __byte_perm(g.w, 0u, 0x0123);
             v.y = __byte_perm(g.z, 0u, 0x0123);
             v.z = __byte_perm(g.y, 0u, 0x0123);
             v.w = __byte_perm(g.x, 0u, 0x0123);
         }
         reinterpret_cast<uint4*>(A)[u] = v;
+    }
+    HK_HD long long count() const {
+        return (long long)(tc_ntiles(N) - (i + 1) / kTcRows) * tc_nblk(L) * kTcKB * 256;
     }
 };
 
@@ -83,11 +90,16 @@ __global__ void __launch_bounds__(256) k_tc_prep(ItemTcPrep f, long long n) {
 }
 #endif
 
+// mode 0 (LDLT step i): CTA column j = jfirst + x with x operand S(j, i), rows
+//   k >= j, item = (column-major triangle of columns jfirst..N-1)(k, j).
+// mode 1 (L^-1 step i): CTA column c = x < b with x operand X(i, c), rows j > i,
+//   item = (j - i - 1) b + c.
 struct TcBulkArgs {
     MpArr S;                     // S (jagged)
+    MpArr X;                     // L^-1 columns (mode 1), row-major N x m
     const uint8_t* A;            // preformatted A (ItemTcPrep)
     uint32_t* P;                 // scratch: item -> tc_scratch_limbs(L) limbs
-    int N, L, i, jfirst;
+    int N, L, i, jfirst, mode, m, b;
     const int* err;
 };
 
@@ -104,9 +116,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
     __shared__ uint64_t full[kTcStages], empty[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
-    if (*(volatile const int*)a.err >= 0) return;
+    if (a.mode == 0 && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
     const int N = a.N, L = a.L, nb = tc_nb(L);
-    const int j = a.jfirst + int(blockIdx.x);
+    const int j = a.mode == 0 ? a.jfirst + int(blockIdx.x) : a.i + 1; // first valid row
     const int tile = j / kTcRows + int(blockIdx.y);
     if (j >= N || tile * kTcRows >= N) return;
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
@@ -115,8 +127,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     uint32_t* sX = reinterpret_cast<uint32_t*>(sE + 16 * (size_t)tc_ncell(L)); // x bytes, 32-byte zero pad
     const int pmin = -31;
 
-    // x_j = S(j, i) bytes into sX (word 8 = byte 32 holds X[0]); cells p = pmin + c: X[p .. p+15]
-    const uint32_t* xl = a.S.limbs(tri_idx(j, a.i, N), L);
+    // x bytes into sX (word 8 = byte 32 holds X[0]); cells p = pmin + c: X[p .. p+15]
+    const uint32_t* xl = a.mode == 0 ? a.S.limbs(tri_idx(j, a.i, N), L)
+                                     : a.X.limbs((long long)a.i * a.m + blockIdx.x, L);
     for (int w = tid; w < tc_sx_words(L); w += kTcThreads) sX[w] = (w >= 8 && w < 8 + L) ? xl[w - 8] : 0u;
     __syncthreads();
     for (int c = tid; c < tc_ncell(L); c += kTcThreads) {
@@ -209,8 +222,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         const int r = 32 * (warp & 3) + ln; // this thread's row / TMEM lane
         const int k = tile * kTcRows + r;
         const bool row_ok = k >= j && k < N;
-        const long long n2 = N - a.jfirst;
-        const long long item = row_ok ? col_off(j - a.jfirst, int(n2)) + (k - j) : 0;
+        long long item = 0;
+        if (row_ok)
+            item = a.mode == 0 ? col_off(j - a.jfirst, N - a.jfirst) + (k - j)
+                               : (long long)(k - a.i - 1) * a.b + blockIdx.x;
         uint32_t* Pout = a.P + item * (long long)tc_scratch_limbs(L);
         const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
         uint64_t carry = 0;
@@ -301,25 +316,88 @@ struct ItemTcRound {
     }
 };
 
-#if !defined(HK_WARP_EMU)
-// Exact redo of the uncertified items: S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)).
-__global__ void __launch_bounds__(256) k_tc_fix(MpArr S, MpArr B, int N, int L, int i, int jfirst,
-                                                const int* fb_count, const long long* fb, int ws_words) {
-    extern __shared__ uint32_t fsm[];
-    const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    uint32_t* ws = fsm + (size_t)wib * ws_words;
-    const int cnt = *fb_count;
-    for (long long q = (long long)blockIdx.x * wpb + wib; q < cnt; q += (long long)gridDim.x * wpb) {
-        const long long w = fb[q];
+// L^-1 step i (mode 1): X(j,c) = RNE(X(j,c) - L(j,i) X(i,c)) for the (N-i-1) b
+// product items, then (i < m) the copies X(j,i) = -L(j,i) as in ItemInvStep.
+struct ItemTcRoundInv {
+    MpArr S, X;
+    const uint32_t* P;
+    int N, L, m, i, b;
+    int* fb_count;
+    long long* fb;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const long long nfma = (long long)(N - i - 1) * b;
+        if (w >= nfma) {
+            const int j = i + 1 + int(w - nfma);
+            const long long el = tri_idx(j, i, N);
+            const long long xd = (long long)j * m + i;
+            copy_entry(X.limbs(xd, L), X.m + xd, S.limbs(el, L), S.m + el, L);
+            if (lane() == 0) X.m[xd].sign = -X.m[xd].sign;
+            wsync();
+            return;
+        }
+        const int j = i + 1 + int(w / b), c = int(w % b);
+        const long long xc = (long long)j * m + c, xi = (long long)i * m + c, el = tri_idx(j, i, N);
+        const Meta cm = X.m[xc], xm = S.m[el], ym = X.m[xi];
+        const int sp = -(xm.sign * ym.sign);
+        if (sp == 0) return;
+        uint32_t* o = X.limbs(xc, L);
+        const int t0 = L - kTcGuard;
+        const int lsbP = xm.exp + ym.exp - 64 * L;
+        const Opd Xo{o, L, cm.exp - 32 * L, cm.sign};
+        const Opd Y{P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L), lsbP + 32 * t0, sp};
+        bool ok = false;
+        const RMeta rr = warp_round_sum(Xo, Y, ws, o, L, lsbP + 32 * t0 + 46, &ok);
+        if (lane() == 0) {
+            if (ok) {
+                X.m[xc] = Meta{rr.exp, rr.sign};
+            } else {
+#if defined(HK_WARP_EMU)
+                fb[(*fb_count)++] = w;
+#else
+                fb[atomicAdd(fb_count, 1)] = w;
+#endif
+            }
+        }
+        wsync();
+    }
+};
+
+// Exact redo of one uncertified item (full warp FMA workspace).
+struct FixLdlt {
+    MpArr S, B;
+    int N, L, i, jfirst;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
         int jj, kk;
         tri_decode(w, N - jfirst, jj, kk);
         const int j = jfirst + jj, k = jfirst + kk;
         const long long ec = tri_idx(k, j, N), ex = tri_idx(j, i, N);
         uint32_t* c = S.limbs(ec, L);
-        const Meta m = warp_fms(c, S.m[ec], S.limbs(ex, L), S.m[ex], B.limbs(k, L), B.m[k], c, L, opws_carve(ws, L));
-        if (lane() == 0) S.m[ec] = m;
+        const Meta r = warp_fms(c, S.m[ec], S.limbs(ex, L), S.m[ex], B.limbs(k, L), B.m[k], c, L, opws_carve(ws, L));
+        if (lane() == 0) S.m[ec] = r;
         wsync();
     }
+};
+struct FixInv {
+    MpArr S, X;
+    int N, L, m, i, b;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const int j = i + 1 + int(w / b), c = int(w % b);
+        const long long xc = (long long)j * m + c, xi = (long long)i * m + c, el = tri_idx(j, i, N);
+        uint32_t* o = X.limbs(xc, L);
+        const Meta r = warp_fms(o, X.m[xc], S.limbs(el, L), S.m[el], X.limbs(xi, L), X.m[xi], o, L, opws_carve(ws, L));
+        if (lane() == 0) X.m[xc] = r;
+        wsync();
+    }
+};
+
+#if !defined(HK_WARP_EMU)
+template <class F>
+__global__ void __launch_bounds__(256) k_tc_fix(F f, const int* fb_count, const long long* fb, int ws_words) {
+    extern __shared__ uint32_t fsm[];
+    const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    uint32_t* ws = fsm + (size_t)wib * ws_words;
+    const int cnt = *fb_count;
+    for (long long q = (long long)blockIdx.x * wpb + wib; q < cnt; q += (long long)gridDim.x * wpb) f(fb[q], ws);
 }
 #endif
 
