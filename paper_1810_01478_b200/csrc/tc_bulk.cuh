@@ -272,10 +272,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
 // Second pass: S(k,j) = RNE(S(k,j) - x_j y_k) from the scratch product, with the
 // Ziv certificate; exact warp FMA when it cannot certify.  Items enumerate the
 // column-major triangle of columns jfirst..N-1 (as ItemTrailing / the scratch).
-// The window needs max(L, L+8, L) + 4 words; the rare items the certificate
-// cannot settle are appended to `fb` and redone exactly by k_tc_fix (so this
-// pass runs at high occupancy with a window-sized workspace).
-HK_HD int tcround_words(int L) { return (L + 16 + 3) & ~3; }
+// The rounding passes first copy both operands (c: L limbs, the product: L+8
+// limbs) into the warp's shared workspace with cp.async (all loads in flight at
+// once), then round from shared memory; the window G needs max(L, L+8, L) + 4
+// words.  The rare items the certificate cannot settle are appended to `fb`
+// and redone exactly by k_tc_fix.
+HK_HD int tcround_words(int L) { return align4(L) + align4(L + kTcGuard) + align4(L + 16); }
+
+#if defined(HK_WARP_EMU)
+HK_DEV void warp_stage16(uint32_t* dst, const uint32_t* src, int nwords) {
+    for (int q = lane(); q < nwords; q += 32) dst[q] = src[q];
+    wsync();
+}
+#else
+// nwords % 4 == 0, both pointers 16-byte aligned
+HK_DEV void warp_stage16(uint32_t* dst, const uint32_t* src, int nwords) {
+    for (int q = 4 * lane(); q < nwords; q += 128)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(dst + q)), "l"(src + q)
+                     : "memory");
+}
+#endif
+HK_DEV void warp_stage_wait() {
+#if !defined(HK_WARP_EMU)
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
+    wsync();
+}
 
 struct ItemTcRound {
     MpArr S, B;
@@ -297,10 +319,15 @@ struct ItemTcRound {
         if (sp == 0) return; // x or y zero: RNE(c - 0) = c, nothing to write
         const int t0 = L - kTcGuard;
         const int lsbP = xm.exp + ym.exp - 64 * L;
-        const Opd X{c, L, cm.exp - 32 * L, cm.sign};
-        const Opd Y{P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L), lsbP + 32 * t0, sp};
+        uint32_t* Xs = ws;
+        uint32_t* Ys = ws + align4(L);
+        warp_stage16(Xs, c, L);
+        warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
+        warp_stage_wait();
+        const Opd X{Xs, L, cm.exp - 32 * L, cm.sign};
+        const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
-        const RMeta rr = warp_round_sum(X, Y, ws, c, L, lsbP + 32 * t0 + 46, &ok);
+        const RMeta rr = warp_round_sum(X, Y, Ys + align4(L + kTcGuard), c, L, lsbP + 32 * t0 + 46, &ok);
         if (lane() == 0) {
             if (ok) {
                 S.m[ec] = Meta{rr.exp, rr.sign};
@@ -343,10 +370,15 @@ struct ItemTcRoundInv {
         uint32_t* o = X.limbs(xc, L);
         const int t0 = L - kTcGuard;
         const int lsbP = xm.exp + ym.exp - 64 * L;
-        const Opd Xo{o, L, cm.exp - 32 * L, cm.sign};
-        const Opd Y{P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L), lsbP + 32 * t0, sp};
+        uint32_t* Xs = ws;
+        uint32_t* Ys = ws + align4(L);
+        warp_stage16(Xs, o, L);
+        warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
+        warp_stage_wait();
+        const Opd Xo{Xs, L, cm.exp - 32 * L, cm.sign};
+        const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
-        const RMeta rr = warp_round_sum(Xo, Y, ws, o, L, lsbP + 32 * t0 + 46, &ok);
+        const RMeta rr = warp_round_sum(Xo, Y, Ys + align4(L + kTcGuard), o, L, lsbP + 32 * t0 + 46, &ok);
         if (lane() == 0) {
             if (ok) {
                 X.m[xc] = Meta{rr.exp, rr.sign};
