@@ -82,7 +82,7 @@ struct hk_ctx {
     cudaStream_t st = nullptr;  // bulk / default stream of the context
     cudaStream_t st2 = nullptr; // high-priority look-ahead stream
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
-    std::vector<cudaEvent_t> evP, evR; // per-step dependencies (graph capture)
+    std::vector<cudaEvent_t> evP, evR, evU; // per-step dependencies (graph capture)
     DevArr mu, S, R, B, X, Y, T, T2, M;
     int* d_err = nullptr;
     std::string err;
@@ -291,9 +291,10 @@ double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// B_i lives in buffer i % 2 (B_{i+1} is produced while B_i is still read).
+// B_i lives in buffer i % 3: B_{i+1} is produced while B_i is still read, and
+// the copy of B_{i-1} into column i-1 (StoreL) trails one step behind.
 MpArr b_buf(hk_ctx* c, int i) {
-    const long long off = (long long)(i & 1) * c->n;
+    const long long off = (long long)(i % 3) * c->n;
     return MpArr{c->B.d + off * c->L, c->B.m + off};
 }
 
@@ -418,6 +419,7 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     cudaStream_t la = c->st2, bulk = c->st;
     std::vector<cudaEvent_t>& evP = c->evP;
     std::vector<cudaEvent_t>& evR = c->evR;
+    std::vector<cudaEvent_t>& evU = c->evU;
     ck(cudaEventRecord(c->evFork, bulk), "fork");
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
     const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
@@ -425,23 +427,27 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, 0, c->d_err}, 1, wcr, la);
     launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, 0), N, L, 0, c->d_err}, N - 1, wc, la);
     ck(cudaEventRecord(evP[0], la), "evP");
+    // bulk: U(i) -> evU(i) -> StoreL(i-1) -> evR(i-1);  LA: [evU(i-1)] P(i+1) with
+    // MulB(i+1) (overwrites buffer (i+1) % 3 = that of B_{i-2}) after [evR(i-2)].
     for (int i = 0; i < N; ++i) {
         ck(cudaStreamWaitEvent(bulk, evP[i], 0), "wait P");
-        const long long nu = (long long)(N - i - 2) * (N - i - 1) / 2;
-        (void)nu;
         enqueue_bulk(c, i, i + 2, bulk);
+        ck(cudaEventRecord(evU[i], bulk), "evU");
+        if (i >= 1) {
+            launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i - 1), N, L, i - 1}, N - i, 64, bulk);
+            ck(cudaEventRecord(evR[i - 1], bulk), "evR");
+        }
         if (i + 1 < N) {
-            if (i > 0) ck(cudaStreamWaitEvent(la, evR[i - 1], 0), "wait R");
+            if (i > 0) ck(cudaStreamWaitEvent(la, evU[i - 1], 0), "wait U");
             launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err}, N - i - 1, wc, la);
             launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la);
+            if (i >= 2) ck(cudaStreamWaitEvent(la, evR[i - 2], 0), "wait R");
             launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err}, N - i - 2,
                        wc, la);
             ck(cudaEventRecord(evP[i + 1], la), "evP");
-            ck(cudaStreamWaitEvent(bulk, evP[i + 1], 0), "wait P next");
         }
-        launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i), N, L, i}, N - i - 1, 64, bulk);
-        ck(cudaEventRecord(evR[i], bulk), "evR");
     }
+    // StoreL(N-1) has no rows; join the streams (the last ColUpd read S(N-1, N-2))
     ck(cudaEventRecord(c->evJoin, la), "join");
     ck(cudaStreamWaitEvent(bulk, c->evJoin, 0), "join wait");
 }
@@ -456,6 +462,7 @@ void ensure_step_events(hk_ctx* c, int N) {
     };
     grow(c->evP, N);
     grow(c->evR, N);
+    grow(c->evU, N);
 }
 
 int check_pivots(hk_ctx* c) {
@@ -538,6 +545,7 @@ void hk_destroy(hk_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);
     for (auto e : c->evR) cudaEventDestroy(e);
+    for (auto e : c->evU) cudaEventDestroy(e);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
     if (c->st2) cudaStreamDestroy(c->st2);
@@ -579,7 +587,7 @@ int hk_ldlt(hk_ctx* c) {
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
-        c->B.ensure(2LL * N, L);
+        c->B.ensure(3LL * N, L);
         ensure_tc_scratch(c);
         ensure_step_events(c, N);
         c->bad_col = -1;
@@ -880,7 +888,7 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
-        c->B.ensure(2LL * N, L);
+        c->B.ensure(3LL * N, L);
         ensure_tc_scratch(c);
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         struct Rec {
