@@ -104,6 +104,14 @@ def run_reference_once(cfg, workers):
     return json.loads(out.stdout)
 
 
+def hbm_peak_gbps():
+    """Measured HBM copy bandwidth of this pool (MEASURED_PEAKS.json), else the recipe's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
 def fmas(n):
     return n * (n * n - 1) // 6
 
@@ -252,12 +260,48 @@ def bench_ours(args, cfg):
         prof, n_tr = {"trailing": 1.0, "total": 1.0}, 1
     ms_tr, ms_ldlt = prof["trailing"], prof["total"]
     alg_macs = fmas(n) * L * L  # L^2 limb-MACs per MP-FMA
-    achieved = alg_macs / (ms_tr * 1e-3) / 1e12
-    peak = api.peak_imad(local) / 1e12
-    traffic = None
-    ncu_file = os.path.join(ROOT, "profiles", f"ncu_trailing_{args.config}.json")
+    tc_path = prof.get("tc_products", 0.0) > 0.0
+    if tc_path:
+        # dominant kernel: the tcgen05 limb-product kernel (k_tc_bulk + its A preformat)
+        ms_k = prof["tc_products"]
+        achieved = alg_macs / (ms_k * 1e-3) / 1e12
+        peak = api.peak_i8mma(local) / 16.0 / 1e12  # u8 MAC/s -> limb-MAC/s (16 u8 MACs per limb-MAC)
+        ncu_file = os.path.join(ROOT, "profiles", f"ncu_tc_bulk_{args.config}.json")
+        round_bytes = fmas(n) * (12 * L + 32)  # read c, read product, write c (4 B limbs)
+        round_gbps = round_bytes / (max(prof["tc_round"], 1e-9) * 1e-3) / 1e9
+        roofline = {
+            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "Tlimb-MAC/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "k_tc_bulk: tcgen05.mma kind::i8 limb products of the trailing update (ldlt.cpp:122-129)",
+            "per_launch": f"avg over {n_tr} steps: {ms_k / n_tr:.4f} ms, {alg_macs / n_tr:.3e} algorithmic limb-MACs",
+            "algorithmic_units": "L^2 limb-MACs per MP-FMA (SURVEY 8d); the kernel forms the short product "
+                                 "(byte columns >= limb L-8, ~half of L^2), so frac can exceed the MMA utilisation",
+            "share_of_ldlt": ms_k / ms_ldlt,
+            "eager_ldlt_kernel_ms": prof,
+            "peak_how": "hk_peak_i8mma: back-to-back tcgen05.mma.kind::i8 M128 N256 K32 on every SM, best of 5, "
+                        "/16 u8 MACs per limb-MAC (MEASURED_PEAKS.json has no integer peak)",
+            "imad_peak": api.peak_imad(local) / 1e12,
+            "rounding_pass": {"kernel": "k_items<ItemTcRound> (+ k_tc_fix)", "ms": prof["tc_round"], "bound": "hbm",
+                              "achieved_GBps": round_gbps, "peak_GBps": hbm_peak_gbps(),
+                              "frac": round_gbps / hbm_peak_gbps(),
+                              "bytes": "12 L + 32 per MP-FMA (read c, read product, write c)"},
+        }
+    else:
+        ms_k = ms_tr
+        achieved = alg_macs / (ms_k * 1e-3) / 1e12
+        peak = api.peak_imad(local) / 1e12
+        ncu_file = os.path.join(ROOT, "profiles", f"ncu_trailing_{args.config}.json")
+        roofline = {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "Tlimb-MAC/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "trailing update k_items_hot<ItemTrailing2> (ldlt.cpp:122-129)",
+                    "per_launch": f"avg over {n_tr} launches: {ms_k / n_tr:.4f} ms, "
+                                  f"{alg_macs / n_tr:.3e} algorithmic limb-MACs",
+                    "share_of_ldlt": ms_k / ms_ldlt,
+                    "eager_ldlt_kernel_ms": prof,
+                    "peak_how": "hk_peak_imad: register-only IMAD.WIDE carry-chain microkernel on this GPU, "
+                                "best of 5 (MEASURED_PEAKS.json has no integer peak)"}
     if os.path.exists(ncu_file):
-        traffic = json.load(open(ncu_file)).get("dram_bytes_per_launch")
+        roofline["traffic"] = json.load(open(ncu_file)).get("dram_bytes_per_launch")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -270,15 +314,7 @@ def bench_ours(args, cfg):
         "lambda_min": repr(lam[0][0] + lam[1][0]),
         "e2e": {"value": fmas(n) / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "roofline": {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "Tlimb-MAC/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "trailing update k_items<ItemTrailing> (ldlt.cpp:122-129)",
-                     "per_launch": f"avg over {n_tr} launches: {ms_tr / n_tr:.4f} ms, "
-                                   f"{alg_macs / n_tr:.3e} algorithmic limb-MACs",
-                     "share_of_ldlt": ms_tr / ms_ldlt,
-                     "eager_ldlt_kernel_ms": prof,
-                     "peak_how": "hk_peak_imad: register-only IMAD.WIDE carry-chain microkernel on this GPU, "
-                                 "best of 5 (MEASURED_PEAKS.json has no integer peak)"},
+        "roofline": roofline,
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }

@@ -124,16 +124,24 @@ int hk_mp_batch(hk_ctx* ctx, int op, long long count, const uint32_t* a_l, const
 void* hk_stream(const hk_ctx* ctx);
 
 /* Measurement hook (no reference counterpart): run the LDLT once more,
- * eagerly on one stream, with CUDA events around every launch.  ms5 receives
- * the summed kernel milliseconds of [0] trailing update (the hot kernel,
- * ldlt.cpp:122-129), [1] reciprocal, [2] B column, [3] L store, and [4] the
- * whole eager LDLT; *n_trailing the number of trailing launches. */
-int hk_profile_ldlt(hk_ctx* ctx, double* ms5, long long* n_trailing);
+ * eagerly on one stream, with CUDA events around every launch.  ms7 receives
+ * the summed kernel milliseconds of [0] trailing update (the hot stage,
+ * ldlt.cpp:122-129), [1] reciprocal, [2] B column, [3] L store, [4] the whole
+ * eager LDLT, and on the tensor-core path the split of [0] into [5] limb
+ * products (A preformat + k_tc_bulk) and [6] certified rounding (+ fix-ups);
+ * *n_trailing the number of trailing steps. */
+int hk_profile_ldlt(hk_ctx* ctx, double* ms7, long long* n_trailing);
 
 /* Measured integer-MAC peak of the device: 32x32->64-bit limb MACs per second
  * of the IMAD.WIDE carry chain the MP kernels use (register-only microkernel
  * over all SMs).  The roofline denominator for the IMAD path. */
 int hk_peak_imad(int device, double* limb_macs_per_s);
+
+/* Measured int8 tensor-core peak: u8 x u8 MACs per second of back-to-back
+ * tcgen05.mma.kind::i8 (M=128, N=256, K=32, the product kernel's shape) on
+ * every SM.  The roofline denominator for the tensor-core path (one limb-MAC
+ * = 16 u8 MACs). */
+int hk_peak_i8mma(int device, double* u8_macs_per_s);
 
 /* ---- multi-GPU (one process per GPU) --------------------------
  * decompose_parallel's worker split (ldlt.hpp:97-99; W threads + slot channel,

@@ -67,6 +67,7 @@ def lib():
             "hk_stream": (vp, [vp]),
             "hk_profile_ldlt": (C.c_int, [vp, f64p, C.POINTER(C.c_longlong)]),
             "hk_peak_imad": (C.c_int, [C.c_int, f64p]),
+            "hk_peak_i8mma": (C.c_int, [C.c_int, f64p]),
             "hk_nccl_unique_id": (C.c_int, [C.c_char_p]),
             "hk_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]),
             "hk_world": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -155,6 +156,15 @@ def peak_imad(device: int = 0) -> float:
     rc = lib().hk_peak_imad(device, C.byref(v))
     if rc != HK_OK:
         raise RuntimeError(f"hk_peak_imad failed ({rc})")
+    return v.value
+
+
+def peak_i8mma(device: int = 0) -> float:
+    """Measured int8 tensor-core u8-MAC/s of the device (tcgen05 kind::i8; roofline denominator)."""
+    v = C.c_double()
+    rc = lib().hk_peak_i8mma(device, C.byref(v))
+    if rc != HK_OK:
+        raise RuntimeError(f"hk_peak_i8mma failed ({rc})")
     return v.value
 
 
@@ -312,11 +322,12 @@ class Context:
         return int(lib().hk_stream(self.h) or 0)
 
     def profile_ldlt(self):
-        """Eager instrumented LDLT: ({kernel: summed ms}, number of trailing launches)."""
-        ms = np.zeros(5)
+        """Eager instrumented LDLT: ({stage: summed ms}, number of trailing steps).  On the
+        tensor-core path `tc_products` + `tc_round` split `trailing`."""
+        ms = np.zeros(7)
         n = C.c_longlong()
         _check(lib().hk_profile_ldlt(self.h, ms.ctypes.data_as(C.POINTER(C.c_double)), C.byref(n)), self.h)
-        keys = ("trailing", "recip", "mulB", "storeL", "total")
+        keys = ("trailing", "recip", "mulB", "storeL", "total", "tc_products", "tc_round")
         return dict(zip(keys, ms.tolist())), n.value
 
     def launch_count(self) -> int:

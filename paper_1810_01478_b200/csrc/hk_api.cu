@@ -107,6 +107,7 @@ struct hk_ctx {
     uint32_t* tc_P = nullptr;
     size_t tc_P_words = 0;
     uint8_t* tc_A = nullptr;      // preformatted A operand of the current step
+    cudaEvent_t prof_mid = nullptr; // hk_profile_ldlt: recorded between TC products and rounding
     int* tc_fb_count = nullptr;   // uncertified items of the current step
     long long* tc_fb = nullptr;
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
@@ -374,6 +375,7 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
     }
     tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
                 b_buf(c, i), unsigned(ncols), st);
+    if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
     ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
     launch(c,
            hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count, c->tc_fb},
@@ -875,13 +877,47 @@ __global__ void __launch_bounds__(256) k_peak_imad(int iters, uint32_t seed, uin
     if (s == 0x12345678u) sink[threadIdx.x] = s;
 }
 
+// int8 tensor-core peak: one CTA per SM, thread 0 issues back-to-back
+// tcgen05.mma kind::i8 M=128 N=256 K=32 (the product kernel's shape) from
+// shared memory into two alternating TMEM accumulators.
+__global__ void __launch_bounds__(128, 1) k_peak_i8(int iters, uint32_t* sink) {
+    extern __shared__ __align__(1024) uint8_t psm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t taddr;
+    const int tid = threadIdx.x;
+    for (int q = tid; q < (4096 + 8192) / 4; q += blockDim.x) reinterpret_cast<uint32_t*>(psm)[q] = q * 2654435761u;
+    hk::tc::fence_async_smem();
+    if (tid < 32) hk::tc::tmem_alloc(&taddr, 512);
+    if (tid == 0) hk::tc::mbar_init(&bar, 1);
+    hk::tc::fence_before();
+    __syncthreads();
+    hk::tc::fence_after();
+    const uint32_t tm = taddr;
+    if (tid == 0) {
+        const uint32_t idesc = hk::tc::idesc_u8(128, 256, false, true);
+        const uint64_t ad = hk::tc::sdesc(psm, 128, 256), bd = hk::tc::sdesc(psm + 4096, 128, 512);
+        for (int it = 0; it < iters; ++it) hk::tc::mma_i8(tm + uint32_t((it & 1) * 256), ad, bd, idesc, it > 1);
+        hk::tc::commit(&bar);
+        hk::tc::mbar_wait(&bar, 0);
+    }
+    __syncthreads();
+    hk::tc::fence_after();
+    uint32_t v[8];
+    hk::tc::tmem_ld8(tm + ((uint32_t)((tid >> 5) * 32) << 16), v);
+    hk::tc::tmem_ld_wait();
+    if (v[0] == 0x12345678u && v[1] == 7u) sink[tid] = v[2];
+    hk::tc::fence_before();
+    __syncthreads();
+    if (tid < 32) hk::tc::tmem_dealloc(tm, 512);
+}
+
 } // namespace
 
 extern "C" {
 
 void* hk_stream(const hk_ctx* c) { return c ? (void*)c->st : nullptr; }
 
-int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
+int hk_profile_ldlt(hk_ctx* c, double* ms7, long long* n_trailing) {
     return guarded(c, [&] {
         if (c->n < 1) return fail(c, HK_ERR_INVALID, "hk_profile_ldlt: no moments loaded");
         const int N = c->n, L = c->L;
@@ -893,16 +929,20 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         struct Rec {
             int kind;
-            cudaEvent_t a, b;
+            cudaEvent_t a, b, mid;
         };
         std::vector<Rec> recs;
+        const bool tc = use_tc(c);
         auto timed = [&](int kind, auto&& fn) {
-            Rec r{kind, nullptr, nullptr};
+            Rec r{kind, nullptr, nullptr, nullptr};
             ck(cudaEventCreate(&r.a), "event");
             ck(cudaEventCreate(&r.b), "event");
+            if (kind == 0 && tc) ck(cudaEventCreate(&r.mid), "event");
+            c->prof_mid = r.mid;
             ck(cudaEventRecord(r.a, c->st), "event");
             fn();
             ck(cudaEventRecord(r.b, c->st), "event");
+            c->prof_mid = nullptr;
             recs.push_back(r);
         };
         const int wo = ws_op_words(L), wr = ws_recip_words(L);
@@ -930,11 +970,19 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
         }
         ck(cudaEventRecord(e1, c->st), "event");
         ck(cudaEventSynchronize(e1), "sync");
-        for (int q = 0; q < 5; ++q) ms5[q] = 0;
+        for (int q = 0; q < 7; ++q) ms7[q] = 0;
         for (auto& r : recs) {
             float ms = 0;
             ck(cudaEventElapsedTime(&ms, r.a, r.b), "elapsed");
-            ms5[r.kind] += ms;
+            ms7[r.kind] += ms;
+            if (r.mid) {
+                float m1 = 0, m2 = 0;
+                ck(cudaEventElapsedTime(&m1, r.a, r.mid), "elapsed");
+                ck(cudaEventElapsedTime(&m2, r.mid, r.b), "elapsed");
+                ms7[5] += m1;
+                ms7[6] += m2;
+                cudaEventDestroy(r.mid);
+            }
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }
@@ -942,7 +990,7 @@ int hk_profile_ldlt(hk_ctx* c, double* ms5, long long* n_trailing) {
         ck(cudaEventElapsedTime(&tot, e0, e1), "elapsed");
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        ms5[4] = tot;
+        ms7[4] = tot;
         *n_trailing = nt;
         const int rc = check_pivots(c);
         if (rc == HK_OK) c->factored = true;
@@ -971,6 +1019,40 @@ int hk_peak_imad(int device, double* out) {
         float ms = 0;
         cudaEventElapsedTime(&ms, a, b);
         const double macs = double(blocks) * threads * iters * 8.0;
+        if (ms > 0 && macs / (ms * 1e-3) > best) best = macs / (ms * 1e-3);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return HK_ERR_RUNTIME;
+    *out = best;
+    return HK_OK;
+}
+
+int hk_peak_i8mma(int device, double* out) {
+    if (!out) return HK_ERR_INVALID;
+    if (cudaSetDevice(device) != cudaSuccess) return HK_ERR_RUNTIME;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return HK_ERR_RUNTIME;
+    uint32_t* sink = nullptr;
+    if (cudaMalloc(&sink, 1024 * sizeof(uint32_t)) != cudaSuccess) return HK_ERR_RUNTIME;
+    const int smem = 120 * 1024; // one CTA per SM (512 TMEM columns each)
+    cudaFuncSetAttribute(k_peak_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = prop.multiProcessorCount, iters = 20000;
+    k_peak_i8<<<blocks, 128, smem>>>(64, sink); // warm-up
+    double best = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(a);
+        k_peak_i8<<<blocks, 128, smem>>>(iters, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        const double macs = double(blocks) * iters * 128.0 * 256.0 * 32.0;
         if (ms > 0 && macs / (ms * 1e-3) > best) best = macs / (ms * 1e-3);
     }
     cudaEventDestroy(a);

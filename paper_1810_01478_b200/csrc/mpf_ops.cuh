@@ -491,6 +491,7 @@ HK_DEV FxRecipWs fxrecipws_carve(uint32_t* b, int L) {
 }
 
 HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_t* wsb) {
+    HK_TRACE(0);
     FxRecipWs w = fxrecipws_carve(wsb, L);
     const bool w0 = warp_id() == 0;
     // seed: z0 = 1/m_hi in binary64, as a fixed-point value with 2 fraction limbs
@@ -525,6 +526,7 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
         cta_stage_padded(w.rw.Bp, Z, nf + 1);
         cta_sync();
         cta_mul(w.rw.A, mn, w.rw.Bp, nf + 1, w.rw.P, 0, w.CS);
+        HK_TRACE(1);
         const int FT = mn + nf; // fraction limbs of T
         const bool neg = w.rw.P[FT] != 0u; // T >= 1  ->  e <= 0
         for (int q = cta_tid(); q < nk; q += cta_threads()) {
@@ -537,6 +539,7 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
         cta_stage_padded(w.rw.Bp, w.rw.E, nk);
         cta_sync();
         cta_mul(w.rw.A, nf + 1, w.rw.Bp, nk, w.rw.P, 0, w.CS);
+        HK_TRACE(2);
         // Z' = (Z << 32 (nk - nf)) -/+ (D >> 32 nf), over nk + 1 limbs
         if (w0) {
             const int shl = nk - nf;
@@ -557,6 +560,7 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
             }
         }
         cta_sync();
+        HK_TRACE(3);
         uint32_t* t = Z;
         Z = Zn;
         Zn = t;
@@ -588,6 +592,7 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
         if (lane() == 0) w.sh[0] = rexp;
     }
     cta_sync();
+    HK_TRACE(4);
     const int rexp = w.sh[0];
     cta_copy(out, w.rw.T, L);
     cta_sync();

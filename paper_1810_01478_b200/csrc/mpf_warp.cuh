@@ -26,6 +26,10 @@
 // with warp_emu.h (lockstep emulation) so the arithmetic is unit-tested on CPU.
 #pragma once
 
+#ifndef HK_TRACE
+#define HK_TRACE(tag) // dev probes (tools/recip_probe.cu) record timestamps here
+#endif
+
 #include <cstdint>
 
 #if defined(HK_WARP_EMU)
@@ -374,6 +378,7 @@ HK_HD int cta_cs_words(int ntot) { return 96 * ((ntot + 31) / 32); }
 HK_DEV void cta_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint32_t* P, int tfirst, uint32_t* CS) {
     const int ntot = nA + nB, ng = (ntot - tfirst + 31) / 32;
     const int w = warp_id(), nw = num_warps();
+    HK_TRACE(5);
     for (int g = w; g < ng; g += nw) {
         uint32_t a0, a1, a2;
         colsum_group(A, nA, Bp, nB, tfirst + 32 * g, a0, a1, a2);
@@ -383,6 +388,7 @@ HK_DEV void cta_mul(const uint32_t* A, int nA, const uint32_t* Bp, int nB, uint3
         c[64] = a2;
     }
     cta_sync();
+    HK_TRACE(6);
     if (w == 0) {
         CarryState cs;
         for (int g = 0; g < ng; ++g) {

@@ -6,10 +6,10 @@ timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for cfg in c1 c3; do timeout 900 python bench.py --config $cfg --steps 2 --warmup 1 > gpurun_out/bench_$cfg.json 2> gpurun_out/bench_$cfg.err; done
+for cfg in c1 c3 c4; do timeout 1200 python bench.py --config $cfg --steps 2 --warmup 3 > gpurun_out/bench_$cfg.json 2> gpurun_out/bench_$cfg.err; done
 if [ "${NCU:-1}" = "1" ]; then
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
-$CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-$CMD > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:ItemTrailing2 -s 20 -c 1 -o gpurun_out/prof_trailing $CMD > gpurun_out/ncu_full.log 2>&1
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
+$CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_tc_bulk|ItemTcRound" -s 40 -c 2 -o gpurun_out/prof_tc_c2 $CMD > gpurun_out/ncu_full.log 2>&1
 fi
 echo done
