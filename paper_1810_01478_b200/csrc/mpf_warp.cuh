@@ -46,6 +46,7 @@ HK_DEV int lane() { return hk_emu::cur_lane(); }
 HK_DEV uint32_t ballot(bool p) { return hk_emu::ballot(p); }
 HK_DEV uint32_t shfl(uint32_t v, int src) { return hk_emu::shfl(v, src); }
 HK_DEV uint32_t shfl_up(uint32_t v, int d) { return hk_emu::shfl_up(v, d); }
+HK_DEV uint32_t shfl_down(uint32_t v, int d) { return hk_emu::shfl_down(v, d); }
 HK_DEV void wsync() { hk_emu::syncwarp(); }
 HK_DEV int clz32(uint32_t x) { return x ? __builtin_clz(x) : 32; }
 HK_DEV uint32_t fshr(uint32_t lo, uint32_t hi, int sh) {
@@ -86,6 +87,7 @@ HK_DEV int lane() { return int(threadIdx.x & 31); }
 HK_DEV uint32_t ballot(bool p) { return __ballot_sync(0xffffffffu, p); }
 HK_DEV uint32_t shfl(uint32_t v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 HK_DEV uint32_t shfl_up(uint32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+HK_DEV uint32_t shfl_down(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
 HK_DEV void wsync() { __syncwarp(); }
 HK_DEV int clz32(uint32_t x) { return __clz(x); }
 HK_DEV uint32_t fshr(uint32_t lo, uint32_t hi, int sh) { return __funnelshift_r(lo, hi, sh); }
@@ -554,6 +556,260 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
         cc = seg_carry(r, false, cc);
         if (j < nout) out[j] = r;
         ovf |= ballot(j == nout && r != 0u) != 0u;
+    }
+    if (ovf) { // mantissa overflowed to 2^(32 nout): renormalise
+        wsync();
+        for (int i = ln; i < nout; i += 32) out[i] = (i == nout - 1) ? 0x80000000u : 0u;
+        ++tb;
+    }
+    wsync();
+    return RMeta{(base - 32) + tb + 1, sign};
+}
+
+// ---- warp_round_sum_fast: the same contract and results as warp_round_sum,
+// with four window limbs per lane (128 per warp iteration): each pass pays its
+// ballot lookahead, branches and address arithmetic once per 128 limbs instead
+// of once per 32, and the carry inside a lane's four limbs is a plain add chain.
+
+// The lane's four words w0..w0+3 of bits [off + 32 w, off + 32 w + 32) of INT(d[0..n)).
+HK_DEV void read4(const uint32_t* d, int n, int off, int w0, uint32_t (&v)[4]) {
+    const int q = (off >> 5) + w0, sh = off & 31;
+    uint32_t x[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        const int idx = q + t;
+        x[t] = (idx >= 0 && idx < n) ? d[idx] : 0u;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = fshr(x[t], x[t + 1], sh);
+}
+
+// Carry-lookahead over lanes holding 4-limb groups: g = carry (or borrow) out
+// of the lane's own chain, p = a carry (borrow) into the lane would pass through
+// all four limbs.  Returns the carry into this lane; cio: carry into lane 0 in,
+// carry out of lane 31 out.
+HK_DEV uint32_t lane_carry_in(bool g, bool p, uint32_t& cio) {
+    const uint32_t G = ballot(g), P = ballot(p);
+    const uint32_t X = G | P;
+    const uint64_t S = (uint64_t)G + X + cio;
+    const uint32_t C = uint32_t(S) ^ G ^ X;
+    cio = uint32_t(S >> 32);
+    return (C >> lane()) & 1u;
+}
+
+HK_DEV void ripple_add4(uint32_t (&r)[4], uint32_t c) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint64_t s = (uint64_t)r[t] + c;
+        r[t] = uint32_t(s);
+        c = uint32_t(s >> 32);
+    }
+}
+HK_DEV void ripple_sub4(uint32_t (&r)[4], uint32_t b) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint64_t s = (uint64_t)r[t] - b;
+        r[t] = uint32_t(s);
+        b = uint32_t(s >> 63);
+    }
+}
+
+// Bit length of INT(d[0..n)) (0 for zero).  Warp-uniform.
+HK_DEV int warp_bitlen4(const uint32_t* d, int n) {
+    for (int b0 = ((n - 1) >> 7) << 7; b0 >= 0; b0 -= 128) {
+        const int w0 = b0 + 4 * lane();
+        int top = -1;
+        uint32_t tv = 0u;
+#pragma unroll
+        for (int t = 3; t >= 0; --t) {
+            const int w = w0 + t;
+            const uint32_t v = w < n ? d[w] : 0u;
+            if (top < 0 && v != 0u) {
+                top = w;
+                tv = v;
+            }
+        }
+        const uint32_t m = ballot(top >= 0);
+        if (m) {
+            const int hl = 31 - clz32(m);
+            const int tw = int(shfl(uint32_t(top), hl));
+            const uint32_t v = shfl(tv, hl);
+            return tw * 32 + (32 - clz32(v));
+        }
+    }
+    return 0;
+}
+
+// Bits [lo, hi] (0 <= lo <= hi) of INT(d[0..n)): bit0 = any set, bit1 = all set.
+HK_DEV int warp_bit_range4(const uint32_t* d, int n, int lo, int hi) {
+    bool any = false, all = true;
+    const int ql = lo >> 5, qh = hi >> 5;
+    for (int b0 = ql; b0 <= qh; b0 += 128) {
+        const int w0 = b0 + 4 * lane();
+        bool a = false, na = false;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int w = w0 + t;
+            if (w <= qh) {
+                const int s = lo - 32 * w > 0 ? lo - 32 * w : 0;
+                const int e = hi - 32 * w < 31 ? hi - 32 * w : 31;
+                const uint32_t mask = (e == 31 ? 0xffffffffu : ((1u << (e + 1)) - 1u)) & ~((1u << s) - 1u);
+                const uint32_t v = (w < n ? d[w] : 0u) & mask;
+                a |= v != 0u;
+                na |= v != mask;
+            }
+        }
+        any |= ballot(a) != 0u;
+        all &= ballot(na) == 0u;
+    }
+    return (any ? 1 : 0) | (all ? 2 : 0);
+}
+
+HK_DEV RMeta warp_round_sum_fast(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_t* out, int nout,
+                                 int ubit = kExact, bool* ok = nullptr) {
+    const int ln = lane();
+    if (ok) *ok = true;
+    const int blX = Xin.sign ? warp_bitlen4(Xin.d, Xin.n) : 0;
+    const int blY = Yin.sign ? warp_bitlen4(Yin.d, Yin.n) : 0;
+    if (blX == 0 && blY == 0) {
+        for (int i = ln; i < nout; i += 32) out[i] = 0u;
+        wsync();
+        return RMeta{0, 0};
+    }
+    const int TX = Xin.lsb + blX, TY = Yin.lsb + blY;
+    const bool xbig = blY == 0 || (blX != 0 && TX >= TY);
+    const Opd Big = xbig ? Xin : Yin;
+    const Opd Small = xbig ? Yin : Xin;
+    const int blS = xbig ? blY : blX;
+    const int Tbig = xbig ? TX : TY;
+    const int W = max(max(Big.n, Small.n), nout) + 3; // window limbs 1..W, limb 0 = sticky
+    const int base = Tbig - 32 * (W - 1);             // absolute bit of window limb 1, bit 0
+    const int nw = W + 1;
+    const bool small_live = blS != 0;
+    bool sticky = false;
+    if (small_live) {
+        const int rel = base - Small.lsb; // Small's bits below the window
+        if (rel > 0) sticky = (warp_bit_range4(Small.d, Small.n, 0, min(rel, 32 * Small.n) - 1) & 1) != 0;
+    }
+    const bool eff_sub = small_live && (Big.sign != Small.sign);
+
+    // G = |Big| +- |Small| over limbs 0..W (limb 0 holds the sticky unit of Small)
+    const int offB = (base - 32) - Big.lsb, offS = (base - 32) - Small.lsb;
+    const int nS = small_live ? Small.n : 0;
+    uint32_t c = 0;
+    for (int b0 = 0; b0 < nw; b0 += 128) {
+        const int w0 = b0 + 4 * ln;
+        uint32_t vb[4], vs[4], r[4];
+        read4(Big.d, Big.n, offB, w0, vb);
+        read4(Small.d, nS, offS, w0, vs);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int w = w0 + t;
+            if (w == 0) {
+                vb[t] = 0u;
+                vs[t] = sticky ? 1u : 0u;
+            } else if (w > W) {
+                vb[t] = vs[t] = 0u;
+            }
+        }
+        if (eff_sub) {
+            uint32_t br = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint64_t d = (uint64_t)vb[t] - vs[t] - br;
+                r[t] = uint32_t(d);
+                br = uint32_t(d >> 63);
+            }
+            const uint32_t ci = lane_carry_in(br != 0u, (r[0] | r[1] | r[2] | r[3]) == 0u, c);
+            ripple_sub4(r, ci);
+        } else {
+            uint32_t cr = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint64_t s2 = (uint64_t)vb[t] + vs[t] + cr;
+                r[t] = uint32_t(s2);
+                cr = uint32_t(s2 >> 32);
+            }
+            const uint32_t ci = lane_carry_in(cr != 0u, (r[0] & r[1] & r[2] & r[3]) == 0xffffffffu, c);
+            ripple_add4(r, ci);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (w0 + t <= W) G[w0 + t] = r[t];
+    }
+    int sign = Big.sign;
+    if (eff_sub && c) { // negative: two's-complement negate
+        wsync();
+        uint32_t cc = 1;
+        for (int b0 = 0; b0 < nw; b0 += 128) {
+            const int w0 = b0 + 4 * ln;
+            uint32_t r[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) r[t] = w0 + t <= W ? ~G[w0 + t] : 0u;
+            const uint32_t ci = lane_carry_in(false, (r[0] & r[1] & r[2] & r[3]) == 0xffffffffu, cc);
+            ripple_add4(r, ci);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (w0 + t <= W) G[w0 + t] = r[t];
+        }
+        sign = -sign;
+    }
+    wsync();
+    const int bl = warp_bitlen4(G, nw);
+    if (bl == 0) {
+        if (ubit != kExact) { // X + Y = 0 exactly but the true value is a tiny delta
+            *ok = false;
+            return RMeta{0, 0};
+        }
+        for (int i = ln; i < nout; i += 32) out[i] = 0u;
+        wsync();
+        return RMeta{0, 0};
+    }
+    int tb = bl - 1;                 // top bit index in G
+    const int lsbpos = tb - 32 * nout + 1;
+    bool rbit = false, st = false;
+    if (lsbpos - 1 >= 0) rbit = (G[(lsbpos - 1) >> 5] >> ((lsbpos - 1) & 31)) & 1u;
+    if (ubit != kExact) {
+        // as warp_round_sum: the distance to the nearest rounding midpoint must
+        // exceed the uncertainty 2^ubit (the sticky limb [0,32) is uncertain)
+        const int rb_rel = lsbpos - 1;
+        int u_rel = ubit - (base - 32);
+        if (u_rel < 32) u_rel = 32;
+        bool safe = rb_rel - u_rel >= 4;
+        if (safe) {
+            const int rs = warp_bit_range4(G, nw, u_rel, rb_rel - 1);
+            safe = rbit ? (rs & 1) != 0 : (rs & 2) == 0;
+        }
+        if (!safe) {
+            *ok = false;
+            return RMeta{0, 0};
+        }
+        st = rbit; // safe with the round bit set: a set bit lies in [u_rel, rb_rel)
+    } else if (lsbpos - 1 > 0) {
+        st = (warp_bit_range4(G, nw, 0, lsbpos - 2) & 1) != 0;
+    }
+    const bool low0 = lsbpos >= 0 && ((G[lsbpos >> 5] >> (lsbpos & 31)) & 1u);
+    const bool inc = rbit && (st || low0);
+    wsync(); // every read of X / Y done before `out` (which may alias X or Y) is written
+    uint32_t cc = inc ? 1u : 0u;
+    bool ovf = false;
+    for (int b0 = 0; b0 <= nout; b0 += 128) {
+        const int j0 = b0 + 4 * ln;
+        uint32_t r[4];
+        read4(G, nw, lsbpos, j0, r);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (j0 + t >= nout) r[t] = 0u;
+        const uint32_t ci = lane_carry_in(false, (r[0] & r[1] & r[2] & r[3]) == 0xffffffffu, cc);
+        ripple_add4(r, ci);
+        bool o = false;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int j = j0 + t;
+            if (j < nout) out[j] = r[t];
+            if (j == nout) o = r[t] != 0u;
+        }
+        ovf |= ballot(o) != 0u;
     }
     if (ovf) { // mantissa overflowed to 2^(32 nout): renormalise
         wsync();

@@ -49,6 +49,16 @@ inline uint32_t shfl(uint32_t v, int src) {
     return r;
 }
 
+inline uint32_t shfl_down(uint32_t v, int d) {
+    Warp& w = *cur_warp();
+    const int l = cur_lane();
+    w.slot[l] = v;
+    w.bar.arrive_and_wait();
+    const uint32_t r = l + d < 32 ? w.slot[l + d] : v;
+    w.bar.arrive_and_wait();
+    return r;
+}
+
 inline uint32_t shfl_up(uint32_t v, int d) {
     Warp& w = *cur_warp();
     const int l = cur_lane();
