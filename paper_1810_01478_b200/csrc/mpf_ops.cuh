@@ -75,12 +75,12 @@ HK_DEV RMeta round_with_product(const Opd& X, const uint32_t* xd, const uint32_t
     if (t0 > 0) {
         const Opd Yh{ws.P + t0, 2 * L - t0, lsbP + 32 * t0, sp};
         bool ok = false;
-        const RMeta r = warp_round_sum_fast(X, Yh, ws.G, out, L, lsbP + 32 * t0 + 46, &ok);
+        const RMeta r = warp_round_sum(X, Yh, ws.G, out, L, lsbP + 32 * t0 + 46, &ok);
         if (ok) return r;
         stage_and_mul(xd, yd, L, ws, 0); // the window overwrote A / Bp: restage, exact product
     }
     const Opd Y{ws.P, 2 * L, lsbP, sp};
-    return warp_round_sum_fast(X, Y, ws.G, out, L);
+    return warp_round_sum(X, Y, ws.G, out, L);
 }
 
 // out = RNE(c - x*y).  c / out may alias (in global memory).
@@ -139,12 +139,12 @@ HK_DEV void warp_fms2(const uint32_t* c0, Meta cm0, const uint32_t* x0, Meta xm0
     wsync();
     const int lsb0 = xm0.exp + ym.exp - 64 * L, lsb1 = xm1.exp + ym.exp - 64 * L;
     bool ok = false;
-    RMeta a = warp_round_sum_fast(Opd{c0, L, cm0.exp - 32 * L, cm0.sign},
+    RMeta a = warp_round_sum(Opd{c0, L, cm0.exp - 32 * L, cm0.sign},
                                   Opd{P0 + t0, 2 * L - t0, lsb0 + 32 * t0, sp0}, ws, out0, L,
                                   lsb0 + 32 * t0 + 46, &ok);
     if (ok) r0 = Meta{a.exp, a.sign};
     else r0 = warp_fms(c0, cm0, x0, xm0, yd, ym, out0, L, opws_carve(ws, L));
-    a = warp_round_sum_fast(Opd{c1, L, cm1.exp - 32 * L, cm1.sign}, Opd{P1 + t0, 2 * L - t0, lsb1 + 32 * t0, sp1},
+    a = warp_round_sum(Opd{c1, L, cm1.exp - 32 * L, cm1.sign}, Opd{P1 + t0, 2 * L - t0, lsb1 + 32 * t0, sp1},
                             ws, out1, L, lsb1 + 32 * t0 + 46, &ok);
     if (ok) r1 = Meta{a.exp, a.sign};
     else r1 = warp_fms(c1, cm1, x1, xm1, yd, ym, out1, L, opws_carve(ws, L));
@@ -155,7 +155,7 @@ HK_DEV Meta warp_addr(const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym, 
                       const OpWs& ws) {
     const Opd X{xd, L, xm.exp - 32 * L, xm.sign};
     const Opd Y{yd, L, ym.exp - 32 * L, ym.sign};
-    const RMeta r = warp_round_sum_fast(X, Y, ws.G, out, L);
+    const RMeta r = warp_round_sum(X, Y, ws.G, out, L);
     return Meta{r.exp, r.sign};
 }
 
@@ -413,7 +413,7 @@ HK_DEV Meta cta_round_with_product(const Opd& X, const uint32_t* xd, const uint3
         bool ok = false;
         if (warp_id() == 0) {
             const Opd Yh{w.op.P + t0, 2 * L - t0, lsbP + 32 * t0, sp};
-            r = warp_round_sum_fast(X, Yh, w.op.G, out, L, lsbP + 32 * t0 + 46, &ok);
+            r = warp_round_sum(X, Yh, w.op.G, out, L, lsbP + 32 * t0 + 46, &ok);
         }
         r = cta_bcast_meta(w, r, ok, &ok);
         if (ok) return Meta{r.exp, r.sign};
@@ -422,7 +422,7 @@ HK_DEV Meta cta_round_with_product(const Opd& X, const uint32_t* xd, const uint3
     RMeta r{0, 0};
     if (warp_id() == 0) {
         const Opd Y{w.op.P, 2 * L, lsbP, sp};
-        r = warp_round_sum_fast(X, Y, w.op.G, out, L);
+        r = warp_round_sum(X, Y, w.op.G, out, L);
     }
     r = cta_bcast_meta(w, r, true, nullptr);
     return Meta{r.exp, r.sign};

@@ -137,17 +137,6 @@ struct Opd {
     int sign; // -1, 0, +1 (0 => value zero, d ignored)
 };
 
-// bits [b, b+32) of |X| where b is an absolute bit position.
-HK_DEV uint32_t opd_word(const Opd& X, int b) {
-    const int r = b - X.lsb;
-    if (r >= 32 * X.n || r <= -32) return 0;
-    const int q = r >> 5; // floor division (arithmetic shift)
-    const int sh = r & 31;
-    const uint32_t lo = (q >= 0 && q < X.n) ? X.d[q] : 0u;
-    const uint32_t hi = (q + 1 >= 0 && q + 1 < X.n) ? X.d[q + 1] : 0u;
-    return fshr(lo, hi, sh);
-}
-
 // Carry-lookahead over one 32-limb segment (one limb per lane).  `w` is the
 // lane's limb after its local add, `g` whether that add overflowed; `cin` is
 // the (warp-uniform) carry into lane 0.  Returns the carry out of lane 31.
@@ -170,36 +159,6 @@ HK_DEV uint32_t seg_borrow(uint32_t& w, bool bor, uint32_t bin) {
     const uint32_t C = uint32_t(S) ^ G ^ X;
     w -= (C >> lane()) & 1u;
     return uint32_t(S >> 32);
-}
-
-// Bit length of the integer d[0..n) (0 for zero).  Warp-uniform result.
-HK_DEV int warp_bitlen(const uint32_t* d, int n) {
-    for (int base = ((n - 1) >> 5) << 5; base >= 0; base -= 32) {
-        const int idx = base + lane();
-        const uint32_t v = idx < n ? d[idx] : 0u;
-        const uint32_t m = ballot(v != 0u);
-        if (m) {
-            const int hl = 31 - clz32(m);
-            const uint32_t top = shfl(v, hl);
-            return (base + hl) * 32 + (32 - clz32(top));
-        }
-    }
-    return 0;
-}
-
-// Is any bit of d[0..n) below relative bit position `rel` set?  Warp-uniform.
-HK_DEV bool warp_any_below(const uint32_t* d, int n, int rel) {
-    if (rel <= 0) return false;
-    const int full = rel >> 5, part = rel & 31;
-    const int lim = min(n, full + (part ? 1 : 0));
-    bool any = false;
-    for (int base = 0; base < lim; base += 32) {
-        const int idx = base + lane();
-        uint32_t v = idx < lim ? d[idx] : 0u;
-        if (idx == full) v &= (part ? ((1u << part) - 1u) : 0u);
-        any |= ballot(v != 0u) != 0u;
-    }
-    return any;
 }
 
 // Stage `n` limbs from `src` into `dst` (lane-strided copy).
@@ -419,157 +378,10 @@ struct RMeta {
 
 constexpr int kExact = -0x40000000; // "no uncertainty" for warp_round_sum's ubit
 
-// Range statistics of bits [lo, hi] (relative positions, lo <= hi) of d[0..n):
-// returns bit0 = any bit set, bit1 = all bits set.  Warp-uniform.
-HK_DEV int warp_bit_range(const uint32_t* d, int n, int lo, int hi) {
-    bool any = false, all = true;
-    const int ql = lo >> 5, qh = hi >> 5;
-    for (int q0 = ql; q0 <= qh; q0 += 32) {
-        const int idx = q0 + lane();
-        const bool in = idx <= qh;
-        uint32_t mask = 0;
-        if (in) {
-            const int s = lo - 32 * idx > 0 ? lo - 32 * idx : 0;
-            const int e = hi - 32 * idx < 31 ? hi - 32 * idx : 31;
-            mask = (e == 31 ? 0xffffffffu : ((1u << (e + 1)) - 1u)) & ~((1u << s) - 1u);
-        }
-        const uint32_t v = (in && idx < n) ? d[idx] : 0u;
-        any |= ballot((v & mask) != 0u) != 0u;
-        all &= ballot(in && (v & mask) != mask) == 0u;
-    }
-    return (any ? 1 : 0) | (all ? 2 : 0);
-}
-
-// out[0..nout) = RNE_{32 nout}(X + Y).  G is a smem scratch window of at least
-// max(X.n, Y.n, nout) + 4 limbs that must not alias X, Y or out.  X or Y may
-// alias `out` (all operand reads finish before the first write).
-//
-// Ziv mode (ubit != kExact): the true value is X + Y + delta with |delta| <
-// 2^ubit (absolute bit position) of unknown sign.  If no rounding midpoint can
-// lie within that distance, the correctly rounded result of the true value is
-// RNE(X + Y): it is written and *ok = true.  Otherwise nothing is written and
-// *ok = false (the caller recomputes exactly).
-HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_t* out, int nout,
-                            int ubit = kExact, bool* ok = nullptr) {
-    const int ln = lane();
-    if (ok) *ok = true;
-    const int blX = Xin.sign ? warp_bitlen(Xin.d, Xin.n) : 0;
-    const int blY = Yin.sign ? warp_bitlen(Yin.d, Yin.n) : 0;
-    if (blX == 0 && blY == 0) {
-        for (int i = ln; i < nout; i += 32) out[i] = 0u;
-        wsync();
-        return RMeta{0, 0};
-    }
-    const int TX = Xin.lsb + blX, TY = Yin.lsb + blY;
-    const bool xbig = blY == 0 || (blX != 0 && TX >= TY);
-    const Opd Big = xbig ? Xin : Yin;
-    const Opd Small = xbig ? Yin : Xin;
-    const int blS = xbig ? blY : blX;
-    const int Tbig = xbig ? TX : TY;
-    const int W = max(max(Big.n, Small.n), nout) + 3; // window limbs 1..W, limb 0 = sticky
-    const int base = Tbig - 32 * (W - 1);             // absolute bit of window limb 1, bit 0
-    const bool small_live = blS != 0;
-    const bool sticky = small_live && warp_any_below(Small.d, Small.n, base - Small.lsb);
-    const bool eff_sub = small_live && (Big.sign != Small.sign);
-
-    // G = |Big| +- |Small| over limbs 0..W (limb 0 holds the sticky unit of Small)
-    uint32_t c = 0;
-    for (int b0 = 0; b0 <= W; b0 += 32) {
-        const int w = b0 + ln;
-        uint32_t vb = 0, vs = 0;
-        if (w >= 1 && w <= W) {
-            const int bit = base + 32 * (w - 1);
-            vb = opd_word(Big, bit);
-            vs = small_live ? opd_word(Small, bit) : 0u;
-        } else if (w == 0) {
-            vs = sticky ? 1u : 0u;
-        }
-        uint32_t r;
-        if (eff_sub) {
-            r = vb - vs;
-            c = seg_borrow(r, vb < vs, c);
-        } else {
-            r = vb + vs;
-            c = seg_carry(r, r < vb, c);
-        }
-        if (w <= W) G[w] = r;
-    }
-    int sign = Big.sign;
-    if (eff_sub && c) { // negative: two's-complement negate
-        wsync();
-        uint32_t cc = 1;
-        for (int b0 = 0; b0 <= W; b0 += 32) {
-            const int w = b0 + ln;
-            uint32_t r = w <= W ? ~G[w] : 0u;
-            cc = seg_carry(r, false, cc);
-            if (w <= W) G[w] = r;
-        }
-        sign = -sign;
-    }
-    wsync();
-    const int bl = warp_bitlen(G, W + 1);
-    if (bl == 0) {
-        if (ubit != kExact) { // X + Y = 0 exactly but the true value is a tiny delta
-            *ok = false;
-            return RMeta{0, 0};
-        }
-        for (int i = ln; i < nout; i += 32) out[i] = 0u;
-        wsync();
-        return RMeta{0, 0};
-    }
-    int tb = bl - 1;                 // top bit index in G
-    const int lsbpos = tb - 32 * nout + 1;
-    const Opd Gw{G, W + 1, 0, 1};
-    bool rb = false, st = false;
-    if (lsbpos - 1 >= 0) {
-        rb = (G[(lsbpos - 1) >> 5] >> ((lsbpos - 1) & 31)) & 1u;
-        st = warp_any_below(G, W + 1, lsbpos - 1);
-    }
-    if (ubit != kExact) {
-        // distance of |X+Y| to the nearest rounding midpoint must exceed the
-        // uncertainty: with the round bit set the bits below must not all be 0,
-        // with it clear they must not all be 1 (down to the uncertain position;
-        // the sticky limb [0,32) counts as uncertain).
-        const int rb_rel = lsbpos - 1;
-        int u_rel = ubit - (base - 32);
-        if (u_rel < 32) u_rel = 32;
-        bool safe = rb_rel - u_rel >= 4;
-        if (safe) {
-            const int rs = warp_bit_range(G, W + 1, u_rel, rb_rel - 1);
-            safe = rb ? (rs & 1) != 0 : (rs & 2) == 0;
-        }
-        if (!safe) {
-            *ok = false;
-            return RMeta{0, 0};
-        }
-    }
-    const uint32_t low0 = opd_word(Gw, lsbpos);
-    const bool inc = rb && (st || (low0 & 1u));
-    wsync(); // every read of X / Y / G done before `out` (which may alias X or Y) is written
-    // Lanes at index >= nout hold 0, so a carry out of limb nout-1 lands (and
-    // stops) on lane index nout; the loop runs far enough to include it.
-    uint32_t cc = inc ? 1u : 0u;
-    bool ovf = false;
-    for (int b0 = 0; b0 <= nout; b0 += 32) {
-        const int j = b0 + ln;
-        uint32_t r = j < nout ? opd_word(Gw, lsbpos + 32 * j) : 0u;
-        cc = seg_carry(r, false, cc);
-        if (j < nout) out[j] = r;
-        ovf |= ballot(j == nout && r != 0u) != 0u;
-    }
-    if (ovf) { // mantissa overflowed to 2^(32 nout): renormalise
-        wsync();
-        for (int i = ln; i < nout; i += 32) out[i] = (i == nout - 1) ? 0x80000000u : 0u;
-        ++tb;
-    }
-    wsync();
-    return RMeta{(base - 32) + tb + 1, sign};
-}
-
-// ---- warp_round_sum_fast: the same contract and results as warp_round_sum,
-// with four window limbs per lane (128 per warp iteration): each pass pays its
-// ballot lookahead, branches and address arithmetic once per 128 limbs instead
-// of once per 32, and the carry inside a lane's four limbs is a plain add chain.
+// ---- correctly rounded sum, four window limbs per lane (128 per warp
+// iteration): each pass pays its ballot lookahead, branches and address
+// arithmetic once per 128 limbs, and the carry inside a lane's four limbs is a
+// plain add chain.
 
 // The lane's four words w0..w0+3 of bits [off + 32 w, off + 32 w + 32) of INT(d[0..n)).
 HK_DEV void read4(const uint32_t* d, int n, int off, int w0, uint32_t (&v)[4]) {
@@ -615,7 +427,7 @@ HK_DEV void ripple_sub4(uint32_t (&r)[4], uint32_t b) {
 }
 
 // Bit length of INT(d[0..n)) (0 for zero).  Warp-uniform.
-HK_DEV int warp_bitlen4(const uint32_t* d, int n) {
+HK_DEV int warp_bitlen(const uint32_t* d, int n) {
     for (int b0 = ((n - 1) >> 7) << 7; b0 >= 0; b0 -= 128) {
         const int w0 = b0 + 4 * lane();
         int top = -1;
@@ -641,7 +453,7 @@ HK_DEV int warp_bitlen4(const uint32_t* d, int n) {
 }
 
 // Bits [lo, hi] (0 <= lo <= hi) of INT(d[0..n)): bit0 = any set, bit1 = all set.
-HK_DEV int warp_bit_range4(const uint32_t* d, int n, int lo, int hi) {
+HK_DEV int warp_bit_range(const uint32_t* d, int n, int lo, int hi) {
     bool any = false, all = true;
     const int ql = lo >> 5, qh = hi >> 5;
     for (int b0 = ql; b0 <= qh; b0 += 128) {
@@ -665,12 +477,21 @@ HK_DEV int warp_bit_range4(const uint32_t* d, int n, int lo, int hi) {
     return (any ? 1 : 0) | (all ? 2 : 0);
 }
 
-HK_DEV RMeta warp_round_sum_fast(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_t* out, int nout,
+// out[0..nout) = RNE_{32 nout}(X + Y).  G is a smem scratch window of at least
+// max(X.n, Y.n, nout) + 4 limbs that must not alias X, Y or out.  X or Y may
+// alias `out` (all operand reads finish before the first write).
+//
+// Ziv mode (ubit != kExact): the true value is X + Y + delta with |delta| <
+// 2^ubit (absolute bit position) of unknown sign.  If no rounding midpoint can
+// lie within that distance, the correctly rounded result of the true value is
+// RNE(X + Y): it is written and *ok = true.  Otherwise nothing is written and
+// *ok = false (the caller recomputes exactly).
+HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_t* out, int nout,
                                  int ubit = kExact, bool* ok = nullptr) {
     const int ln = lane();
     if (ok) *ok = true;
-    const int blX = Xin.sign ? warp_bitlen4(Xin.d, Xin.n) : 0;
-    const int blY = Yin.sign ? warp_bitlen4(Yin.d, Yin.n) : 0;
+    const int blX = Xin.sign ? warp_bitlen(Xin.d, Xin.n) : 0;
+    const int blY = Yin.sign ? warp_bitlen(Yin.d, Yin.n) : 0;
     if (blX == 0 && blY == 0) {
         for (int i = ln; i < nout; i += 32) out[i] = 0u;
         wsync();
@@ -689,7 +510,7 @@ HK_DEV RMeta warp_round_sum_fast(const Opd& Xin, const Opd& Yin, uint32_t* G, ui
     bool sticky = false;
     if (small_live) {
         const int rel = base - Small.lsb; // Small's bits below the window
-        if (rel > 0) sticky = (warp_bit_range4(Small.d, Small.n, 0, min(rel, 32 * Small.n) - 1) & 1) != 0;
+        if (rel > 0) sticky = (warp_bit_range(Small.d, Small.n, 0, min(rel, 32 * Small.n) - 1) & 1) != 0;
     }
     const bool eff_sub = small_live && (Big.sign != Small.sign);
 
@@ -755,7 +576,7 @@ HK_DEV RMeta warp_round_sum_fast(const Opd& Xin, const Opd& Yin, uint32_t* G, ui
         sign = -sign;
     }
     wsync();
-    const int bl = warp_bitlen4(G, nw);
+    const int bl = warp_bitlen(G, nw);
     if (bl == 0) {
         if (ubit != kExact) { // X + Y = 0 exactly but the true value is a tiny delta
             *ok = false;
@@ -777,7 +598,7 @@ HK_DEV RMeta warp_round_sum_fast(const Opd& Xin, const Opd& Yin, uint32_t* G, ui
         if (u_rel < 32) u_rel = 32;
         bool safe = rb_rel - u_rel >= 4;
         if (safe) {
-            const int rs = warp_bit_range4(G, nw, u_rel, rb_rel - 1);
+            const int rs = warp_bit_range(G, nw, u_rel, rb_rel - 1);
             safe = rbit ? (rs & 1) != 0 : (rs & 2) == 0;
         }
         if (!safe) {
@@ -786,7 +607,7 @@ HK_DEV RMeta warp_round_sum_fast(const Opd& Xin, const Opd& Yin, uint32_t* G, ui
         }
         st = rbit; // safe with the round bit set: a set bit lies in [u_rel, rb_rel)
     } else if (lsbpos - 1 > 0) {
-        st = (warp_bit_range4(G, nw, 0, lsbpos - 2) & 1) != 0;
+        st = (warp_bit_range(G, nw, 0, lsbpos - 2) & 1) != 0;
     }
     const bool low0 = lsbpos >= 0 && ((G[lsbpos >> 5] >> (lsbpos & 31)) & 1u);
     const bool inc = rbit && (st || low0);

@@ -327,7 +327,7 @@ struct ItemTcRound {
         const Opd X{Xs, L, cm.exp - 32 * L, cm.sign};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
-        const RMeta rr = warp_round_sum_fast(X, Y, Ys + align4(L + kTcGuard), c, L,
+        const RMeta rr = warp_round_sum(X, Y, Ys + align4(L + kTcGuard), c, L,
                                              lsbP + 32 * t0 + 46, &ok);
         if (lane() == 0) {
             if (ok) {
@@ -379,7 +379,7 @@ struct ItemTcRoundInv {
         const Opd Xo{Xs, L, cm.exp - 32 * L, cm.sign};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
-        const RMeta rr = warp_round_sum_fast(Xo, Y, Ys + align4(L + kTcGuard), o, L,
+        const RMeta rr = warp_round_sum(Xo, Y, Ys + align4(L + kTcGuard), o, L,
                                              lsbP + 32 * t0 + 46, &ok);
         if (lane() == 0) {
             if (ok) {
