@@ -81,8 +81,9 @@ struct hk_ctx {
     int n = 0, m = 0, k = 0;
     cudaStream_t st = nullptr;  // bulk / default stream of the context
     cudaStream_t st2 = nullptr; // high-priority look-ahead stream
+    cudaStream_t st3 = nullptr; // high-priority: off-diagonal part of the look-ahead column
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
-    std::vector<cudaEvent_t> evP, evR, evU; // per-step dependencies (graph capture)
+    std::vector<cudaEvent_t> evP, evR, evU, evD, evO; // per-step dependencies (graph capture)
     DevArr mu, S, R, B, X, Y, T, T2, M;
     int* d_err = nullptr;
     std::string err;
@@ -422,6 +423,9 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     std::vector<cudaEvent_t>& evP = c->evP;
     std::vector<cudaEvent_t>& evR = c->evR;
     std::vector<cudaEvent_t>& evU = c->evU;
+    std::vector<cudaEvent_t>& evD = c->evD;
+    std::vector<cudaEvent_t>& evO = c->evO;
+    cudaStream_t la2 = c->st3;
     ck(cudaEventRecord(c->evFork, bulk), "fork");
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
     const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
@@ -440,10 +444,17 @@ void enqueue_ldlt_steps(hk_ctx* c) {
             ck(cudaEventRecord(evR[i - 1], bulk), "evR");
         }
         if (i + 1 < N) {
+            // P(i+1): the diagonal entry -> reciprocal on `la`, the rest of the
+            // column concurrently on `la2`; B_{i+1} needs both.
             if (i > 0) ck(cudaStreamWaitEvent(la, evU[i - 1], 0), "wait U");
-            launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err}, N - i - 1, wc, la);
+            ck(cudaEventRecord(evD[i + 1], la), "evD");
+            ck(cudaStreamWaitEvent(la2, evD[i + 1], 0), "wait D");
+            launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 1}, N - i - 2, wc, la2);
+            ck(cudaEventRecord(evO[i + 1], la2), "evO");
+            launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 0}, 1, wc, la);
             launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la);
             if (i >= 2) ck(cudaStreamWaitEvent(la, evR[i - 2], 0), "wait R");
+            ck(cudaStreamWaitEvent(la, evO[i + 1], 0), "wait O");
             launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err}, N - i - 2,
                        wc, la);
             ck(cudaEventRecord(evP[i + 1], la), "evP");
@@ -465,6 +476,8 @@ void ensure_step_events(hk_ctx* c, int N) {
     grow(c->evP, N);
     grow(c->evR, N);
     grow(c->evU, N);
+    grow(c->evD, N);
+    grow(c->evO, N);
 }
 
 int check_pivots(hk_ctx* c) {
@@ -506,6 +519,7 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         int lo = 0, hi = 0;
         ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
         ck(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi), "cudaStreamCreate la");
+        ck(cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, hi), "cudaStreamCreate la2");
         ck(cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming), "event");
         ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
@@ -548,9 +562,12 @@ void hk_destroy(hk_ctx* c) {
     for (auto e : c->evP) cudaEventDestroy(e);
     for (auto e : c->evR) cudaEventDestroy(e);
     for (auto e : c->evU) cudaEventDestroy(e);
+    for (auto e : c->evD) cudaEventDestroy(e);
+    for (auto e : c->evO) cudaEventDestroy(e);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
     if (c->st2) cudaStreamDestroy(c->st2);
+    if (c->st3) cudaStreamDestroy(c->st3);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
 }

@@ -441,13 +441,14 @@ struct CItemMulB { // B_i(k) = RNE(S(k,i) R_i), k = i+1+t
     }
 };
 
-struct CItemColUpd { // look-ahead column j = i+1: S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)), k = j+t
+struct CItemColUpd { // look-ahead column j = i+1: S(k,j) = RNE(S(k,j) - S(j,i) B_i(k)), k = j+k0+t
     MpArr S, B;
     int N, L, i;
     const int* err;
+    int k0 = 0; // 0: from the diagonal; 1: the off-diagonal part only
     HK_DEV void operator()(long long t, uint32_t* ws) const {
         if (*(volatile const int*)err >= 0) return;
-        const int j = i + 1, k = j + int(t);
+        const int j = i + 1, k = j + k0 + int(t);
         const long long ec = tri_idx(k, j, N), ex = tri_idx(j, i, N);
         uint32_t* c = S.limbs(ec, L);
         cta_meta_store(S.m + ec, cta_fms(c, S.m[ec], S.limbs(ex, L), S.m[ex], B.limbs(k, L), B.m[k], c, L,

@@ -12,14 +12,16 @@
 __device__ long long g_tr[4096];
 __device__ int g_tag[4096];
 __device__ int g_n;
+__shared__ int s_n; // event counter in shared memory: a trace point costs a few cycles
 #define HK_TRACE(tag)                                                                                         \
     do {                                                                                                      \
         if (threadIdx.x == 0) {                                                                               \
-            const int k_ = g_n++;                                                                             \
+            const int k_ = s_n++;                                                                             \
             if (k_ < 4096) {                                                                                  \
                 g_tr[k_] = clock64();                                                                         \
                 g_tag[k_] = (tag);                                                                            \
             }                                                                                                 \
+            g_n = s_n;                                                                                        \
         }                                                                                                     \
     } while (0)
 
@@ -29,12 +31,16 @@ using namespace hk;
 
 __global__ void k_recip(const uint32_t* d, Meta dm, uint32_t* out, int L, int ws_words) {
     extern __shared__ __align__(16) uint32_t sm[];
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
     const Meta r = cta_recip(d, dm, out, L, sm);
     if (threadIdx.x == 0) HK_TRACE(9 + 0 * r.exp);
 }
 
 __global__ void k_mul(const uint32_t* x, const uint32_t* y, uint32_t* out, int L) {
     extern __shared__ __align__(16) uint32_t sm[];
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
     HK_TRACE(7);
     const Meta r = cta_mulr(x, Meta{0, 1}, y, Meta{0, 1}, out, L, ctaws_carve(sm, L));
     HK_TRACE(8 + 0 * r.exp);
