@@ -319,6 +319,14 @@ bool use_tc(const hk_ctx* c) {
     if (const char* e = getenv("HK_TC")) return e[0] == '1';
     return L >= 128;
 }
+// Dev-only what-if timing (tools/gpu_whatif.sh): HK_DEV_SKIP="recip,round,..."
+// drops those launches from the captured LDLT graph (results are then wrong;
+// no test or bench sets it) to see which stream bounds the step time.
+bool dev_skip(const char* what) {
+    static const char* e = getenv("HK_DEV_SKIP");
+    return e && strstr(e, what);
+}
+
 bool use_tc_inv(const hk_ctx* c) {
     if (!use_tc(c)) return false;
     if (getenv("HK_TC")) return true;
@@ -374,14 +382,16 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
                    hk::trailing2_items(N, jfirst), hk::opws2_words(L), st);
         return;
     }
-    tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
-                b_buf(c, i), unsigned(ncols), st);
+    if (!dev_skip("prod"))
+        tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
+                    b_buf(c, i), unsigned(ncols), st);
     if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
     ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
-    launch(c,
-           hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count, c->tc_fb},
-           (long long)ncols * (ncols + 1) / 2, hk::tcround_words(L), st);
-    launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st);
+    if (!dev_skip("round"))
+        launch(c,
+               hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count, c->tc_fb},
+               (long long)ncols * (ncols + 1) / 2, hk::tcround_words(L), st);
+    if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st);
 }
 
 // L^-1 step i on the tensor cores (same product kernel, mode 1).
@@ -440,7 +450,8 @@ void enqueue_ldlt_steps(hk_ctx* c) {
         enqueue_bulk(c, i, i + 2, bulk);
         ck(cudaEventRecord(evU[i], bulk), "evU");
         if (i >= 1) {
-            launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i - 1), N, L, i - 1}, N - i, 64, bulk);
+            if (!dev_skip("storel"))
+                launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i - 1), N, L, i - 1}, N - i, 64, bulk);
             ck(cudaEventRecord(evR[i - 1], bulk), "evR");
         }
         if (i + 1 < N) {
@@ -449,14 +460,18 @@ void enqueue_ldlt_steps(hk_ctx* c) {
             if (i > 0) ck(cudaStreamWaitEvent(la, evU[i - 1], 0), "wait U");
             ck(cudaEventRecord(evD[i + 1], la), "evD");
             ck(cudaStreamWaitEvent(la2, evD[i + 1], 0), "wait D");
-            launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 1}, N - i - 2, wc, la2);
+            if (!dev_skip("coloff"))
+                launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 1}, N - i - 2, wc, la2);
             ck(cudaEventRecord(evO[i + 1], la2), "evO");
-            launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 0}, 1, wc, la);
-            launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la);
+            if (!dev_skip("coldiag"))
+                launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 0}, 1, wc, la);
+            if (!dev_skip("recip"))
+                launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la);
             if (i >= 2) ck(cudaStreamWaitEvent(la, evR[i - 2], 0), "wait R");
             ck(cudaStreamWaitEvent(la, evO[i + 1], 0), "wait O");
-            launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err}, N - i - 2,
-                       wc, la);
+            if (!dev_skip("mulb"))
+                launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err},
+                           N - i - 2, wc, la);
             ck(cudaEventRecord(evP[i + 1], la), "evP");
         }
     }
