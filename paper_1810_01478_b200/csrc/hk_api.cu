@@ -335,9 +335,14 @@ bool use_tc_inv(const hk_ctx* c) {
 
 // A operand preformat + the tcgen05 product kernel (one CTA per SM: it owns all
 // 512 TMEM columns).  `rows` is the row-operand source (ItemTcPrep).
-void tc_products(hk_ctx* c, const hk::TcBulkArgs& a, hk::MpArr rows, unsigned gx, cudaStream_t st) {
+void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaStream_t st) {
     const int N = c->n, L = c->L;
-    const size_t smem = std::max(hk::tc_smem_bytes(L), size_t(120 * 1024));
+    // small p: one TMEM accumulator and two CTAs per SM (one CTA's prologue and
+    // epilogue overlap the other's MMAs); large p: two accumulators, one CTA per SM
+    // (the epilogue of chunk c overlaps the MMAs of chunk c + 1).
+    a.nacc = hk::tc_smem_bytes(L) <= 110 * 1024 ? 1 : 2;
+    if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
+    const size_t smem = a.nacc == 1 ? hk::tc_smem_bytes(L) : std::max(hk::tc_smem_bytes(L), size_t(120 * 1024));
     static bool configured = false;
     if (!configured) {
         ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");

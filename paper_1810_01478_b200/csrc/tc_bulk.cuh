@@ -101,6 +101,7 @@ struct TcBulkArgs {
     uint32_t* P;                 // scratch: item -> tc_scratch_limbs(L) limbs
     int N, L, i, jfirst, mode, m, b;
     const int* err;
+    int nacc = 2;
 };
 
 #if !defined(HK_WARP_EMU)
@@ -146,7 +147,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         *reinterpret_cast<uint4*>(sE + 16 * (size_t)c) = v;
     }
     tc::fence_async_smem(); // generic-proxy writes of sE -> visible to the tensor core
-    if (warp == 0) tc::tmem_alloc(&taddr_s, 2 * kTcN);
+    const int nacc = a.nacc; // TMEM accumulators (1: two CTAs per SM overlap instead)
+    if (warp == 0) tc::tmem_alloc(&taddr_s, uint32_t(nacc * kTcN));
     if (tid == 0) {
         for (int s = 0; s < kTcStages; ++s) {
             tc::mbar_init(&full[s], 1);
@@ -191,8 +193,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
             while (qt < Q && qt < kTcStages - 1) issue_tma();
             int q = 0;
             for (int c = 0; c < nch; ++c) {
-                const int ab = c & 1;
-                if (c >= 2) tc::mbar_wait(&accE[ab], uint32_t((c - 2) >> 1) & 1u);
+                const int ab = c % nacc;
+                if (c >= nacc) tc::mbar_wait(&accE[ab], uint32_t((c - nacc) / nacc) & 1u);
                 tc::fence_after();
                 const int tc0 = -31 + kTcN * c;
                 const int u_hi = tc0 < 0 ? nb : nb - tc0;
@@ -230,8 +232,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
         uint64_t carry = 0;
         for (int c = 0; c < nch; ++c) {
-            const int ab = c & 1;
-            tc::mbar_wait(&accF[ab], uint32_t(c >> 1) & 1u);
+            const int ab = c % nacc;
+            tc::mbar_wait(&accF[ab], uint32_t(c / nacc) & 1u);
             tc::fence_after();
             for (int c32 = 0; c32 < kTcN; c32 += 32) {
                 uint32_t v[32];
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (warp == 0) tc::tmem_dealloc(tmem, 2 * kTcN);
+    if (warp == 0) tc::tmem_dealloc(tmem, uint32_t(nacc * kTcN));
 }
 #endif
 
