@@ -315,7 +315,7 @@ MpArr b_buf(hk_ctx* c, int i) {
 // from p >= 12288 bits (measured: C2 5.1 ms IMAD vs 7.4 ms TC, C3 459 vs 107 ms).
 bool use_tc(const hk_ctx* c) {
     const int L = c->L;
-    if (L % 4 != 0 || hk::tc_smem_bytes(L) > 220 * 1024) return false;
+    if (L % 4 != 0 || hk::tc_smem_bytes(L, hk::tc_ewin(L)) > 220 * 1024) return false;
     if (const char* e = getenv("HK_TC")) return e[0] == '1';
     return L >= 128;
 }
@@ -340,9 +340,12 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     // small p: one TMEM accumulator and two CTAs per SM (one CTA's prologue and
     // epilogue overlap the other's MMAs); large p: two accumulators, one CTA per SM
     // (the epilogue of chunk c overlaps the MMAs of chunk c + 1).
-    a.nacc = hk::tc_smem_bytes(L) <= 110 * 1024 ? 1 : 2;
+    a.ewin = hk::tc_ewin(L) ? 1 : 0;
+    if (const char* e = getenv("HK_TC_EWIN")) a.ewin = e[0] == '1' ? 1 : 0;
+    const size_t need = hk::tc_smem_bytes(L, a.ewin != 0);
+    a.nacc = need <= 110 * 1024 ? 1 : 2;
     if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
-    const size_t smem = a.nacc == 1 ? hk::tc_smem_bytes(L) : std::max(hk::tc_smem_bytes(L), size_t(120 * 1024));
+    const size_t smem = a.nacc == 1 ? need : std::max(need, size_t(120 * 1024));
     static bool configured = false;
     if (!configured) {
         ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");

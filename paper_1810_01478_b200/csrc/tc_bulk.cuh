@@ -41,9 +41,15 @@ HK_HD int tc_nks(int L) { return (tc_nb(L) + kTcK - 1) / kTcK; }
 HK_HD int tc_nblk(int L) { return (tc_nks(L) + kTcKB - 1) / kTcKB; }
 HK_HD int tc_ntiles(int N) { return (N + kTcRows - 1) / kTcRows; }
 HK_HD int tc_nchunks(int L) { return (tc_nb(L) + 32 + kTcN - 1) / kTcN; }
-HK_HD size_t tc_smem_bytes(int L) {
-    return (size_t)kTcStages * kTcBlk + 16 * (size_t)tc_ncell(L) + 4 * (size_t)tc_sx_words(L) + 64;
+constexpr int kTcEWin = 384;    // cells of x one A block's 4 K-steps read (windowed expansion)
+// Full expansion: all nb + 352 cells built once per CTA.  Windowed (large p,
+// where the full expansion would not fit): warps 1-3 build each block's
+// 384-cell window into a ring next to the A ring, paced by the same barriers.
+HK_HD size_t tc_smem_bytes(int L, bool ewin = false) {
+    const size_t e = ewin ? (size_t)kTcStages * kTcEWin * 16 : 16 * (size_t)tc_ncell(L);
+    return (size_t)kTcStages * kTcBlk + e + 4 * (size_t)tc_sx_words(L) + 64;
 }
+HK_HD bool tc_ewin(int L) { return tc_smem_bytes(L, false) > 200 * 1024; }
 HK_HD int tc_scratch_limbs(int L) { return L + kTcGuard; }  // limbs [L-8, 2L)
 // preformatted A operand of one step: [row tile][A block][4 K-steps x 128 rows x 32 B]
 HK_HD size_t tc_apre_bytes(int N, int L) { return (size_t)tc_ntiles(N) * tc_nblk(L) * kTcBlk; }
@@ -102,6 +108,7 @@ struct TcBulkArgs {
     int N, L, i, jfirst, mode, m, b;
     const int* err;
     int nacc = 2;
+    int ewin = 0; // windowed x expansion
 };
 
 #if !defined(HK_WARP_EMU)
@@ -115,7 +122,7 @@ struct TcBulkArgs {
 // into limbs) while chunk c + 1 accumulates into the other one (accF / accE).
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    __shared__ uint64_t full[kTcStages], empty[kTcStages], accF[2], accE[2];
+    __shared__ uint64_t full[kTcStages], empty[kTcStages], efull[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
     if (a.mode == 0 && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
     const int N = a.N, L = a.L, nb = tc_nb(L);
@@ -123,18 +130,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     const int tile = j / kTcRows + int(blockIdx.y);
     if (j >= N || tile * kTcRows >= N) return;
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
+    const bool ewin = a.ewin != 0;
     uint8_t* sA = tsm;                                     // kTcStages x 16 KB A ring
-    uint8_t* sE = tsm + (size_t)kTcStages * kTcBlk;        // expanded x cells
-    uint32_t* sX = reinterpret_cast<uint32_t*>(sE + 16 * (size_t)tc_ncell(L)); // x bytes, 32-byte zero pad
+    uint8_t* sE = tsm + (size_t)kTcStages * kTcBlk;        // expanded x cells (full, or the window ring)
+    uint32_t* sX = reinterpret_cast<uint32_t*>(sE + (ewin ? (size_t)kTcStages * kTcEWin * 16
+                                                          : 16 * (size_t)tc_ncell(L))); // x bytes, 32 B zero pad
     const int pmin = -31;
-
-    // x bytes into sX (word 8 = byte 32 holds X[0]); cells p = pmin + c: X[p .. p+15]
-    const uint32_t* xl = a.mode == 0 ? a.S.limbs(tri_idx(j, a.i, N), L)
-                                     : a.X.limbs((long long)a.i * a.m + blockIdx.x, L);
-    for (int w = tid; w < tc_sx_words(L); w += kTcThreads) sX[w] = (w >= 8 && w < 8 + L) ? xl[w - 8] : 0u;
-    __syncthreads();
-    for (int c = tid; c < tc_ncell(L); c += kTcThreads) {
-        const int off = 32 + pmin + c; // byte offset in sX (>= 1)
+    // cell p (byte position in X, p >= pmin) -> X[p .. p+15] from sX (zero outside [0, nb))
+    auto cell = [&](int p) {
+        const int off = 32 + p; // byte offset in sX (>= 1)
         const int w0 = off >> 2, sh = (off & 3) * 8;
         uint32_t W[5];
 #pragma unroll
@@ -144,15 +148,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         v.y = __funnelshift_r(W[1], W[2], sh);
         v.z = __funnelshift_r(W[2], W[3], sh);
         v.w = __funnelshift_r(W[3], W[4], sh);
-        *reinterpret_cast<uint4*>(sE + 16 * (size_t)c) = v;
+        return v;
+    };
+
+    // x bytes into sX (word 8 = byte 32 holds X[0]); cells p = pmin + c: X[p .. p+15]
+    const uint32_t* xl = a.mode == 0 ? a.S.limbs(tri_idx(j, a.i, N), L)
+                                     : a.X.limbs((long long)a.i * a.m + blockIdx.x, L);
+    for (int w = tid; w < tc_sx_words(L); w += kTcThreads) sX[w] = (w >= 8 && w < 8 + L) ? xl[w - 8] : 0u;
+    __syncthreads();
+    if (!ewin) {
+        for (int c = tid; c < tc_ncell(L); c += kTcThreads)
+            *reinterpret_cast<uint4*>(sE + 16 * (size_t)c) = cell(pmin + c);
+        tc::fence_async_smem(); // generic-proxy writes of sE -> visible to the tensor core
     }
-    tc::fence_async_smem(); // generic-proxy writes of sE -> visible to the tensor core
     const int nacc = a.nacc; // TMEM accumulators (1: two CTAs per SM overlap instead)
     if (warp == 0) tc::tmem_alloc(&taddr_s, uint32_t(nacc * kTcN));
     if (tid == 0) {
         for (int s = 0; s < kTcStages; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
+            tc::mbar_init(&efull[s], 3); // one arrival per builder warp (1-3)
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&accF[b], 1);
@@ -165,16 +180,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     tc::fence_after();
     const uint32_t tmem = taddr_s;
     const int nch = tc_nchunks(L);
+    auto nblk_of = [&](int c) {
+        const int tc0 = -31 + kTcN * c;
+        const int u_hi = tc0 < 0 ? nb : nb - tc0; // u' < u_hi contribute
+        return (((u_hi + kTcK - 1) / kTcK) + kTcKB - 1) / kTcKB;
+    };
 
     if (warp == 0) {
         if (ln == 0) {
             const uint32_t idesc = tc::idesc_u8(kTcRows, kTcN, false, true);
             const uint8_t* Abase = a.A + (size_t)tile * tc_nblk(L) * kTcBlk;
-            auto nblk_of = [&](int c) {
-                const int tc0 = -31 + kTcN * c;
-                const int u_hi = tc0 < 0 ? nb : nb - tc0; // u' < u_hi contribute
-                return (((u_hi + kTcK - 1) / kTcK) + kTcKB - 1) / kTcKB;
-            };
             int Q = 0;
             for (int c = 0; c < nch; ++c) Q += nblk_of(c);
             // producer cursor: global block index qt -> (chunk pc, block pb)
@@ -203,13 +218,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                 for (int b = 0; b < nblk; ++b, ++q) {
                     const int s = q % kTcStages;
                     tc::mbar_wait(&full[s], uint32_t(q / kTcStages) & 1u);
+                    if (ewin) tc::mbar_wait(&efull[s], uint32_t(q / kTcStages) & 1u);
                     tc::fence_after();
 #pragma unroll
                     for (int sub = 0; sub < kTcKB; ++sub) {
                         const int ks = b * kTcKB + sub;
                         if (ks < ksteps) {
                             const uint64_t ad = tc::sdesc(sA + (size_t)s * kTcBlk + sub * 4096, 128, 256);
-                            const uint64_t bd = tc::sdesc(sE + 16 * (size_t)(tc0 + ks * kTcK - pmin), 128, 256);
+                            const uint64_t bd =
+                                ewin ? tc::sdesc(sE + (size_t)s * kTcEWin * 16 + 16 * (size_t)(sub * kTcK), 128, 256)
+                                     : tc::sdesc(sE + 16 * (size_t)(tc0 + ks * kTcK - pmin), 128, 256);
                             tc::mma_i8(tmem + uint32_t(ab * kTcN), ad, bd, idesc, ks > 0 ? 1u : 0u);
                         }
                     }
@@ -220,7 +238,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (warp < 4) {
+        if (ewin) { // warps 1-3: the x window of every block, in issue order
+            const int bt = tid - 32;
+            int q = 0;
+            for (int c = 0; c < nch; ++c) {
+                const int tc0 = -31 + kTcN * c, nblk = nblk_of(c);
+                for (int b = 0; b < nblk; ++b, ++q) {
+                    const int s = q % kTcStages;
+                    if (q >= kTcStages) tc::mbar_wait(&empty[s], uint32_t((q / kTcStages) - 1) & 1u);
+                    uint8_t* dst = sE + (size_t)s * kTcEWin * 16;
+                    const int p0 = tc0 + b * kTcKB * kTcK;
+                    for (int cc = bt; cc < kTcEWin; cc += 96) *reinterpret_cast<uint4*>(dst + 16 * cc) = cell(p0 + cc);
+                    tc::fence_async_smem();
+                    __syncwarp();
+                    if (ln == 0) tc::mbar_arrive(&efull[s]);
+                }
+            }
+        }
+    } else {
         const int r = 32 * (warp & 3) + ln; // this thread's row / TMEM lane
         const int k = tile * kTcRows + r;
         const bool row_ok = k >= j && k < N;

@@ -1,0 +1,214 @@
+"""Host-side drivers mirroring the reference's `hankel/pipeline.hpp` on top of the
+device path (`api.Context`): `compute`, `auto_precision`, `scan` and the scan-CSV
+writer/reader (pipeline.cpp:26-245).
+
+Precision: the reference works in fixed point with K fractional bits (2K inside
+the LDLT, pipeline.hpp:19).  Here every value is a p-bit float; K maps to the
+smallest p that holds every moment exactly AND keeps 2K fraction bits on the
+largest one:
+
+    p(K) = 32 L,  L = ceil((bits(mu_{2N-2}) + 2K) / 128) * 4
+
+(L a multiple of 4 so the tensor-core path applies).  Relative precision makes
+every smaller entry at least as precise as the reference's fixed point.  The
+search, its defaults and its agreement test are the reference's
+(`auto_precision`, pipeline.cpp:74-94; AutoPrecisionOptions, pipeline.hpp:52-57).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+from . import api
+
+
+@dataclass
+class ComputeOptions:
+    """pipeline.hpp:16-23 (`workers` = GPUs; `bits` = the reference's K)."""
+
+    n: int = 1
+    beta: tuple = (1, 2)
+    bits: int = 1024
+    k: int = 8
+    workers: int = 1
+    device: int = 0
+
+
+@dataclass
+class AutoPrecisionOptions:
+    """pipeline.hpp:52-57."""
+
+    start_bits: int = 0  # 0 -> 1024 * ceil(n / 500)
+    step_bits: int = 1024
+    max_bits: int = 16384
+    agree_tol: float = 1e-15
+
+
+@dataclass
+class RunRecord:
+    """pipeline.hpp:28-48, plus p (the float precision used) and the ~32-digit lambda."""
+
+    n: int = 0
+    beta: tuple = (1, 2)
+    bits: int = 0
+    k: int = 0
+    workers: int = 0
+    lambda_: list = field(default_factory=list)  # binary64, ascending (up to 3)
+    trunc_err: list = field(default_factory=list)
+    required_bits: int = 0
+    wall_s: float = 0.0
+    ldlt_s: float = 0.0
+    transpose_s: float = 0.0
+    invL_s: float = 0.0
+    invL_arith_s: float = 0.0
+    invL_comm_s: float = 0.0
+    invH_s: float = 0.0
+    eigen_s: float = 0.0
+    p: int = 0
+    lambda_hi: list = field(default_factory=list)
+    lambda_lo: list = field(default_factory=list)
+
+    def lambda1(self) -> float:
+        return self.lambda_[0]
+
+
+def moment_bits(beta: tuple, n: int) -> int:
+    """Bit length of the largest moment mu_{2n-2} (exact, from the moment generator)."""
+    num, den = beta
+    j = 2 * n - 2
+    est = (math.lgamma((j + 1) * den / num) + math.log(den / num)) / math.log(2)
+    L = int(est // 32) + 4
+    mu, exact = api.build_hankel(beta, n, L)
+    if not exact:
+        raise api.PrecisionError("moment_bits: estimate too small")
+    return int(mu.exps[-1])
+
+
+def precision_bits(beta: tuple, n: int, K: int) -> int:
+    """p(K) (module docstring)."""
+    return 128 * math.ceil((moment_bits(beta, n) + 2 * K) / 128)
+
+
+def compute(opts: ComputeOptions) -> RunRecord:
+    """hankel::compute (pipeline.cpp:26-72) at the p equivalent to K = opts.bits."""
+    if opts.n < 1:
+        raise ValueError("compute: need N >= 1")
+    if opts.bits < 1:
+        raise ValueError("compute: need bits >= 1")
+    if opts.workers < 1:
+        raise ValueError("compute: need workers >= 1")
+    if opts.k < 1:
+        raise ValueError("compute: need k >= 1")
+    p = precision_bits(opts.beta, opts.n, opts.bits)
+    L = p // 32
+    mu, exact = api.build_hankel(opts.beta, opts.n, L)
+    if not exact:
+        raise api.PrecisionError("compute: moments not exact at p bits")
+    with api.Context(L, device=opts.device) as ctx:
+        r = ctx.compute(mu, opts.k)
+    return RunRecord(n=opts.n, beta=tuple(opts.beta), bits=opts.bits, k=r.k, workers=opts.workers,
+                     lambda_=[h + l for h, l in zip(r.lambda_hi, r.lambda_lo)], trunc_err=list(r.trunc_err),
+                     wall_s=r.wall_s, ldlt_s=r.ldlt_s, invL_s=r.invL_s, invL_arith_s=r.invL_s, invH_s=r.invH_s,
+                     eigen_s=r.eigen_s, p=p, lambda_hi=list(r.lambda_hi), lambda_lo=list(r.lambda_lo))
+
+
+def auto_precision(base: ComputeOptions, opts: AutoPrecisionOptions | None = None) -> tuple[int, RunRecord]:
+    """Smallest K (step multiples from the N heuristic) whose run agrees with the
+    K + step run on lambda_1 within agree_tol (pipeline.cpp:74-94)."""
+    opts = opts or AutoPrecisionOptions()
+    step = opts.step_bits
+    k0 = opts.start_bits if opts.start_bits > 0 else step * ((base.n + 499) // 500)
+    run = ComputeOptions(**{**base.__dict__, "bits": k0})
+    prev = compute(run)
+    bits = k0
+    while bits <= opts.max_bits:
+        run.bits = bits + step
+        nxt = compute(run)
+        if abs(prev.lambda1() - nxt.lambda1()) <= opts.agree_tol:
+            prev.required_bits = bits
+            return bits, prev
+        prev = nxt
+        bits += step
+    raise api.PrecisionError(f"auto_precision: no agreement up to {opts.max_bits} bits (step {step})")
+
+
+def scan(n_list, base: ComputeOptions, auto_bits: bool = False,
+         auto_opts: AutoPrecisionOptions | None = None) -> list[RunRecord]:
+    """pipeline.cpp:96-122: one record per N; failures become NaN rows."""
+    out = []
+    for n in n_list:
+        run = ComputeOptions(**{**base.__dict__, "n": n})
+        try:
+            out.append(auto_precision(run, auto_opts)[1] if auto_bits else compute(run))
+        except Exception:
+            nan = float("nan")
+            out.append(RunRecord(n=n, beta=tuple(run.beta), bits=run.bits, k=run.k, workers=run.workers,
+                                 lambda_=[nan] * 3, trunc_err=[nan] * 3))
+    return out
+
+
+CSV_HEADER = ("N,beta,bits,k,workers,lambda1,trunc1,lambda2,trunc2,lambda3,trunc3,"
+              "required_bits,wall_s,ldlt_s,transpose_s,invL_s,invL_arith_s,invL_comm_s,invH_s,eigen_s")
+
+
+def _fmt(v: float) -> str:  # std::ostream with precision(17)
+    return "nan" if v != v else f"{v:.17g}"
+
+
+def to_csv_row(r: RunRecord) -> str:
+    """pipeline.cpp:150-160 (17 significant digits)."""
+    cols = [str(r.n), f"{r.beta[0]}/{r.beta[1]}", str(r.bits), str(r.k), str(r.workers)]
+    for i in range(3):
+        cols.append(_fmt(r.lambda_[i] if i < len(r.lambda_) else float("nan")))
+        cols.append(_fmt(r.trunc_err[i] if i < len(r.trunc_err) else float("nan")))
+    cols.append(str(r.required_bits))
+    cols += [_fmt(x) for x in (r.wall_s, r.ldlt_s, r.transpose_s, r.invL_s, r.invL_arith_s, r.invL_comm_s,
+                               r.invH_s, r.eigen_s)]
+    return ",".join(cols)
+
+
+def write_scan_csv(f, records) -> None:
+    f.write(CSV_HEADER + "\n")
+    for r in records:
+        f.write(to_csv_row(r) + "\n")
+
+
+def read_scan_csv(f) -> list[tuple[float, float]]:
+    """(N, lambda1) points, NaN rows skipped (pipeline.cpp:167-207; errors as schema_error)."""
+    lines = f.read().splitlines()
+    if not lines:
+        raise ValueError("scan CSV: empty input")
+    head = lines[0].replace("\r", "").split(",")
+    if "N" not in head or "lambda1" not in head:
+        raise ValueError("scan CSV: header must contain N and lambda1 columns")
+    ni, li = head.index("N"), head.index("lambda1")
+    pts = []
+    for no, line in enumerate(lines[1:], start=2):
+        if not line:
+            continue
+        fields = line.replace("\r", "").split(",")
+        if len(fields) <= max(ni, li):
+            raise ValueError(f"scan CSV: short row at line {no}")
+        try:
+            n, lam = float(fields[ni]), float(fields[li])
+        except ValueError:
+            raise ValueError(f"scan CSV: unparseable number at line {no}") from None
+        if lam == lam:  # NaN rows are failed scan entries
+            pts.append((n, lam))
+    return pts
+
+
+def to_json(r: RunRecord) -> str:
+    """pipeline.cpp:213-231 (plus p and the extended-precision lambda)."""
+    import json
+
+    j = {"N": r.n, "beta": f"{r.beta[0]}/{r.beta[1]}", "bits": r.bits, "k": r.k, "workers": r.workers,
+         "lambda": r.lambda_, "trunc_err": r.trunc_err}
+    if r.required_bits > 0:
+        j["required_bits"] = r.required_bits
+    j["timing"] = {"wall_s": r.wall_s, "ldlt_s": r.ldlt_s, "transpose_s": r.transpose_s, "invL_s": r.invL_s,
+                   "invL_arith_s": r.invL_arith_s, "invL_comm_s": r.invL_comm_s, "invH_s": r.invH_s,
+                   "eigen_s": r.eigen_s}
+    j["p_bits"] = r.p
+    j["lambda_hi_lo"] = [[h, lo] for h, lo in zip(r.lambda_hi, r.lambda_lo)]
+    return json.dumps(j, indent=2)
