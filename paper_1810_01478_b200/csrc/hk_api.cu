@@ -340,10 +340,13 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     // small p: one TMEM accumulator and two CTAs per SM (one CTA's prologue and
     // epilogue overlap the other's MMAs); large p: two accumulators, one CTA per SM
     // (the epilogue of chunk c overlaps the MMAs of chunk c + 1).
-    a.ewin = hk::tc_ewin(L) ? 1 : 0;
+    // LDLT (many CTAs per step): windowed x expansion (93-103 KB of shared memory)
+    // and one TMEM accumulator, two CTAs per SM.  L^-1 (b <= m column CTAs per
+    // step): full expansion when it fits and two accumulators, one CTA per SM.
+    a.ewin = (a.mode == 0 || hk::tc_ewin(L)) ? 1 : 0;
     if (const char* e = getenv("HK_TC_EWIN")) a.ewin = e[0] == '1' ? 1 : 0;
     const size_t need = hk::tc_smem_bytes(L, a.ewin != 0);
-    a.nacc = need <= 110 * 1024 ? 1 : 2;
+    a.nacc = (a.mode == 0 && need <= 110 * 1024) ? 1 : 2;
     if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
     const size_t smem = a.nacc == 1 ? need : std::max(need, size_t(120 * 1024));
     static bool configured = false;
