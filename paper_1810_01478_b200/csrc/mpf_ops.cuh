@@ -491,6 +491,35 @@ HK_DEV FxRecipWs fxrecipws_carve(uint32_t* b, int L) {
     return w;
 }
 
+// Register product for the small Newton levels: lane s holds A[s] / B[s] (a, b
+// <= 32 limbs, a + b <= 64); returns C[lane] in lo and C[32 + lane] in hi.
+HK_DEV void reg_mul(uint32_t A, int a, uint32_t B, int b, uint32_t& lo, uint32_t& hi) {
+    const int ln = lane();
+    uint32_t c0 = 0, c1 = 0, c2 = 0, d0 = 0, d1 = 0, d2 = 0;
+    for (int s = 0; s < a; ++s) {
+        const uint32_t as = shfl(A, s);
+        const int i0 = ln - s, i1 = ln + 32 - s;
+        const uint32_t b0 = shfl(B, i0 & 31), b1 = shfl(B, i1 & 31);
+        if (i0 >= 0 && i0 < b) mac96(c0, c1, c2, as, b0);
+        if (i1 >= 0 && i1 < b) mac96(d0, d1, d2, as, b1);
+    }
+    CarryState cs;
+    lo = carry_group(cs, c0, c1, c2);
+    hi = carry_group(cs, d0, d1, d2);
+}
+// limb t (0 <= t < 64) of a (lo, hi) register product, for every lane's own t
+HK_DEV uint32_t reg_limb(uint32_t lo, uint32_t hi, int t) {
+    const uint32_t vl = shfl(lo, t & 31), vh = shfl(hi, t & 31);
+    return t < 32 ? vl : vh;
+}
+
+// The small Newton levels (nk <= kRegLevel limbs): warp 0 alone with one limb per
+// lane in registers — no shared-memory staging, no block barriers.
+#ifndef HK_REG_LEVEL
+#define HK_REG_LEVEL 30
+#endif
+constexpr int kRegLevel = HK_REG_LEVEL;
+
 HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_t* wsb) {
     HK_TRACE(0);
     FxRecipWs w = fxrecipws_carve(wsb, L);
@@ -500,26 +529,64 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
     const double zd = 1.0 / ldexp((double)mh, -64);
     int ex;
     const uint64_t mant = (uint64_t)ldexp(frexp(zd, &ex), 53); // zd = mant 2^(ex-53), ex in {1, 2}
-    if (cta_tid() == 0) {
-        const int sh = ex + 11; // Z = mant << (64 + ex - 53), a 66-bit value
-        const uint64_t lo = mant << sh;
-        w.rw.Z[0] = uint32_t(lo);
-        w.rw.Z[1] = uint32_t(lo >> 32);
-        w.rw.Z[2] = uint32_t(mant >> (64 - sh));
-        w.rw.Z[3] = 0u;
-    }
     if (cta_tid() == 1) w.rw.one[0] = 1u;
-    cta_sync();
-    int nf = 2;
     int sched[32];
     int ns = 0;
     for (int n = L + 2;; n = (n + 1) / 2 + 1) {
         sched[ns++] = n;
         if (n <= 3) break;
     }
+    // levels handled in registers by warp 0 (block-uniform bookkeeping)
+    int nreg = 0;
+    while (nreg < ns && sched[ns - 1 - nreg] <= kRegLevel) ++nreg;
+    if (w0) {
+        const int ln = lane();
+        // top min(L, 32) limbs of m, lane l -> Md[mbase + l]
+        const int mbase = L > 32 ? L - 32 : 0;
+        const uint32_t Mt = ln < L ? Md[mbase + ln] : 0u;
+        uint32_t Zr; // seed: Z = mant << (64 + ex - 53), a 66-bit value with 2 fraction limbs
+        {
+            const int sh = ex + 11;
+            const uint64_t lo = mant << sh;
+            Zr = ln == 0 ? uint32_t(lo) : ln == 1 ? uint32_t(lo >> 32) : ln == 2 ? uint32_t(mant >> (64 - sh)) : 0u;
+        }
+        int nfr = 2;
+        for (int r = 0; r < nreg; ++r) {
+            const int nk = sched[ns - 1 - r];
+            const int mn = nk >= L ? L : nk;
+            const uint32_t mv = shfl(Mt, (L - mn - mbase + ln) & 31);
+            const uint32_t mtop = ln < mn ? mv : 0u;
+            uint32_t tlo, thi;
+            reg_mul(Zr, nfr + 1, mtop, mn, tlo, thi); // T = m_top * z
+            const int FT = mn + nfr;
+            const bool neg = reg_limb(tlo, thi, FT) != 0u; // T >= 1  ->  e <= 0
+            const uint32_t ev = reg_limb(tlo, thi, FT - nk + ln);
+            const uint32_t E = ln < nk ? (neg ? ev : ~ev) : 0u;
+            uint32_t dlo, dhi;
+            reg_mul(Zr, nfr + 1, E, nk, dlo, dhi); // D = z * |e|
+            const int shl = nk - nfr;
+            const uint32_t zs = shfl(Zr, (ln - shl) & 31);
+            const uint32_t zv = (ln >= shl && ln - shl <= nfr) ? zs : 0u;
+            const uint32_t dd = reg_limb(dlo, dhi, nfr + ln);
+            const uint32_t dv = ln <= nk ? dd : 0u;
+            uint32_t r2;
+            if (neg) {
+                r2 = zv - dv;
+                seg_borrow(r2, zv < dv, 0u);
+            } else {
+                r2 = zv + dv;
+                seg_carry(r2, r2 < zv, 0u);
+            }
+            Zr = ln <= nk ? r2 : 0u;
+            nfr = nk;
+        }
+        if (ln <= nfr + 1) w.rw.Z[ln] = ln <= nfr ? Zr : 0u;
+    }
+    cta_sync();
+    int nf = nreg ? sched[ns - nreg] : 2;
     uint32_t* Z = w.rw.Z;
     uint32_t* Zn = w.Z2;
-    for (int si = ns - 1; si >= 0; --si) {
+    for (int si = ns - 1 - nreg; si >= 0; --si) {
         const int nk = sched[si];
         const int mn = nk >= L ? L : nk;
         // T = m_top * z

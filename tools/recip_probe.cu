@@ -13,6 +13,9 @@ __device__ long long g_tr[4096];
 __device__ int g_tag[4096];
 __device__ int g_n;
 __shared__ int s_n; // event counter in shared memory: a trace point costs a few cycles
+#ifdef HK_PROBE_NOTRACE
+#define HK_TRACE(tag)
+#else
 #define HK_TRACE(tag)                                                                                         \
     do {                                                                                                      \
         if (threadIdx.x == 0) {                                                                               \
@@ -24,6 +27,7 @@ __shared__ int s_n; // event counter in shared memory: a trace point costs a few
             g_n = s_n;                                                                                        \
         }                                                                                                     \
     } while (0)
+#endif
 
 #include "../paper_1810_01478_b200/csrc/mpf_ops.cuh"
 
@@ -85,6 +89,25 @@ int main(int argc, char** argv) {
         k_mul<<<1, 256, wc * 4>>>(d, y, o, L);
         cudaDeviceSynchronize();
         if (rep == 2) dump("cta_mulr");
+    }
+    // untraced timing: 200 back-to-back single-CTA launches (CUDA events)
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int pass = 0; pass < 2; ++pass) {
+        cudaEventRecord(e0);
+        for (int r = 0; r < 200; ++r) k_recip<<<1, 256, wr * 4>>>(d, Meta{0, 1}, o, L, wr);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (pass == 1) printf("recip_us %.2f\n", ms * 1e3 / 200);
+        cudaEventRecord(e0);
+        for (int r = 0; r < 200; ++r) k_mul<<<1, 256, wc * 4>>>(d, y, o, L);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (pass == 1) printf("mul_us %.2f\n", ms * 1e3 / 200);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
