@@ -108,6 +108,7 @@ struct hk_ctx {
     uint32_t* tc_P = nullptr;
     size_t tc_P_words = 0;
     uint8_t* tc_A = nullptr;      // preformatted A operand of the current step
+    uint64_t* tc_gcarry = nullptr; // L^-1 chunk-group carries
     cudaEvent_t prof_mid = nullptr; // hk_profile_ldlt: recorded between TC products and rounding
     int* tc_fb_count = nullptr;   // uncertified items of the current step
     long long* tc_fb = nullptr;
@@ -360,7 +361,7 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     ck(cudaGetLastError(), "tc prep launch");
     ++c->launches;
     const int first_row = a.mode == 0 ? a.jfirst : a.i + 1;
-    const dim3 grid(gx, unsigned(hk::tc_ntiles(N) - first_row / hk::kTcRows));
+    const dim3 grid(gx, unsigned(hk::tc_ntiles(N) - first_row / hk::kTcRows), unsigned(a.groups));
     hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
     ck(cudaGetLastError(), "tc bulk launch");
     ++c->launches;
@@ -410,13 +411,23 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
     const int N = c->n, L = c->L, m = c->m;
     const int b = i < m ? i : m;
     if (i + 1 >= N) return;
-    if (b > 0)
-        tc_products(c, hk::TcBulkArgs{c->S.view(), c->X.view(), c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err},
-                    c->S.view(), unsigned(b), st);
+    // narrow step: split each product's output chunks over G CTAs (carries joined in the rounding pass)
+    const int tiles = hk::tc_ntiles(N) - (i + 1) / hk::kTcRows;
+    int G = b > 0 ? (c->sm_count + b * tiles - 1) / (b * tiles) : 1;
+    G = std::min(G, std::min(int(hk::kTcMaxGroups), hk::tc_nchunks(L) / 2));
+    if (G < 1) G = 1;
+    if (b > 0) {
+        hk::TcBulkArgs a{c->S.view(), c->X.view(), c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err};
+        a.groups = G;
+        a.gcarry = c->tc_gcarry;
+        tc_products(c, a, c->S.view(), unsigned(b), st);
+    }
     ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
     const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
-    launch(c, hk::ItemTcRoundInv{c->S.view(), c->X.view(), c->tc_P, N, L, m, i, b, c->tc_fb_count, c->tc_fb},
-           items, hk::tcround_words(L), st);
+    hk::ItemTcRoundInv ri{c->S.view(), c->X.view(), c->tc_P, N, L, m, i, b, c->tc_fb_count, c->tc_fb};
+    ri.G = G;
+    ri.gcarry = c->tc_gcarry;
+    launch(c, ri, items, hk::tcround_words(L), st);
     if (b > 0) launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st);
 }
 
@@ -429,6 +440,8 @@ void ensure_tc_scratch(hk_ctx* c, int m = 0) {
     if (c->tc_fb) cudaFree(c->tc_fb);
     if (c->tc_A) cudaFree(c->tc_A);
     ck(cudaMalloc(&c->tc_A, hk::tc_apre_bytes(c->n, c->L)), "cudaMalloc tc A");
+    if (c->tc_gcarry) cudaFree(c->tc_gcarry);
+    ck(cudaMalloc(&c->tc_gcarry, items * (hk::kTcMaxGroups - 1) * sizeof(uint64_t)), "cudaMalloc tc carries");
     if (!c->tc_fb_count) ck(cudaMalloc(&c->tc_fb_count, sizeof(int)), "cudaMalloc fb count");
     c->tc_P = nullptr;
     c->tc_fb = nullptr;
@@ -583,6 +596,7 @@ void hk_destroy(hk_ctx* c) {
     if (c->tc_fb) cudaFree(c->tc_fb);
     if (c->tc_fb_count) cudaFree(c->tc_fb_count);
     if (c->tc_A) cudaFree(c->tc_A);
+    if (c->tc_gcarry) cudaFree(c->tc_gcarry);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);

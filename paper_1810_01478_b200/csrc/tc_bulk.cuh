@@ -41,6 +41,7 @@ HK_HD int tc_nks(int L) { return (tc_nb(L) + kTcK - 1) / kTcK; }
 HK_HD int tc_nblk(int L) { return (tc_nks(L) + kTcKB - 1) / kTcKB; }
 HK_HD int tc_ntiles(int N) { return (N + kTcRows - 1) / kTcRows; }
 HK_HD int tc_nchunks(int L) { return (tc_nb(L) + 32 + kTcN - 1) / kTcN; }
+constexpr int kTcMaxGroups = 8; // chunk groups per product (L^-1)
 constexpr int kTcEWin = 384;    // cells of x one A block's 4 K-steps read (windowed expansion)
 // Full expansion: all nb + 352 cells built once per CTA.  Windowed (large p,
 // where the full expansion would not fit): warps 1-3 build each block's
@@ -50,6 +51,28 @@ HK_HD size_t tc_smem_bytes(int L, bool ewin = false) {
     return (size_t)kTcStages * kTcBlk + e + 4 * (size_t)tc_sx_words(L) + 64;
 }
 HK_HD bool tc_ewin(int L) { return tc_smem_bytes(L, false) > 200 * 1024; }
+
+// A blocks (4 K-steps each) of output chunk c; chunk c covers product bytes from
+// t' = -31 + 256 c, i.e. scratch limbs [64 c, 64 c + 64).
+HK_HD int tc_chunk_blocks(int L, int c) {
+    const int nb = tc_nb(L), tc0 = -31 + 256 * c;
+    const int u_hi = tc0 < 0 ? nb : nb - tc0; // u' < u_hi contribute
+    return (((u_hi + 31) / 32) + 3) / 4;
+}
+// First chunk of group z when the chunks are split into G groups of about
+// equal MMA work (narrow L^-1 steps run G CTAs per (column, row tile)).
+HK_HD int tc_group_first_chunk(int L, int G, int z) {
+    if (z <= 0) return 0;
+    const int nch = tc_nchunks(L);
+    if (z >= G) return nch;
+    long long Q = 0;
+    for (int c = 0; c < nch; ++c) Q += tc_chunk_blocks(L, c);
+    const long long target = Q * z / G;
+    long long acc = 0;
+    int c = 0;
+    while (c < nch && acc < target) acc += tc_chunk_blocks(L, c++);
+    return c;
+}
 HK_HD int tc_scratch_limbs(int L) { return L + kTcGuard; }  // limbs [L-8, 2L)
 // preformatted A operand of one step: [row tile][A block][4 K-steps x 128 rows x 32 B]
 HK_HD size_t tc_apre_bytes(int N, int L) { return (size_t)tc_ntiles(N) * tc_nblk(L) * kTcBlk; }
@@ -108,7 +131,9 @@ struct TcBulkArgs {
     int N, L, i, jfirst, mode, m, b;
     const int* err;
     int nacc = 2;
-    int ewin = 0; // windowed x expansion
+    int ewin = 0;            // windowed x expansion
+    int groups = 1;          // chunk groups (blockIdx.z): G > 1 only for L^-1 steps
+    uint64_t* gcarry = nullptr; // [item][G - 1]: carry out of each group but the last
 };
 
 #if !defined(HK_WARP_EMU)
@@ -179,21 +204,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = taddr_s;
-    const int nch = tc_nchunks(L);
-    auto nblk_of = [&](int c) {
-        const int tc0 = -31 + kTcN * c;
-        const int u_hi = tc0 < 0 ? nb : nb - tc0; // u' < u_hi contribute
-        return (((u_hi + kTcK - 1) / kTcK) + kTcKB - 1) / kTcKB;
-    };
+    // this CTA's output chunks [c_lo, nch)
+    const int G = a.groups, z = int(blockIdx.z);
+    const int c_lo = tc_group_first_chunk(L, G, z);
+    const int nch = tc_group_first_chunk(L, G, z + 1);
+    auto nblk_of = [&](int c) { return tc_chunk_blocks(L, c); };
 
     if (warp == 0) {
         if (ln == 0) {
             const uint32_t idesc = tc::idesc_u8(kTcRows, kTcN, false, true);
             const uint8_t* Abase = a.A + (size_t)tile * tc_nblk(L) * kTcBlk;
             int Q = 0;
-            for (int c = 0; c < nch; ++c) Q += nblk_of(c);
-            // producer cursor: global block index qt -> (chunk pc, block pb)
-            int qt = 0, pc = 0, pb = 0, pcn = nblk_of(0);
+            for (int c = c_lo; c < nch; ++c) Q += nblk_of(c);
+            // producer cursor: block index qt -> (chunk pc, block pb)
+            int qt = 0, pc = c_lo, pb = 0, pcn = nblk_of(c_lo);
             auto issue_tma = [&]() {
                 const int s = qt % kTcStages;
                 if (qt >= kTcStages) tc::mbar_wait(&empty[s], uint32_t((qt / kTcStages) - 1) & 1u);
@@ -207,9 +231,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
             };
             while (qt < Q && qt < kTcStages - 1) issue_tma();
             int q = 0;
-            for (int c = 0; c < nch; ++c) {
-                const int ab = c % nacc;
-                if (c >= nacc) tc::mbar_wait(&accE[ab], uint32_t((c - nacc) / nacc) & 1u);
+            for (int c = c_lo; c < nch; ++c) {
+                const int cl = c - c_lo; // local chunk index (accumulator / phase)
+                const int ab = cl % nacc;
+                if (cl >= nacc) tc::mbar_wait(&accE[ab], uint32_t((cl - nacc) / nacc) & 1u);
                 tc::fence_after();
                 const int tc0 = -31 + kTcN * c;
                 const int u_hi = tc0 < 0 ? nb : nb - tc0;
@@ -242,7 +267,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         if (ewin) { // warps 1-3: the x window of every block, in issue order
             const int bt = tid - 32;
             int q = 0;
-            for (int c = 0; c < nch; ++c) {
+            for (int c = c_lo; c < nch; ++c) {
                 const int tc0 = -31 + kTcN * c, nblk = nblk_of(c);
                 for (int b = 0; b < nblk; ++b, ++q) {
                     const int s = q % kTcStages;
@@ -267,9 +292,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         uint32_t* Pout = a.P + item * (long long)tc_scratch_limbs(L);
         const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
         uint64_t carry = 0;
-        for (int c = 0; c < nch; ++c) {
-            const int ab = c % nacc;
-            tc::mbar_wait(&accF[ab], uint32_t(c / nacc) & 1u);
+        for (int c = c_lo; c < nch; ++c) {
+            const int cl = c - c_lo;
+            const int ab = cl % nacc;
+            tc::mbar_wait(&accF[ab], uint32_t(cl / nacc) & 1u);
             tc::fence_after();
             for (int c32 = 0; c32 < kTcN; c32 += 32) {
                 uint32_t v[32];
@@ -299,6 +325,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
             __syncwarp();
             if (ln == 0) tc::mbar_arrive(&accE[ab]);
         }
+        if (G > 1 && z < G - 1 && row_ok) a.gcarry[item * (G - 1) + z] = carry; // added in the rounding pass
     }
     tc::fence_before();
     __syncthreads();
@@ -390,6 +417,8 @@ struct ItemTcRoundInv {
     int N, L, m, i, b;
     int* fb_count;
     long long* fb;
+    int G = 1;                       // chunk groups of the product kernel
+    const uint64_t* gcarry = nullptr; // their carries, added here
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         const long long nfma = (long long)(N - i - 1) * b;
         if (w >= nfma) {
@@ -414,6 +443,18 @@ struct ItemTcRoundInv {
         warp_stage16(Xs, o, L);
         warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
         warp_stage_wait();
+        if (G > 1) { // each chunk group started from carry 0: add the carries back in
+            if (lane() == 0)
+                for (int z = 0; z + 1 < G; ++z) {
+                    uint64_t v = gcarry[w * (G - 1) + z];
+                    for (int q = 64 * tc_group_first_chunk(L, G, z + 1); v != 0 && q < tc_scratch_limbs(L); ++q) {
+                        v += Ys[q];
+                        Ys[q] = uint32_t(v);
+                        v >>= 32;
+                    }
+                }
+            wsync();
+        }
         const Opd Xo{Xs, L, cm.exp - 32 * L, cm.sign};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
