@@ -108,6 +108,7 @@ struct hk_ctx {
     uint32_t* tc_P = nullptr;
     size_t tc_P_words = 0;
     uint8_t* tc_A = nullptr;      // preformatted A operand of the current step
+    int tc_A_n = 0;               // rows it was sized for
     uint64_t* tc_gcarry = nullptr; // L^-1 chunk-group carries
     cudaEvent_t prof_mid = nullptr; // hk_profile_ldlt: recorded between TC products and rounding
     int* tc_fb_count = nullptr;   // uncertified items of the current step
@@ -122,6 +123,8 @@ struct hk_ctx {
         int* d_erow = nullptr;
         int* d_ecol = nullptr;
         int* d_err = nullptr;
+        int* d_owned = nullptr;      // tensor-core path: owned columns / local offsets on the device
+        long long* d_off = nullptr;
     };
     int world = 1, rank = 0;
     bool virt = false;               // all `world` ranks emulated in this one context
@@ -344,10 +347,10 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     // LDLT (many CTAs per step): windowed x expansion (93-103 KB of shared memory)
     // and one TMEM accumulator, two CTAs per SM.  L^-1 (b <= m column CTAs per
     // step): full expansion when it fits and two accumulators, one CTA per SM.
-    a.ewin = (a.mode == 0 || hk::tc_ewin(L)) ? 1 : 0;
+    a.ewin = (a.mode != 1 || hk::tc_ewin(L)) ? 1 : 0;
     if (const char* e = getenv("HK_TC_EWIN")) a.ewin = e[0] == '1' ? 1 : 0;
     const size_t need = hk::tc_smem_bytes(L, a.ewin != 0);
-    a.nacc = (a.mode == 0 && need <= 110 * 1024) ? 1 : 2;
+    a.nacc = (a.mode != 1 && need <= 110 * 1024) ? 1 : 2;
     if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
     const size_t smem = a.nacc == 1 ? need : std::max(need, size_t(120 * 1024));
     static bool configured = false;
@@ -360,7 +363,7 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     hk::k_tc_prep<<<unsigned((nprep + 255) / 256), 256, 0, st>>>(prep, nprep);
     ck(cudaGetLastError(), "tc prep launch");
     ++c->launches;
-    const int first_row = a.mode == 0 ? a.jfirst : a.i + 1;
+    const int first_row = a.mode != 1 ? a.jfirst : a.i + 1;
     const dim3 grid(gx, unsigned(hk::tc_ntiles(N) - first_row / hk::kTcRows), unsigned(a.groups));
     hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
     ck(cudaGetLastError(), "tc bulk launch");
@@ -431,23 +434,32 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
     if (b > 0) launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st);
 }
 
-void ensure_tc_scratch(hk_ctx* c, int m = 0) {
-    if (!use_tc(c)) return;
-    const size_t items = std::max((size_t)c->n * (c->n + 1) / 2, (size_t)c->n * m);
+// Tensor-core scratch for up to `items` products per step (+ the A operand of N rows).
+void ensure_tc_items(hk_ctx* c, size_t items) {
+    if (c->tc_A_n < c->n) {
+        if (c->tc_A) cudaFree(c->tc_A);
+        c->tc_A = nullptr;
+        ck(cudaMalloc(&c->tc_A, hk::tc_apre_bytes(c->n, c->L)), "cudaMalloc tc A");
+        c->tc_A_n = c->n;
+    }
     const size_t need = items * hk::tc_scratch_limbs(c->L);
     if (c->tc_P_words >= need) return;
     if (c->tc_P) cudaFree(c->tc_P);
     if (c->tc_fb) cudaFree(c->tc_fb);
-    if (c->tc_A) cudaFree(c->tc_A);
-    ck(cudaMalloc(&c->tc_A, hk::tc_apre_bytes(c->n, c->L)), "cudaMalloc tc A");
     if (c->tc_gcarry) cudaFree(c->tc_gcarry);
-    ck(cudaMalloc(&c->tc_gcarry, items * (hk::kTcMaxGroups - 1) * sizeof(uint64_t)), "cudaMalloc tc carries");
-    if (!c->tc_fb_count) ck(cudaMalloc(&c->tc_fb_count, sizeof(int)), "cudaMalloc fb count");
     c->tc_P = nullptr;
     c->tc_fb = nullptr;
+    c->tc_gcarry = nullptr;
+    ck(cudaMalloc(&c->tc_gcarry, items * (hk::kTcMaxGroups - 1) * sizeof(uint64_t)), "cudaMalloc tc carries");
+    if (!c->tc_fb_count) ck(cudaMalloc(&c->tc_fb_count, sizeof(int)), "cudaMalloc fb count");
     ck(cudaMalloc(&c->tc_P, need * sizeof(uint32_t)), "cudaMalloc tc scratch");
     ck(cudaMalloc(&c->tc_fb, items * sizeof(long long)), "cudaMalloc fb list");
     c->tc_P_words = need;
+}
+
+void ensure_tc_scratch(hk_ctx* c, int m = 0) {
+    if (!use_tc(c)) return;
+    ensure_tc_items(c, std::max((size_t)c->n * (c->n + 1) / 2, (size_t)c->n * m));
 }
 
 void enqueue_ldlt_steps(hk_ctx* c) {
@@ -585,6 +597,8 @@ void hk_destroy(hk_ctx* c) {
         if (s.d_erow) cudaFree(s.d_erow);
         if (s.d_ecol) cudaFree(s.d_ecol);
         if (s.d_err) cudaFree(s.d_err);
+        if (s.d_owned) cudaFree(s.d_owned);
+        if (s.d_off) cudaFree(s.d_off);
     }
     if (c->nccl_comm) {
         void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -1215,7 +1229,38 @@ void shard_setup(hk_ctx* c, Shard& s, int N) {
     }
     if (!s.d_err) ck(cudaMalloc(&s.d_err, sizeof(int)), "malloc err");
     ck(cudaMemsetAsync(s.d_err, 0xff, sizeof(int), c->st), "memset err");
+    if (s.d_owned) cudaFree(s.d_owned);
+    if (s.d_off) cudaFree(s.d_off);
+    ck(cudaMalloc(&s.d_owned, (s.owned.size() + 1) * sizeof(int)), "malloc owned");
+    ck(cudaMalloc(&s.d_off, s.off.size() * sizeof(long long)), "malloc off");
+    if (!s.owned.empty())
+        ck(cudaMemcpyAsync(s.d_owned, s.owned.data(), s.owned.size() * sizeof(int), cudaMemcpyHostToDevice, c->st),
+           "H2D owned");
+    ck(cudaMemcpyAsync(s.d_off, s.off.data(), s.off.size() * sizeof(long long), cudaMemcpyHostToDevice, c->st),
+       "H2D off");
     ck(cudaStreamSynchronize(c->st), "sync");
+}
+
+// Sharded step-i update of one rank's owned columns >= i+1 on the tensor cores
+// (mode 2 of the product kernel; same ops as ItemDTrailing, bit-identical).
+void enqueue_dist_tc(hk_ctx* c, Shard& s, int i) {
+    const int N = c->n, L = c->L;
+    size_t q = 0;
+    while (q < s.owned.size() && s.owned[q] < i + 1) ++q;
+    const int ncols = int(s.owned.size() - q);
+    if (ncols <= 0) return;
+    const long long e0 = s.off[q], n = s.off.back() - e0;
+    hk::TcBulkArgs a{s.S.view(), s.panel.view(), c->tc_A, c->tc_P, N, L, i, s.owned[q], 2, 0, 0, s.d_err};
+    a.owned = s.d_owned;
+    a.off = s.d_off;
+    a.e0 = e0;
+    a.first_loc = int(q);
+    tc_products(c, a, s.B.view(), unsigned(ncols), c->st);
+    ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), c->st), "memset fb");
+    launch(c, hk::ItemTcRoundD{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err,
+                               c->tc_fb_count, c->tc_fb},
+           n, hk::tcround_words(L), c->st);
+    launch_fix(c, hk::FixD{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0}, c->st);
 }
 
 // entries of `s` belonging to owned columns >= j0 form a suffix of the local storage
@@ -1333,11 +1378,21 @@ int dist_ldlt(hk_ctx* c) {
     }
     publish(c, 0);
     for (auto& s : c->shards) derive(c, s, 0);
+    const bool tc = use_tc(c);
+    if (tc) {
+        long long most = 1;
+        for (auto& s : c->shards) most = std::max(most, s.off.back());
+        ensure_tc_items(c, most);
+    }
     for (int i = 0; i < N; ++i) {
         for (auto& s : c->shards) {
             const long long e0 = suffix_start(s, i + 1), n = s.off.back() - e0;
-            launch(c, hk::ItemDTrailing{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0, s.d_err},
-                   n, wo);
+            if (tc)
+                enqueue_dist_tc(c, s, i);
+            else
+                launch(c,
+                       hk::ItemDTrailing{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0, s.d_err},
+                       n, wo);
             if (c->owner[size_t(i)] == s.rank && N - i - 1 > 0) {
                 const long long dst = s.off[size_t(s.loc[size_t(i)])] + 1;
                 launch(c, hk::ItemCopy{s.S.view(), s.B.view(), dst, i + 1, L}, N - i - 1, 64);

@@ -98,7 +98,7 @@ struct ItemTcPrep {
         const int u0 = ks * kTcK + 16 * h;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (k > i && k < N && u0 < nb) {
-            const uint32_t* row = mode == 0 ? R.limbs(k, L) : R.limbs(tri_idx(k, i, N), L);
+            const uint32_t* row = mode != 1 ? R.limbs(k, L) : R.limbs(tri_idx(k, i, N), L);
             const uint4 g = *reinterpret_cast<const uint4*>(row + (L - 4 - u0 / 4));
             v.x = __byte_perm(g.w, 0u, 0x0123);
             v.y = __byte_perm(g.z, 0u, 0x0123);
@@ -134,6 +134,13 @@ struct TcBulkArgs {
     int ewin = 0;            // windowed x expansion
     int groups = 1;          // chunk groups (blockIdx.z): G > 1 only for L^-1 steps
     uint64_t* gcarry = nullptr; // [item][G - 1]: carry out of each group but the last
+    // mode 2 (column-sharded LDLT, one rank's owned columns): CTA x -> local column
+    // first_loc + x, global column owned[.], local entries from off[.]; x operand =
+    // the broadcast panel (X) entry j - i; items = local entry index - e0
+    const int* owned = nullptr;
+    const long long* off = nullptr;
+    long long e0 = 0;
+    int first_loc = 0;
 };
 
 #if !defined(HK_WARP_EMU)
@@ -149,9 +156,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
     __shared__ uint64_t full[kTcStages], empty[kTcStages], efull[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
-    if (a.mode == 0 && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
+    if (a.mode != 1 && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
     const int N = a.N, L = a.L, nb = tc_nb(L);
-    const int j = a.mode == 0 ? a.jfirst + int(blockIdx.x) : a.i + 1; // first valid row
+    const int locj = a.first_loc + int(blockIdx.x);
+    const int j = a.mode == 0 ? a.jfirst + int(blockIdx.x) : a.mode == 2 ? a.owned[locj] : a.i + 1; // first valid row
     const int tile = j / kTcRows + int(blockIdx.y);
     if (j >= N || tile * kTcRows >= N) return;
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
@@ -177,8 +185,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     };
 
     // x bytes into sX (word 8 = byte 32 holds X[0]); cells p = pmin + c: X[p .. p+15]
-    const uint32_t* xl = a.mode == 0 ? a.S.limbs(tri_idx(j, a.i, N), L)
-                                     : a.X.limbs((long long)a.i * a.m + blockIdx.x, L);
+    const uint32_t* xl = a.mode == 0   ? a.S.limbs(tri_idx(j, a.i, N), L)
+                         : a.mode == 2 ? a.X.limbs(j - a.i, L)
+                                       : a.X.limbs((long long)a.i * a.m + blockIdx.x, L);
     for (int w = tid; w < tc_sx_words(L); w += kTcThreads) sX[w] = (w >= 8 && w < 8 + L) ? xl[w - 8] : 0u;
     __syncthreads();
     if (!ewin) {
@@ -287,8 +296,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         const bool row_ok = k >= j && k < N;
         long long item = 0;
         if (row_ok)
-            item = a.mode == 0 ? col_off(j - a.jfirst, N - a.jfirst) + (k - j)
-                               : (long long)(k - a.i - 1) * a.b + blockIdx.x;
+            item = a.mode == 0   ? col_off(j - a.jfirst, N - a.jfirst) + (k - j)
+                   : a.mode == 2 ? a.off[locj] + (k - j) - a.e0
+                                 : (long long)(k - a.i - 1) * a.b + blockIdx.x;
         uint32_t* Pout = a.P + item * (long long)tc_scratch_limbs(L);
         const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
         uint64_t carry = 0;
@@ -475,6 +485,52 @@ struct ItemTcRoundInv {
     }
 };
 
+// Sharded LDLT step i on one rank (mode 2): local entry e = e0 + w of the owned
+// columns >= i+1, S(k,j) = RNE(S(k,j) - panel(j-i) B_i(k)) (ItemDTrailing's op).
+struct ItemTcRoundD {
+    MpArr S, panel, B;
+    const int* erow;
+    const int* ecol;
+    const uint32_t* P;
+    int L, i;
+    long long e0;
+    const int* err;
+    int* fb_count;
+    long long* fb;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const long long e = e0 + w;
+        const int k = erow[e], j = ecol[e];
+        const Meta cm = S.m[e], xm = panel.m[j - i], ym = B.m[k];
+        const int sp = -(xm.sign * ym.sign);
+        if (sp == 0) return;
+        uint32_t* c = S.limbs(e, L);
+        const int t0 = L - kTcGuard;
+        const int lsbP = xm.exp + ym.exp - 64 * L;
+        uint32_t* Xs = ws;
+        uint32_t* Ys = ws + align4(L);
+        warp_stage16(Xs, c, L);
+        warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
+        warp_stage_wait();
+        const Opd X{Xs, L, cm.exp - 32 * L, cm.sign};
+        const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
+        bool ok = false;
+        const RMeta rr = warp_round_sum(X, Y, Ys + align4(L + kTcGuard), c, L, lsbP + 32 * t0 + 46, &ok);
+        if (lane() == 0) {
+            if (ok) {
+                S.m[e] = Meta{rr.exp, rr.sign};
+            } else {
+#if defined(HK_WARP_EMU)
+                fb[(*fb_count)++] = w;
+#else
+                fb[atomicAdd(fb_count, 1)] = w;
+#endif
+            }
+        }
+        wsync();
+    }
+};
+
 // Exact redo of one uncertified item (full warp FMA workspace).
 struct FixLdlt {
     MpArr S, B;
@@ -499,6 +555,23 @@ struct FixInv {
         uint32_t* o = X.limbs(xc, L);
         const Meta r = warp_fms(o, X.m[xc], S.limbs(el, L), S.m[el], X.limbs(xi, L), X.m[xi], o, L, opws_carve(ws, L));
         if (lane() == 0) X.m[xc] = r;
+        wsync();
+    }
+};
+
+struct FixD {
+    MpArr S, panel, B;
+    const int* erow;
+    const int* ecol;
+    int L, i;
+    long long e0;
+    HK_DEV void operator()(long long w, uint32_t* ws) const {
+        const long long e = e0 + w;
+        const int k = erow[e], j = ecol[e];
+        uint32_t* c = S.limbs(e, L);
+        const Meta r =
+            warp_fms(c, S.m[e], panel.limbs(j - i, L), panel.m[j - i], B.limbs(k, L), B.m[k], c, L, opws_carve(ws, L));
+        if (lane() == 0) S.m[e] = r;
         wsync();
     }
 };
