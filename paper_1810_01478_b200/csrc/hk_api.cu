@@ -229,6 +229,10 @@ void launch_cta(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t s
         const size_t v = smem < 48 * 1024 ? 48 * 1024 : smem;
         ck(cudaFuncSetAttribute(k_cta_items<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v)),
            "cudaFuncSetAttribute");
+        // every kernel asks for the same (maximal) shared-memory carveout, so the
+        // critical-path CTAs can start on SMs busy with bulk work without an L1/smem
+        // reconfiguration (which waits for the SM to drain)
+        ck(cudaFuncSetAttribute(k_cta_items<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         configured[key] = v;
     }
     const long long blocks = n < (1LL << 30) ? n : (1LL << 30);
@@ -356,6 +360,8 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     static bool configured = false;
     if (!configured) {
         ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");
+        ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        ck(cudaFuncSetAttribute(hk::k_tc_prep, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         configured = true;
     }
     const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
@@ -378,6 +384,7 @@ void launch_fix(hk_ctx* c, const F& f, cudaStream_t st) {
     static bool cfg = false;
     if (!cfg) {
         ck(cudaFuncSetAttribute(hk::k_tc_fix<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "fix attr");
+        ck(cudaFuncSetAttribute(hk::k_tc_fix<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         cfg = true;
     }
     hk::k_tc_fix<F><<<unsigned(c->sm_count), unsigned(32 * wpb), size_t(wo) * 4 * wpb, st>>>(f, c->tc_fb_count,
@@ -685,7 +692,7 @@ int hk_ldlt(hk_ctx* c) {
             enqueue_ldlt_steps(c);
             ck(cudaStreamEndCapture(c->st, &g), "end capture");
             cudaGraphExec_t ge;
-            ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+            ck(cudaGraphInstantiateWithFlags(&ge, g, cudaGraphInstantiateFlagUseNodePriority), "graph instantiate");
             cudaGraphDestroy(g);
             it = c->graphs.emplace(N, ge).first;
             c->graph_launches[N] = c->launches - before;
