@@ -376,6 +376,26 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     ++c->launches;
 }
 
+// Per-(column, row) items over `ncols` columns of at most `maxrows` rows (k_cols).
+template <class F>
+void launch_cols(hk_ctx* c, const F& f, int ncols, int maxrows, int ws_words, cudaStream_t st) {
+    if (ncols <= 0 || maxrows <= 0) return;
+    const size_t per_warp = size_t(ws_words) * sizeof(uint32_t);
+    int wpb = int((96 * 1024) / per_warp);
+    wpb = std::max(1, std::min(8, wpb));
+    const size_t smem = per_warp * wpb;
+    static bool cfg = false;
+    if (!cfg) {
+        ck(cudaFuncSetAttribute(hk::k_cols<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024), "cols attr");
+        ck(cudaFuncSetAttribute(hk::k_cols<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        cfg = true;
+    }
+    const unsigned gx = unsigned((maxrows + wpb - 1) / wpb);
+    hk::k_cols<F><<<dim3(gx, unsigned(ncols)), unsigned(32 * wpb), smem, st>>>(f, ws_words);
+    ck(cudaGetLastError(), "cols launch");
+    ++c->launches;
+}
+
 // Exact redo of the items the rounding pass could not certify (device-side count).
 template <class F>
 void launch_fix(hk_ctx* c, const F& f, cudaStream_t st) {
@@ -410,9 +430,9 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
     if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
     ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
     if (!dev_skip("round"))
-        launch(c,
-               hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count, c->tc_fb},
-               (long long)ncols * (ncols + 1) / 2, hk::tcround_words(L), st);
+        launch_cols(c, hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count,
+                                       c->tc_fb},
+                    ncols, ncols, hk::tcround_words(L), st);
     if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st);
 }
 

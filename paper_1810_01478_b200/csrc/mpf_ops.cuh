@@ -87,7 +87,7 @@ HK_DEV RMeta round_with_product(const Opd& X, const uint32_t* xd, const uint32_t
 HK_DEV Meta warp_fms(const uint32_t* cd, Meta cm, const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym,
                      uint32_t* out, int L, const OpWs& ws) {
     const int sp = -(xm.sign * ym.sign);
-    const Opd X{cd, L, cm.exp - 32 * L, cm.sign};
+    const Opd X{cd, L, cm.exp - 32 * L, cm.sign, 32 * L};
     if (sp == 0) {
         const Opd Z{nullptr, 0, 0, 0};
         const RMeta r = warp_round_sum(X, Z, ws.G, out, L);
@@ -139,12 +139,12 @@ HK_DEV void warp_fms2(const uint32_t* c0, Meta cm0, const uint32_t* x0, Meta xm0
     wsync();
     const int lsb0 = xm0.exp + ym.exp - 64 * L, lsb1 = xm1.exp + ym.exp - 64 * L;
     bool ok = false;
-    RMeta a = warp_round_sum(Opd{c0, L, cm0.exp - 32 * L, cm0.sign},
+    RMeta a = warp_round_sum(Opd{c0, L, cm0.exp - 32 * L, cm0.sign, 32 * L},
                                   Opd{P0 + t0, 2 * L - t0, lsb0 + 32 * t0, sp0}, ws, out0, L,
                                   lsb0 + 32 * t0 + 46, &ok);
     if (ok) r0 = Meta{a.exp, a.sign};
     else r0 = warp_fms(c0, cm0, x0, xm0, yd, ym, out0, L, opws_carve(ws, L));
-    a = warp_round_sum(Opd{c1, L, cm1.exp - 32 * L, cm1.sign}, Opd{P1 + t0, 2 * L - t0, lsb1 + 32 * t0, sp1},
+    a = warp_round_sum(Opd{c1, L, cm1.exp - 32 * L, cm1.sign, 32 * L}, Opd{P1 + t0, 2 * L - t0, lsb1 + 32 * t0, sp1},
                             ws, out1, L, lsb1 + 32 * t0 + 46, &ok);
     if (ok) r1 = Meta{a.exp, a.sign};
     else r1 = warp_fms(c1, cm1, x1, xm1, yd, ym, out1, L, opws_carve(ws, L));
@@ -153,8 +153,8 @@ HK_DEV void warp_fms2(const uint32_t* c0, Meta cm0, const uint32_t* x0, Meta xm0
 // out = RNE(x + y); x, y may alias out.
 HK_DEV Meta warp_addr(const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym, uint32_t* out, int L,
                       const OpWs& ws) {
-    const Opd X{xd, L, xm.exp - 32 * L, xm.sign};
-    const Opd Y{yd, L, ym.exp - 32 * L, ym.sign};
+    const Opd X{xd, L, xm.exp - 32 * L, xm.sign, 32 * L};
+    const Opd Y{yd, L, ym.exp - 32 * L, ym.sign, 32 * L};
     const RMeta r = warp_round_sum(X, Y, ws.G, out, L);
     return Meta{r.exp, r.sign};
 }
@@ -431,7 +431,7 @@ HK_DEV Meta cta_round_with_product(const Opd& X, const uint32_t* xd, const uint3
 HK_DEV Meta cta_fms(const uint32_t* cd, Meta cm, const uint32_t* xd, Meta xm, const uint32_t* yd, Meta ym,
                     uint32_t* out, int L, const CtaWs& w) {
     const int sp = -(xm.sign * ym.sign);
-    const Opd X{cd, L, cm.exp - 32 * L, cm.sign};
+    const Opd X{cd, L, cm.exp - 32 * L, cm.sign, 32 * L};
     if (sp == 0) {
         RMeta r{0, 0};
         if (warp_id() == 0) r = warp_round_sum(X, Opd{nullptr, 0, 0, 0}, w.op.G, out, L);

@@ -134,7 +134,8 @@ struct Opd {
     const uint32_t* d;
     int n;
     int lsb;
-    int sign; // -1, 0, +1 (0 => value zero, d ignored)
+    int sign;    // -1, 0, +1 (0 => value zero, d ignored)
+    int bl = 0;  // bit length of INT(d) when known (normalised mantissa: 32 n), else 0
 };
 
 // Carry-lookahead over one 32-limb segment (one limb per lane).  `w` is the
@@ -490,8 +491,8 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
                                  int ubit = kExact, bool* ok = nullptr) {
     const int ln = lane();
     if (ok) *ok = true;
-    const int blX = Xin.sign ? warp_bitlen(Xin.d, Xin.n) : 0;
-    const int blY = Yin.sign ? warp_bitlen(Yin.d, Yin.n) : 0;
+    const int blX = Xin.sign ? (Xin.bl ? Xin.bl : warp_bitlen(Xin.d, Xin.n)) : 0;
+    const int blY = Yin.sign ? (Yin.bl ? Yin.bl : warp_bitlen(Yin.d, Yin.n)) : 0;
     if (blX == 0 && blY == 0) {
         for (int i = ln; i < nout; i += 32) out[i] = 0u;
         wsync();
@@ -598,8 +599,20 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
         if (u_rel < 32) u_rel = 32;
         bool safe = rb_rel - u_rel >= 4;
         if (safe) {
-            const int rs = warp_bit_range(G, nw, u_rel, rb_rel - 1);
-            safe = rbit ? (rs & 1) != 0 : (rs & 2) == 0;
+            // fast path: the (up to) 64 bits just below the round bit almost always
+            // decide it (a set bit when rbit, a clear bit otherwise); else scan all
+            const int lo = rb_rel - 64 > u_rel ? rb_rel - 64 : u_rel;
+            const int q = lo >> 5, sh = lo & 31, nbits = rb_rel - lo; // 4 <= nbits <= 64
+            const uint32_t w0 = G[q], w1 = q + 1 < nw ? G[q + 1] : 0u, w2 = q + 2 < nw ? G[q + 2] : 0u;
+            const uint64_t v = (((uint64_t)fshr(w1, w2, sh) << 32) | fshr(w0, w1, sh)) &
+                               (nbits >= 64 ? ~0ull : ((1ull << nbits) - 1ull));
+            const uint64_t all = nbits >= 64 ? ~0ull : ((1ull << nbits) - 1ull);
+            if (rbit ? v != 0ull : v != all) {
+                safe = true;
+            } else {
+                const int rs = warp_bit_range(G, nw, u_rel, rb_rel - 1);
+                safe = rbit ? (rs & 1) != 0 : (rs & 2) == 0;
+            }
         }
         if (!safe) {
             *ok = false;

@@ -382,11 +382,18 @@ struct ItemTcRound {
     int* fb_count;
     long long* fb;
     HK_DEV void operator()(long long w, uint32_t* ws) const {
-        if (*(volatile const int*)err >= 0) return;
         const int n2 = N - jfirst;
         int jj, kk;
         tri_decode(w, n2, jj, kk);
-        const int j = jfirst + jj, k = jfirst + kk;
+        item(w, jfirst + jj, jfirst + kk, ws);
+    }
+    // 2-D launch (k_cols): column offset jj, row r of that column
+    HK_DEV int rows(int jj) const { return N - jfirst - jj; }
+    HK_DEV void operator()(int jj, int r, uint32_t* ws) const {
+        item(col_off(jj, N - jfirst) + r, jfirst + jj, jfirst + jj + r, ws);
+    }
+    HK_DEV void item(long long w, int j, int k, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
         const long long ec = tri_idx(k, j, N), ex = tri_idx(j, i, N);
         const Meta cm = S.m[ec], xm = S.m[ex], ym = B.m[k];
         uint32_t* c = S.limbs(ec, L);
@@ -399,7 +406,7 @@ struct ItemTcRound {
         warp_stage16(Xs, c, L);
         warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
         warp_stage_wait();
-        const Opd X{Xs, L, cm.exp - 32 * L, cm.sign};
+        const Opd X{Xs, L, cm.exp - 32 * L, cm.sign, 32 * L};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
         const RMeta rr = warp_round_sum(X, Y, Ys + align4(L + kTcGuard), c, L,
@@ -465,7 +472,7 @@ struct ItemTcRoundInv {
                 }
             wsync();
         }
-        const Opd Xo{Xs, L, cm.exp - 32 * L, cm.sign};
+        const Opd Xo{Xs, L, cm.exp - 32 * L, cm.sign, 32 * L};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
         const RMeta rr = warp_round_sum(Xo, Y, Ys + align4(L + kTcGuard), o, L,
@@ -512,7 +519,7 @@ struct ItemTcRoundD {
         warp_stage16(Xs, c, L);
         warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
         warp_stage_wait();
-        const Opd X{Xs, L, cm.exp - 32 * L, cm.sign};
+        const Opd X{Xs, L, cm.exp - 32 * L, cm.sign, 32 * L};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
         const RMeta rr = warp_round_sum(X, Y, Ys + align4(L + kTcGuard), c, L, lsbP + 32 * t0 + 46, &ok);
@@ -577,6 +584,17 @@ struct FixD {
 };
 
 #if !defined(HK_WARP_EMU)
+// Column-wise launch of a per-(column, row) item (no triangle decode per item):
+// blockIdx.y = column offset, warps stride over that column's rows.
+template <class F>
+__global__ void __launch_bounds__(256) k_cols(F f, int ws_words) {
+    extern __shared__ __align__(16) uint32_t csm[];
+    const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    uint32_t* ws = csm + (size_t)wib * ws_words;
+    const int jj = int(blockIdx.y), rows = f.rows(jj);
+    for (int r = int(blockIdx.x) * wpb + wib; r < rows; r += int(gridDim.x) * wpb) f(jj, r, ws);
+}
+
 template <class F>
 __global__ void __launch_bounds__(256) k_tc_fix(F f, const int* fb_count, const long long* fb, int ws_words) {
     extern __shared__ uint32_t fsm[];
