@@ -83,7 +83,8 @@ struct hk_ctx {
     cudaStream_t st2 = nullptr; // high-priority look-ahead stream
     cudaStream_t st3 = nullptr; // high-priority: off-diagonal part of the look-ahead column
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
-    std::vector<cudaEvent_t> evP, evR, evU, evD, evO; // per-step dependencies (graph capture)
+    std::vector<cudaEvent_t> evP, evR, evU, evD, evO, evC, evB1; // per-step dependencies (graph capture)
+    cudaEvent_t evJoin2 = nullptr;
     DevArr mu, S, R, B, X, Y, T, T2, M;
     int* d_err = nullptr;
     std::string err;
@@ -111,7 +112,7 @@ struct hk_ctx {
     int tc_A_n = 0;               // rows it was sized for
     uint64_t* tc_gcarry = nullptr; // L^-1 chunk-group carries
     cudaEvent_t prof_mid = nullptr; // hk_profile_ldlt: recorded between TC products and rounding
-    int* tc_fb_count = nullptr;   // uncertified items of the current step
+    int* tc_fb_count = nullptr;   // uncertified items: [0] / [1] by step parity, [2] sharded path
     long long* tc_fb = nullptr;
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
     struct Shard {
@@ -398,7 +399,7 @@ void launch_cols(hk_ctx* c, const F& f, int ncols, int maxrows, int ws_words, cu
 
 // Exact redo of the items the rounding pass could not certify (device-side count).
 template <class F>
-void launch_fix(hk_ctx* c, const F& f, cudaStream_t st) {
+void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset) {
     const int wo = ws_op_words(c->L);
     const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
     static bool cfg = false;
@@ -407,8 +408,8 @@ void launch_fix(hk_ctx* c, const F& f, cudaStream_t st) {
         ck(cudaFuncSetAttribute(hk::k_tc_fix<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         cfg = true;
     }
-    hk::k_tc_fix<F><<<unsigned(c->sm_count), unsigned(32 * wpb), size_t(wo) * 4 * wpb, st>>>(f, c->tc_fb_count,
-                                                                                            c->tc_fb, wo);
+    hk::k_tc_fix<F><<<unsigned(c->sm_count), unsigned(32 * wpb), size_t(wo) * 4 * wpb, st>>>(f, count, c->tc_fb, wo,
+                                                                                            reset);
     ck(cudaGetLastError(), "tc fix launch");
     ++c->launches;
 }
@@ -428,12 +429,13 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
         tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
                     b_buf(c, i), unsigned(ncols), st);
     if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
-    ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
+    // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
+    int* cnt = c->tc_fb_count + (i & 1);
+    int* nxt = c->tc_fb_count + ((i + 1) & 1);
     if (!dev_skip("round"))
-        launch_cols(c, hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, c->tc_fb_count,
-                                       c->tc_fb},
+        launch_cols(c, hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, cnt, c->tc_fb},
                     ncols, ncols, hk::tcround_words(L), st);
-    if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st);
+    if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st, cnt, nxt);
 }
 
 // L^-1 step i on the tensor cores (same product kernel, mode 1).
@@ -452,13 +454,17 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
         a.gcarry = c->tc_gcarry;
         tc_products(c, a, c->S.view(), unsigned(b), st);
     }
-    ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), st), "memset fb");
+    int* cnt = c->tc_fb_count + (i & 1);
+    int* nxt = c->tc_fb_count + ((i + 1) & 1);
     const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
-    hk::ItemTcRoundInv ri{c->S.view(), c->X.view(), c->tc_P, N, L, m, i, b, c->tc_fb_count, c->tc_fb};
+    hk::ItemTcRoundInv ri{c->S.view(), c->X.view(), c->tc_P, N, L, m, i, b, cnt, c->tc_fb};
     ri.G = G;
     ri.gcarry = c->tc_gcarry;
     launch(c, ri, items, hk::tcround_words(L), st);
-    if (b > 0) launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st);
+    if (b > 0)
+        launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st, cnt, nxt);
+    else
+        ck(cudaMemsetAsync(nxt, 0, sizeof(int), st), "memset fb");
 }
 
 // Tensor-core scratch for up to `items` products per step (+ the A operand of N rows).
@@ -478,7 +484,10 @@ void ensure_tc_items(hk_ctx* c, size_t items) {
     c->tc_fb = nullptr;
     c->tc_gcarry = nullptr;
     ck(cudaMalloc(&c->tc_gcarry, items * (hk::kTcMaxGroups - 1) * sizeof(uint64_t)), "cudaMalloc tc carries");
-    if (!c->tc_fb_count) ck(cudaMalloc(&c->tc_fb_count, sizeof(int)), "cudaMalloc fb count");
+    if (!c->tc_fb_count) {
+        ck(cudaMalloc(&c->tc_fb_count, 4 * sizeof(int)), "cudaMalloc fb count");
+        ck(cudaMemset(c->tc_fb_count, 0, 4 * sizeof(int)), "memset fb count");
+    }
     ck(cudaMalloc(&c->tc_P, need * sizeof(uint32_t)), "cudaMalloc tc scratch");
     ck(cudaMalloc(&c->tc_fb, items * sizeof(long long)), "cudaMalloc fb list");
     c->tc_P_words = need;
@@ -498,7 +507,10 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     std::vector<cudaEvent_t>& evU = c->evU;
     std::vector<cudaEvent_t>& evD = c->evD;
     std::vector<cudaEvent_t>& evO = c->evO;
+    std::vector<cudaEvent_t>& evC = c->evC;
+    std::vector<cudaEvent_t>& evB1 = c->evB1;
     cudaStream_t la2 = c->st3;
+    if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), bulk), "memset fb counters");
     ck(cudaEventRecord(c->evFork, bulk), "fork");
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
     const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
@@ -530,17 +542,31 @@ void enqueue_ldlt_steps(hk_ctx* c) {
                 launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 0}, 1, wc, la);
             if (!dev_skip("recip"))
                 launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la);
+            ck(cudaEventRecord(evC[i + 1], la), "evC");
+            // B_{i+1}: the first entry (all the next diagonal update needs) on `la`,
+            // the rest on `la2`; B buffer (i+1) % 3 was last read by StoreL(i-2)
             if (i >= 2) ck(cudaStreamWaitEvent(la, evR[i - 2], 0), "wait R");
             ck(cudaStreamWaitEvent(la, evO[i + 1], 0), "wait O");
-            if (!dev_skip("mulb"))
-                launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err},
-                           N - i - 2, wc, la);
-            ck(cudaEventRecord(evP[i + 1], la), "evP");
+            if (!dev_skip("mulb") && N - i - 2 > 0)
+                launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err, 1}, 1,
+                           wc, la);
+            ck(cudaEventRecord(evB1[i + 1], la), "evB1");
+            ck(cudaStreamWaitEvent(la2, evC[i + 1], 0), "wait C");
+            if (i >= 2) ck(cudaStreamWaitEvent(la2, evR[i - 2], 0), "wait R2");
+            if (!dev_skip("mulb") && N - i - 3 > 0)
+                launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err, 2},
+                           N - i - 3, wc, la2);
+            ck(cudaStreamWaitEvent(la2, evB1[i + 1], 0), "wait B1");
+            ck(cudaEventRecord(evP[i + 1], la2), "evP");
         }
     }
     // StoreL(N-1) has no rows; join the streams (the last ColUpd read S(N-1, N-2))
     ck(cudaEventRecord(c->evJoin, la), "join");
     ck(cudaStreamWaitEvent(bulk, c->evJoin, 0), "join wait");
+    if (N >= 2) { // la2 joined the capture at step 0
+        ck(cudaEventRecord(c->evJoin2, la2), "join2");
+        ck(cudaStreamWaitEvent(bulk, c->evJoin2, 0), "join2 wait");
+    }
 }
 
 void ensure_step_events(hk_ctx* c, int N) {
@@ -556,6 +582,8 @@ void ensure_step_events(hk_ctx* c, int N) {
     grow(c->evU, N);
     grow(c->evD, N);
     grow(c->evO, N);
+    grow(c->evC, N);
+    grow(c->evB1, N);
 }
 
 int check_pivots(hk_ctx* c) {
@@ -600,6 +628,7 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, hi), "cudaStreamCreate la2");
         ck(cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->evJoin2, cudaEventDisableTiming), "event");
         ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
         ck(cudaEventCreate(&c->ev[0]), "event");
         ck(cudaEventCreate(&c->ev[1]), "event");
@@ -645,6 +674,9 @@ void hk_destroy(hk_ctx* c) {
     for (auto e : c->evU) cudaEventDestroy(e);
     for (auto e : c->evD) cudaEventDestroy(e);
     for (auto e : c->evO) cudaEventDestroy(e);
+    for (auto e : c->evC) cudaEventDestroy(e);
+    for (auto e : c->evB1) cudaEventDestroy(e);
+    if (c->evJoin2) cudaEventDestroy(c->evJoin2);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
     if (c->st2) cudaStreamDestroy(c->st2);
@@ -776,6 +808,7 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
             const long long before = c->launches;
             cudaGraph_t g;
             ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), c->st), "memset fb counters");
             launch(c, hk::ItemInvInit{c->S.view(), c->X.view(), N, L, m}, (long long)N * m, 64);
             for (int i = 0; i < N; ++i) {
                 const int b = i < m ? i : m;
@@ -1049,6 +1082,7 @@ int hk_profile_ldlt(hk_ctx* c, double* ms7, long long* n_trailing) {
         ck(cudaEventCreate(&e1), "event");
         ck(cudaEventRecord(e0, c->st), "event");
         launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
+        if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), c->st), "memset fb counters");
         long long nt = 0;
         for (int i = 0; i < N; ++i) {
             timed(1, [&] {
@@ -1283,11 +1317,13 @@ void enqueue_dist_tc(hk_ctx* c, Shard& s, int i) {
     a.e0 = e0;
     a.first_loc = int(q);
     tc_products(c, a, s.B.view(), unsigned(ncols), c->st);
-    ck(cudaMemsetAsync(c->tc_fb_count, 0, sizeof(int), c->st), "memset fb");
+    int* cnt = c->tc_fb_count + 2;
+    ck(cudaMemsetAsync(cnt, 0, sizeof(int), c->st), "memset fb");
     launch(c, hk::ItemTcRoundD{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err,
-                               c->tc_fb_count, c->tc_fb},
+                               cnt, c->tc_fb},
            n, hk::tcround_words(L), c->st);
-    launch_fix(c, hk::FixD{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0}, c->st);
+    launch_fix(c, hk::FixD{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0}, c->st, cnt,
+               c->tc_fb_count + 3);
 }
 
 // entries of `s` belonging to owned columns >= j0 form a suffix of the local storage

@@ -428,13 +428,14 @@ struct CItemRecip { // R_i = RNE(1/S_ii) with the pivot sign test
     }
 };
 
-struct CItemMulB { // B_i(k) = RNE(S(k,i) R_i), k = i+1+t
+struct CItemMulB { // B_i(k) = RNE(S(k,i) R_i), k = i+k0+t
     MpArr S, R, B;
     int N, L, i;
     const int* err;
+    int k0 = 1;
     HK_DEV void operator()(long long t, uint32_t* ws) const {
         if (*(volatile const int*)err >= 0) return;
-        const int k = i + 1 + int(t);
+        const int k = i + k0 + int(t);
         const long long e = tri_idx(k, i, N);
         cta_meta_store(B.m + k, cta_mulr(S.limbs(e, L), S.m[e], R.limbs(i, L), R.m[i], B.limbs(k, L), L,
                                          ctaws_carve(ws, L)));
