@@ -390,6 +390,16 @@ HK_DEV void cta_stage_and_mul(const uint32_t* xd, const uint32_t* yd, int L, con
     cta_mul(w.op.A, L, w.op.Bp, L, w.op.P, t0, w.CS);
 }
 
+HK_DEV void atomicMax_emu(int* a, int v) {
+#if defined(HK_WARP_EMU)
+    int cur = __atomic_load_n(a, __ATOMIC_RELAXED); // emulated lanes are host threads
+    while (cur < v && !__atomic_compare_exchange_n(a, &cur, v, false, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+    }
+#else
+    atomicMax(a, v);
+#endif
+}
+
 // warp 0's RMeta (and ok flag) to every thread of the CTA
 HK_DEV RMeta cta_bcast_meta(const CtaWs& w, RMeta r, bool ok, bool* ok_out) {
     if (warp_id() == 0 && lane() == 0) {
@@ -589,25 +599,35 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
     for (int si = ns - 1 - nreg; si >= 0; --si) {
         const int nk = sched[si];
         const int mn = nk >= L ? L : nk;
-        // T = m_top * z
+        // T = m_top * z; only limbs FT-nk .. FT are used: a short product from two
+        // guard limbs below (the dropped columns perturb limb FT-nk by at most a unit,
+        // inside the level's truncation budget; the final Ziv test / exact fallback
+        // still decides the rounding)
+        const int FT = mn + nf; // fraction limbs of T
+        const int tT = FT - nk - 2 > 0 ? FT - nk - 2 : 0;
         cta_copy(w.rw.A, Md + (L - mn), mn);
         cta_stage_padded(w.rw.Bp, Z, nf + 1);
+        if (cta_tid() == 0) w.sh[1] = 0;
         cta_sync();
-        cta_mul(w.rw.A, mn, w.rw.Bp, nf + 1, w.rw.P, 0, w.CS);
+        cta_mul(w.rw.A, mn, w.rw.Bp, nf + 1, w.rw.P, tT, w.CS);
         HK_TRACE(1);
-        const int FT = mn + nf; // fraction limbs of T
         const bool neg = w.rw.P[FT] != 0u; // T >= 1  ->  e <= 0
         for (int q = cta_tid(); q < nk; q += cta_threads()) {
             const uint32_t v = w.rw.P[FT - nk + q];
-            w.rw.E[q] = neg ? v : ~v;
+            const uint32_t e = neg ? v : ~v;
+            w.rw.E[q] = e;
+            if (e != 0u) atomicMax_emu(w.sh + 1, q + 1);
         }
         cta_sync();
-        // D = z * |e|
+        // D = z * |e|: |e| < 2^(-32 (nf - 1)), so its top limbs are zero; the product
+        // runs over the ne significant ones only (exact: zeros contribute nothing)
+        const int ne = w.sh[1] > 0 ? w.sh[1] : 1;
         cta_copy(w.rw.A, Z, nf + 1);
-        cta_stage_padded(w.rw.Bp, w.rw.E, nk);
+        cta_stage_padded(w.rw.Bp, w.rw.E, ne);
         cta_sync();
-        cta_mul(w.rw.A, nf + 1, w.rw.Bp, nk, w.rw.P, 0, w.CS);
+        cta_mul(w.rw.A, nf + 1, w.rw.Bp, ne, w.rw.P, 0, w.CS);
         HK_TRACE(2);
+        const int nD = nf + 1 + ne; // limbs of D
         // Z' = (Z << 32 (nk - nf)) -/+ (D >> 32 nf), over nk + 1 limbs
         if (w0) {
             const int shl = nk - nf;
@@ -615,7 +635,7 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
             for (int b0 = 0; b0 <= nk; b0 += 32) {
                 const int q = b0 + lane();
                 const uint32_t zv = (q <= nk && q >= shl) ? Z[q - shl] : 0u;
-                const uint32_t dv = q <= nk ? w.rw.P[nf + q] : 0u;
+                const uint32_t dv = (q <= nk && nf + q < nD) ? w.rw.P[nf + q] : 0u;
                 uint32_t r;
                 if (neg) {
                     r = zv - dv;
