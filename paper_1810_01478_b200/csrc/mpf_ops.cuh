@@ -605,11 +605,13 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
         // still decides the rounding)
         const int FT = mn + nf; // fraction limbs of T
         const int tT = FT - nk - 2 > 0 ? FT - nk - 2 : 0;
-        cta_copy(w.rw.A, Md + (L - mn), mn);
+        // m_top sits in rw.T (free until the final round): staged before the first
+        // CTA level, later by the warps idle during the previous level's Z update
+        if (si == ns - 1 - nreg) cta_copy(w.rw.T, Md + (L - mn), mn);
         cta_stage_padded(w.rw.Bp, Z, nf + 1);
         if (cta_tid() == 0) w.sh[1] = 0;
         cta_sync();
-        cta_mul(w.rw.A, mn, w.rw.Bp, nf + 1, w.rw.P, tT, w.CS);
+        cta_mul(w.rw.T, mn, w.rw.Bp, nf + 1, w.rw.P, tT, w.CS);
         HK_TRACE(1);
         const bool neg = w.rw.P[FT] != 0u; // T >= 1  ->  e <= 0
         for (int q = cta_tid(); q < nk; q += cta_threads()) {
@@ -646,6 +648,12 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
                 }
                 if (q <= nk) Zn[q] = r;
             }
+        }
+        if (si > 0 && (!w0 || num_warps() == 1)) { // stage the next level's m_top
+            const int mn1 = sched[si - 1] >= L ? L : sched[si - 1];
+            const int t0 = num_warps() == 1 ? cta_tid() : cta_tid() - 32;
+            const int nt = num_warps() == 1 ? cta_threads() : cta_threads() - 32;
+            for (int q = t0; q < mn1; q += nt) w.rw.T[q] = Md[L - mn1 + q];
         }
         cta_sync();
         HK_TRACE(3);
