@@ -630,23 +630,34 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
         cta_mul(w.rw.A, nf + 1, w.rw.Bp, ne, w.rw.P, 0, w.CS);
         HK_TRACE(2);
         const int nD = nf + 1 + ne; // limbs of D
-        // Z' = (Z << 32 (nk - nf)) -/+ (D >> 32 nf), over nk + 1 limbs
+        // Z' = (Z << 32 (nk - nf)) -/+ (D >> 32 nf), over nk + 1 limbs; four limbs per
+        // lane, one ballot lookahead per 128 limbs
         if (w0) {
             const int shl = nk - nf;
             uint32_t c = 0;
-            for (int b0 = 0; b0 <= nk; b0 += 32) {
-                const int q = b0 + lane();
-                const uint32_t zv = (q <= nk && q >= shl) ? Z[q - shl] : 0u;
-                const uint32_t dv = (q <= nk && nf + q < nD) ? w.rw.P[nf + q] : 0u;
-                uint32_t r;
-                if (neg) {
-                    r = zv - dv;
-                    c = seg_borrow(r, zv < dv, c);
-                } else {
-                    r = zv + dv;
-                    c = seg_carry(r, r < zv, c);
+            for (int b0 = 0; b0 <= nk; b0 += 128) {
+                const int q0 = b0 + 4 * lane();
+                uint32_t r[4];
+                uint32_t br = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int q = q0 + t;
+                    const uint32_t zv = (q <= nk && q >= shl) ? Z[q - shl] : 0u;
+                    const uint32_t dv = (q <= nk && nf + q < nD) ? w.rw.P[nf + q] : 0u;
+                    const uint64_t d = neg ? (uint64_t)zv - dv - br : (uint64_t)zv + dv + br;
+                    r[t] = uint32_t(d);
+                    br = neg ? uint32_t(d >> 63) : uint32_t(d >> 32);
                 }
-                if (q <= nk) Zn[q] = r;
+                if (neg) {
+                    const uint32_t ci = lane_carry_in(br != 0u, (r[0] | r[1] | r[2] | r[3]) == 0u, c);
+                    ripple_sub4(r, ci);
+                } else {
+                    const uint32_t ci = lane_carry_in(br != 0u, (r[0] & r[1] & r[2] & r[3]) == 0xffffffffu, c);
+                    ripple_add4(r, ci);
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (q0 + t <= nk) Zn[q0 + t] = r[t];
             }
         }
         if (si > 0 && (!w0 || num_warps() == 1)) { // stage the next level's m_top
