@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 #include <nccl.h> // types only; libnccl.so.2 is dlopen'ed (multi-GPU section)
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -126,7 +127,12 @@ struct hk_ctx {
         int* d_err = nullptr;
         int* d_owned = nullptr;      // tensor-core path: owned columns / local offsets on the device
         long long* d_off = nullptr;
+        int* d_fb = nullptr;         // uncertified-item counters of this shard, by step parity
+        int setup_n = -1;            // order the maps / buffers were built for
     };
+    cudaGraphExec_t dist_graph = nullptr; // sharded LDLT step graph (look-ahead, NCCL captured)
+    long long dist_graph_launches = 0;
+    std::vector<const void*> dist_sig;    // buffers it was captured on
     int world = 1, rank = 0;
     bool virt = false;               // all `world` ranks emulated in this one context
     void* nccl_comm = nullptr;       // ncclComm_t (one rank per process)
@@ -655,7 +661,9 @@ void hk_destroy(hk_ctx* c) {
         if (s.d_err) cudaFree(s.d_err);
         if (s.d_owned) cudaFree(s.d_owned);
         if (s.d_off) cudaFree(s.d_off);
+        if (s.d_fb) cudaFree(s.d_fb);
     }
+    if (c->dist_graph) cudaGraphExecDestroy(c->dist_graph);
     if (c->nccl_comm) {
         void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         auto destroy = h ? (int (*)(void*))dlsym(h, "ncclCommDestroy") : nullptr;
@@ -1201,20 +1209,28 @@ int hk_peak_i8mma(int device, double* out) {
 // ====================================================================== multi-GPU
 //
 // Column-sharded LDLT: rank r owns columns {c : owner[c] == r} of
-// the boustrophedon map (ldlt.cpp:22-35).  Per step i (eager, one stream):
-//   U(i)     every rank: step-i update of its owned columns j >= i+1 (panel_i, B_i)
-//   STORE(i) owner(i): column i <- B_i (L in place)
-//   PUBLISH  owner(i+1): panel <- column i+1; ncclBroadcast(panel, root = owner(i+1))
-//            (ldlt.cpp:294-298 publish / 248 wait_complete)
-//   every rank: R_{i+1} = recip(panel[0]), B_{i+1} = panel * R_{i+1} — the
-//            identical deterministic kernels, so no second broadcast (B never
-//            travels; the reference's BroadcastPolicy chunking is moot).
-// Then all columns are gathered to rank 0 (ncclSend/Recv), which runs L^{-1},
-// the block and the eigensolve exactly as on one GPU.  Every op is correctly
-// rounded, so results are bit-identical for any world size.
-// Virtual mode runs all ranks' shards in one process on one GPU with the
-// broadcast / gather as device-to-device copies (tests the sharded kernels and
-// index maps on a single B200).
+// the boustrophedon map (ldlt.cpp:22-35), stored concatenated (rows j..N-1 of
+// each owned column j).  Every rank holds the pivot column i in a panel slot
+// (rows i..N-1) and B_i, both triple-buffered by i % 3.  The step loop is the
+// reference's depth-1 look-ahead (ldlt.cpp:271-331), recorded into one CUDA
+// graph on two streams of every rank:
+//   BULK (ctx stream)  [P(i)] U(i): step-i update of the owned columns >= i+2,
+//                      then StoreL(i) on the owner of i (D_i, L(:,i) in place)
+//   LA (high priority) P(i+1): the owner of column i+1 updates it with step i
+//                      straight into panel slot i+1 [after its U(i-1)];
+//                      ncclBroadcast(panel, root = owner(i+1)) (ldlt.cpp:294-298
+//                      publish / 248 wait_complete); every rank derives
+//                      R_{i+1} = recip(panel[0]) and B_{i+1} = panel * R_{i+1}
+//                      with the same deterministic kernels (B never travels, so
+//                      the reference's BroadcastPolicy chunking is moot).
+// The broadcast and the reciprocal chain of step i+1 thus overlap the bulk
+// update of step i on every GPU.  Slot (i+1) % 3 is rewritten only after
+// StoreL(i-2), its last reader.  After the loop all columns are gathered to
+// rank 0 (ncclSend/Recv), which runs L^{-1}, the block and the eigensolve as on
+// one GPU.  Every op is correctly rounded, so results are bit-identical for any
+// world size.  Virtual mode runs all ranks' shards in one process on one GPU
+// with the broadcast / gather as device-to-device copies (tests the sharded
+// kernels, index maps and the schedule on a single B200).
 
 namespace {
 
@@ -1260,7 +1276,13 @@ void nk(ncclResult_t r, const char* what) {
 
 using Shard = hk_ctx::Shard;
 
+MpArr slot3(const DevArr& a, int N, int L, int i) {
+    const long long off = (long long)(i % 3) * N;
+    return MpArr{a.d + off * L, a.m + off};
+}
+
 void shard_setup(hk_ctx* c, Shard& s, int N) {
+    if (s.setup_n == N) return; // the maps depend on (N, world) only
     s.owned.clear();
     s.loc.assign(size_t(N), -1);
     s.off.assign(1, 0);
@@ -1277,9 +1299,9 @@ void shard_setup(hk_ctx* c, Shard& s, int N) {
     }
     const long long tot = (long long)erow.size();
     s.S.ensure(tot > 0 ? tot : 1, c->L);
-    s.panel.ensure(N, c->L);
+    s.panel.ensure(3LL * N, c->L);
     s.R.ensure(N, c->L);
-    s.B.ensure(N, c->L);
+    s.B.ensure(3LL * N, c->L);
     if (s.d_erow) cudaFree(s.d_erow);
     if (s.d_ecol) cudaFree(s.d_ecol);
     ck(cudaMalloc(&s.d_erow, size_t(tot > 0 ? tot : 1) * sizeof(int)), "malloc erow");
@@ -1289,7 +1311,7 @@ void shard_setup(hk_ctx* c, Shard& s, int N) {
         ck(cudaMemcpyAsync(s.d_ecol, ecol.data(), size_t(tot) * sizeof(int), cudaMemcpyHostToDevice, c->st), "H2D ecol");
     }
     if (!s.d_err) ck(cudaMalloc(&s.d_err, sizeof(int)), "malloc err");
-    ck(cudaMemsetAsync(s.d_err, 0xff, sizeof(int), c->st), "memset err");
+    if (!s.d_fb) ck(cudaMalloc(&s.d_fb, 2 * sizeof(int)), "malloc fb");
     if (s.d_owned) cudaFree(s.d_owned);
     if (s.d_off) cudaFree(s.d_off);
     ck(cudaMalloc(&s.d_owned, (s.owned.size() + 1) * sizeof(int)), "malloc owned");
@@ -1300,75 +1322,122 @@ void shard_setup(hk_ctx* c, Shard& s, int N) {
     ck(cudaMemcpyAsync(s.d_off, s.off.data(), s.off.size() * sizeof(long long), cudaMemcpyHostToDevice, c->st),
        "H2D off");
     ck(cudaStreamSynchronize(c->st), "sync");
+    s.setup_n = N;
 }
 
-// Sharded step-i update of one rank's owned columns >= i+1 on the tensor cores
-// (mode 2 of the product kernel; same ops as ItemDTrailing, bit-identical).
-void enqueue_dist_tc(hk_ctx* c, Shard& s, int i) {
+// index of the first owned column >= j0 (owned columns of >= j0 form a suffix
+// of the local storage, starting at entry off[q])
+size_t first_owned(const Shard& s, int j0) {
+    return size_t(std::lower_bound(s.owned.begin(), s.owned.end(), j0) - s.owned.begin());
+}
+
+// U(i) on one shard: step-i update of its owned columns >= i+2 (the look-ahead
+// column i+1 is done by P(i+1)); IMAD warp FMAs or the tensor-core products
+// (mode 2 of the product kernel) + the certified rounding pass — the same ops
+// as ItemDTrailing, bit-identical.
+void dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st) {
     const int N = c->n, L = c->L;
-    size_t q = 0;
-    while (q < s.owned.size() && s.owned[q] < i + 1) ++q;
+    const size_t q = first_owned(s, i + 2);
     const int ncols = int(s.owned.size() - q);
     if (ncols <= 0) return;
     const long long e0 = s.off[q], n = s.off.back() - e0;
-    hk::TcBulkArgs a{s.S.view(), s.panel.view(), c->tc_A, c->tc_P, N, L, i, s.owned[q], 2, 0, 0, s.d_err};
+    const MpArr panel = slot3(s.panel, N, L, i), B = slot3(s.B, N, L, i);
+    if (!tc) {
+        launch(c, hk::ItemDTrailing{s.S.view(), panel, B, s.d_erow, s.d_ecol, L, i, e0, s.d_err}, n, ws_op_words(L),
+               st);
+        return;
+    }
+    hk::TcBulkArgs a{s.S.view(), panel, c->tc_A, c->tc_P, N, L, i, s.owned[q], 2, 0, 0, s.d_err};
     a.owned = s.d_owned;
     a.off = s.d_off;
     a.e0 = e0;
     a.first_loc = int(q);
-    tc_products(c, a, s.B.view(), unsigned(ncols), c->st);
-    int* cnt = c->tc_fb_count + 2;
-    ck(cudaMemsetAsync(cnt, 0, sizeof(int), c->st), "memset fb");
-    launch(c, hk::ItemTcRoundD{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err,
-                               cnt, c->tc_fb},
-           n, hk::tcround_words(L), c->st);
-    launch_fix(c, hk::FixD{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0}, c->st, cnt,
-               c->tc_fb_count + 3);
+    tc_products(c, a, B, unsigned(ncols), st);
+    // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
+    int* cnt = s.d_fb + (i & 1);
+    int* nxt = s.d_fb + ((i + 1) & 1);
+    launch(c, hk::ItemTcRoundD{s.S.view(), panel, B, s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err, cnt, c->tc_fb}, n,
+           hk::tcround_words(L), st);
+    launch_fix(c, hk::FixD{s.S.view(), panel, B, s.d_erow, s.d_ecol, L, i, e0}, st, cnt, nxt);
 }
 
-// entries of `s` belonging to owned columns >= j0 form a suffix of the local storage
-long long suffix_start(const Shard& s, int j0) {
-    size_t q = 0;
-    while (q < s.owned.size() && s.owned[q] < j0) ++q;
-    return s.off[q];
-}
-
-// make every shard's panel hold column `col` rows col..N-1 (N - col entries)
-void publish(hk_ctx* c, int col) {
+// make every shard's panel slot `col` hold column col (rows col..N-1): the
+// owner wrote it; broadcast from there (ldlt.cpp:294-298 publish / 248 wait)
+void dist_publish(hk_ctx* c, int col, cudaStream_t st) {
     const int N = c->n, L = c->L, root = c->owner[size_t(col)];
     const long long cnt = N - col;
     if (c->virt) {
-        Shard& o = c->shards[size_t(root)];
-        const long long src = o.off[size_t(o.loc[size_t(col)])];
-        launch(c, hk::ItemCopy{o.panel.view(), o.S.view(), 0, src, L}, cnt, 64);
+        const MpArr src = slot3(c->shards[size_t(root)].panel, N, L, col);
         for (auto& s : c->shards) {
             if (s.rank == root) continue;
-            ck(cudaMemcpyAsync(s.panel.d, o.panel.d, size_t(cnt) * L * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st),
+            const MpArr dst = slot3(s.panel, N, L, col);
+            ck(cudaMemcpyAsync(dst.d, src.d, size_t(cnt) * L * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st),
                "panel copy");
-            ck(cudaMemcpyAsync(s.panel.m, o.panel.m, size_t(cnt) * sizeof(Meta), cudaMemcpyDeviceToDevice, c->st),
+            ck(cudaMemcpyAsync(dst.m, src.m, size_t(cnt) * sizeof(Meta), cudaMemcpyDeviceToDevice, st),
                "panel meta copy");
         }
         return;
     }
-    Shard& s = c->shards[0];
-    if (s.rank == root) {
-        const long long src = s.off[size_t(s.loc[size_t(col)])];
-        launch(c, hk::ItemCopy{s.panel.view(), s.S.view(), 0, src, L}, cnt, 64);
-    }
+    const MpArr p = slot3(c->shards[0].panel, N, L, col);
     NcclApi* A = nccl_api();
     ncclComm_t comm = (ncclComm_t)c->nccl_comm;
     nk(A->GroupStart(), "group start");
-    nk(A->Broadcast(s.panel.d, s.panel.d, size_t(cnt) * L, ncclUint32, root, comm, c->st), "bcast limbs");
-    nk(A->Broadcast(s.panel.m, s.panel.m, size_t(cnt) * 2, ncclInt32, root, comm, c->st), "bcast meta");
+    nk(A->Broadcast(p.d, p.d, size_t(cnt) * L, ncclUint32, root, comm, st), "bcast limbs");
+    nk(A->Broadcast(p.m, p.m, size_t(cnt) * 2, ncclInt32, root, comm, st), "bcast meta");
     nk(A->GroupEnd(), "group end");
 }
 
-void derive(hk_ctx* c, Shard& s, int i) {
+// R_i = RNE(1/panel_i[0]) (pivot test) and B_i = panel_i * R_i, on every rank
+void dist_derive(hk_ctx* c, Shard& s, int i, cudaStream_t st) {
     const int N = c->n, L = c->L;
-    launch_cta(c, hk::CItemDRecip{s.panel.view(), s.R.view(), L, i, s.d_err}, 1, ws_cta_recip_words(L));
+    const MpArr p = slot3(s.panel, N, L, i);
+    launch_cta(c, hk::CItemDRecip{p, s.R.view(), L, i, s.d_err}, 1, ws_cta_recip_words(L), st);
     if (N - i - 1 > 0)
-        launch_cta(c, hk::CItemDMulB{s.panel.view(), s.R.view(), s.B.view(), L, i, s.d_err}, N - i - 1,
-                   ws_cta_words(L));
+        launch_cta(c, hk::CItemDMulB{p, s.R.view(), slot3(s.B, N, L, i), L, i, s.d_err}, N - i - 1, ws_cta_words(L),
+                   st);
+}
+
+void enqueue_dist_steps(hk_ctx* c, bool tc) {
+    const int N = c->n, L = c->L;
+    cudaStream_t bulk = c->st, la = c->st2;
+    ck(cudaEventRecord(c->evFork, bulk), "fork");
+    ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
+    // P(0): column 0 (owned by rank 0) is final as loaded
+    for (auto& s : c->shards)
+        if (c->owner[0] == s.rank)
+            launch(c, hk::ItemCopy{slot3(s.panel, N, L, 0), s.S.view(), 0, s.off[size_t(s.loc[0])], L}, N, 64, la);
+    dist_publish(c, 0, la);
+    for (auto& s : c->shards) dist_derive(c, s, 0, la);
+    ck(cudaEventRecord(c->evP[0], la), "evP");
+    for (int i = 0; i < N; ++i) {
+        ck(cudaStreamWaitEvent(bulk, c->evP[size_t(i)], 0), "wait P");
+        for (auto& s : c->shards) dist_bulk(c, s, i, tc, bulk);
+        ck(cudaEventRecord(c->evU[size_t(i)], bulk), "evU");
+        for (auto& s : c->shards)
+            if (c->owner[size_t(i)] == s.rank)
+                launch(c,
+                       hk::ItemDStoreL{s.S.view(), slot3(s.panel, N, L, i), slot3(s.B, N, L, i),
+                                       s.off[size_t(s.loc[size_t(i)])], L, i},
+                       N - i, 64, bulk);
+        ck(cudaEventRecord(c->evR[size_t(i)], bulk), "evR");
+        if (i + 1 >= N) continue;
+        // P(i+1): slot (i+1) % 3 was last read by U(i-2) / StoreL(i-2)
+        if (i >= 2) ck(cudaStreamWaitEvent(la, c->evR[size_t(i - 2)], 0), "wait R");
+        for (auto& s : c->shards) {
+            if (c->owner[size_t(i + 1)] != s.rank) continue;
+            if (i >= 1) ck(cudaStreamWaitEvent(la, c->evU[size_t(i - 1)], 0), "wait U"); // column i+1 after step i-1
+            launch_cta(c,
+                       hk::CItemDColUpd{s.S.view(), slot3(s.panel, N, L, i), slot3(s.B, N, L, i),
+                                        slot3(s.panel, N, L, i + 1), s.off[size_t(s.loc[size_t(i + 1)])], L, i,
+                                        s.d_err},
+                       N - i - 1, ws_cta_words(L), la);
+        }
+        dist_publish(c, i + 1, la);
+        for (auto& s : c->shards) dist_derive(c, s, i + 1, la);
+        ck(cudaEventRecord(c->evP[size_t(i + 1)], la), "evP");
+    }
+    ck(cudaEventRecord(c->evJoin, la), "join");
+    ck(cudaStreamWaitEvent(bulk, c->evJoin, 0), "join wait");
 }
 
 // gather all columns into the standard jagged S on rank 0 (+ R)
@@ -1430,42 +1499,49 @@ void gather_to_root(hk_ctx* c) {
 
 int dist_ldlt(hk_ctx* c) {
     const int N = c->n, L = c->L;
-    c->owner.assign(size_t(N), 0);
-    hk_assign_columns(N, c->world, c->owner.data());
-    for (auto& s : c->shards) shard_setup(c, s, N);
-    const int wo = ws_op_words(L);
-    ck(cudaEventRecord(c->ev[0], c->st), "event");
-    for (auto& s : c->shards) {
-        const long long tot = s.off.back();
-        launch(c, hk::ItemDInit{s.S.view(), c->mu.view(), s.d_erow, s.d_ecol, L}, tot, 64);
+    if ((int)c->owner.size() != N) {
+        c->owner.assign(size_t(N), 0);
+        hk_assign_columns(N, c->world, c->owner.data());
+        for (auto& s : c->shards) s.setup_n = -1;
     }
-    publish(c, 0);
-    for (auto& s : c->shards) derive(c, s, 0);
+    for (auto& s : c->shards) shard_setup(c, s, N);
     const bool tc = use_tc(c);
     if (tc) {
         long long most = 1;
         for (auto& s : c->shards) most = std::max(most, s.off.back());
-        ensure_tc_items(c, most);
+        ensure_tc_items(c, size_t(most));
     }
-    for (int i = 0; i < N; ++i) {
-        for (auto& s : c->shards) {
-            const long long e0 = suffix_start(s, i + 1), n = s.off.back() - e0;
-            if (tc)
-                enqueue_dist_tc(c, s, i);
-            else
-                launch(c,
-                       hk::ItemDTrailing{s.S.view(), s.panel.view(), s.B.view(), s.d_erow, s.d_ecol, L, i, e0, s.d_err},
-                       n, wo);
-            if (c->owner[size_t(i)] == s.rank && N - i - 1 > 0) {
-                const long long dst = s.off[size_t(s.loc[size_t(i)])] + 1;
-                launch(c, hk::ItemCopy{s.S.view(), s.B.view(), dst, i + 1, L}, N - i - 1, 64);
-            }
-        }
-        if (i + 1 < N) {
-            publish(c, i + 1);
-            for (auto& s : c->shards) derive(c, s, i + 1);
-        }
+    ensure_step_events(c, N);
+    c->bad_col = -1;
+    ck(cudaEventRecord(c->ev[0], c->st), "event");
+    for (auto& s : c->shards) {
+        ck(cudaMemsetAsync(s.d_err, 0xff, sizeof(int), c->st), "memset err");
+        ck(cudaMemsetAsync(s.d_fb, 0, 2 * sizeof(int), c->st), "memset fb");
+        launch(c, hk::ItemDInit{s.S.view(), c->mu.view(), s.d_erow, s.d_ecol, L}, s.off.back(), 64);
     }
+    // the step graph is valid for the buffers it was captured on
+    std::vector<const void*> sig{(const void*)(long long)N, (const void*)(long long)tc, c->tc_A, c->tc_P, c->tc_fb};
+    for (auto& s : c->shards)
+        for (const void* p : {(const void*)s.S.d, (const void*)s.panel.d, (const void*)s.B.d, (const void*)s.R.d,
+                              (const void*)s.d_err, (const void*)s.d_fb, (const void*)s.d_erow, (const void*)s.d_owned})
+            sig.push_back(p);
+    if (!c->dist_graph || sig != c->dist_sig) {
+        if (c->dist_graph) cudaGraphExecDestroy(c->dist_graph);
+        c->dist_graph = nullptr;
+        cudaGraph_t g;
+        const long long before = c->launches;
+        ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        enqueue_dist_steps(c, tc);
+        ck(cudaStreamEndCapture(c->st, &g), "end capture");
+        ck(cudaGraphInstantiateWithFlags(&c->dist_graph, g, cudaGraphInstantiateFlagUseNodePriority),
+           "graph instantiate");
+        cudaGraphDestroy(g);
+        c->dist_graph_launches = c->launches - before;
+        c->launches = before;
+        c->dist_sig = sig;
+    }
+    ck(cudaGraphLaunch(c->dist_graph, c->st), "graph launch");
+    c->launches += c->dist_graph_launches;
     // pivot errors: every rank computed the same reciprocals, so the flags agree
     int bad = -1;
     for (auto& s : c->shards) {

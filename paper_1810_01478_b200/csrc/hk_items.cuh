@@ -484,6 +484,38 @@ struct CItemDMulB { // sharded: B_i(k) = RNE(panel_i(k) R_i)
     }
 };
 
+// sharded look-ahead (ldlt.cpp:274-277 on the owner of column j = i+1): the
+// column's step-i update is written straight into the next panel, which is what
+// gets broadcast: pnext(r) = RNE(S(j+r, j) - panel_i(1) B_i(j+r)), r = k0 + t.
+// The local column keeps its step-(i-1) values until ItemDStoreL(j).
+struct CItemDColUpd {
+    MpArr S, panel, B, pnext;
+    long long offj; // local entry of (j, j)
+    int L, i;
+    const int* err;
+    int k0 = 0;
+    HK_DEV void operator()(long long t, uint32_t* ws) const {
+        if (*(volatile const int*)err >= 0) return;
+        const int j = i + 1, r = k0 + int(t);
+        const long long ec = offj + r;
+        cta_meta_store(pnext.m + r, cta_fms(S.limbs(ec, L), S.m[ec], panel.limbs(1, L), panel.m[1], B.limbs(j + r, L),
+                                            B.m[j + r], pnext.limbs(r, L), L, ctaws_carve(ws, L)));
+    }
+};
+
+// sharded StoreL of owned column j: S(j,j) <- panel_j(0) = D_j, S(j+t, j) <- B_j(j+t)
+struct ItemDStoreL {
+    MpArr S, panel, B;
+    long long offj;
+    int L, j;
+    HK_DEV void operator()(long long t, uint32_t*) const {
+        if (t == 0)
+            copy_entry(S.limbs(offj, L), S.m + offj, panel.limbs(0, L), panel.m, L);
+        else
+            copy_entry(S.limbs(offj + t, L), S.m + offj + t, B.limbs(j + t, L), B.m + j + t, L);
+    }
+};
+
 // L^{-1} step i with one CTA per item (the step is latency-bound: N sequential
 // steps of at most (N-i-1) min(m,i) independent FMAs) — same ops as ItemInvStep.
 struct CItemInvStep {

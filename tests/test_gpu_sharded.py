@@ -81,3 +81,33 @@ def test_virtual_sharded_precision_error(api):
         with pytest.raises(api.PrecisionError):
             ctx.decompose()
         assert ctx.bad_column == want
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_virtual_sharded_tensor_core_path(api, single, world, monkeypatch):
+    """The sharded look-ahead schedule with the tensor-core bulk products forced
+    (mode 2 of the product kernel + certified rounding), against the 1-GPU path."""
+    monkeypatch.setenv("HK_TC", "1")
+    for (beta, n, L, k), (mu, (r0, D0, X0, M0)) in single.items():
+        if L % 4:
+            continue
+        with api.Context(L, world=world, virtual=True) as ctx:
+            r1, D1, X1, M1 = results(ctx, mu, k)
+            # replay of the cached step graph gives the same factors
+            r2, D2, _, _ = results(ctx, mu, k)
+        assert D1 == D0 and X1 == X0 and M1 == M0, (beta, n, world)
+        assert D2 == D0 and r2.lambda_hi == r0.lambda_hi
+
+
+def test_nccl_world1_c2_digest(api):
+    """Real NCCL communicator (world 1): the broadcasts are captured into the step graph."""
+    from tests.test_gpu_parity import digest
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "model_c2.json")))
+    n, L, k = g["n"], g["p"] // 32, g["k"]
+    mu, _ = api.build_hankel((1, 1), n, L)
+    with api.Context(L, rank=0, world=1, nccl_id=api.nccl_unique_id()) as ctx:
+        for _ in range(2):
+            ctx.compute(mu, k)
+            assert digest(from_arr(ctx.D())) == g["D_sha256"]
+            assert digest(from_arr(ctx.block())) == g["block_sha256"]
