@@ -11,7 +11,7 @@ CSRC := paper_1810_01478_b200/csrc
 HDRS := $(wildcard $(CSRC)/*.cuh) include/hankel_b200.h
 LIB := paper_1810_01478_b200/libhankel_b200.so
 
-all: $(LIB) build/emu_mp
+all: $(LIB) build/emu_mp build/test_facade
 
 build:
 	mkdir -p build
@@ -27,6 +27,11 @@ $(LIB): build/hk_api.o build/host_math.o
 
 build/emu_mp: tools/emu_mp.cpp $(HDRS) $(CSRC)/warp_emu.h | build
 	$(CXX) -std=c++20 -O2 -pthread -Wall -Wno-unknown-pragmas -o $@ $<
+
+# C++ entry points (include/hankel_b200.hpp) over the C ABI, run as the reference's unit tests
+build/test_facade: tests/cpp/test_facade.cpp include/hankel_b200.hpp include/hankel_b200.h $(LIB) | build
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -Lpaper_1810_01478_b200 -lhankel_b200 \
+		-Wl,-rpath,'$$ORIGIN/../paper_1810_01478_b200'
 
 oracle:
 	$(MAKE) -C oracle

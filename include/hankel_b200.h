@@ -2,7 +2,7 @@
  *
  * The reference (/root/reference/proj, hankel-eig v0.1.0) is a C++ library with
  * no C ABI, plugin registry or FFI of its own; its entry points
- * are the C++ functions of proj/include/hankel/*.hpp.  This header is the thin
+ * are the C++ functions of proj/include/hankel/ *.hpp.  This header is the thin
  * C layer *below* those entry points: each call is annotated with the reference
  * function it replaces.  Plain pointers and sizes only; no torch, no C++ types.
  *
@@ -97,6 +97,16 @@ int hk_get_block(hk_ctx* ctx, uint32_t* limbs, int32_t* exps, int32_t* signs);
  * (jacobi.hpp:29-30; jacobi.cpp:74-103).  Host cyclic Jacobi in binary128;
  * lambda = lambda_hi + lambda_lo (double-double, ~32 digits). */
 int hk_smallest_eigs(hk_ctx* ctx, int s, double* lambda_hi, double* lambda_lo, double* trunc_err);
+
+/* Host-only eigensolves (no context, no device):
+ * hk_jacobi_eigenvalues — jacobi_eigenvalues(m, k, {tol_factor, max_sweeps})
+ *   (jacobi.hpp:16-17): ascending eigenvalues of a symmetric k x k binary64
+ *   block, cyclic Jacobi carried in binary128.  HK_ERR_RUNTIME on no convergence.
+ * hk_block_eigenvalues — smallest_eigs_of_H (jacobi.hpp:29-30) on a k x k MP
+ *   block given as host SoA (e.g. from hk_get_block): as hk_smallest_eigs. */
+int hk_jacobi_eigenvalues(const double* m, int k, double tol_factor, int max_sweeps, double* out);
+int hk_block_eigenvalues(int k, int limbs, const uint32_t* limbs_in, const int32_t* exps, const int32_t* signs, int s,
+                         double* lambda_hi, double* lambda_lo, double* trunc_err);
 
 /* Whole path, host buffers in, lambdas out: upload -> LDLT -> L^{-1} -> block
  * -> eigen.  Replaces hankel::compute (pipeline.hpp:50; pipeline.cpp:26-72)

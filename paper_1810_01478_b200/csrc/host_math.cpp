@@ -241,3 +241,27 @@ extern "C" int hk_block_eigs_impl(int k, int limbs, const uint32_t* l, const int
     }
     return 0;
 }
+
+// jacobi_eigenvalues (jacobi.hpp:16-17; jacobi.cpp:27-72) on a host binary64
+// block: the same cyclic sweep and stopping rule, carried in binary128, the
+// ascending eigenvalues rounded to binary64.  No device.
+extern "C" int hk_jacobi_eigenvalues(const double* m, int k, double tol_factor, int max_sweeps, double* out) {
+    if (!m || !out || k < 1 || max_sweeps < 0) return 3;
+    try {
+        std::vector<q128> M(size_t(k) * size_t(k));
+        for (size_t i = 0; i < M.size(); ++i) M[i] = m[i];
+        const std::vector<q128> ev = jacobi_q(M, k, tol_factor, max_sweeps);
+        for (int i = 0; i < k; ++i) out[i] = (double)ev[size_t(i)];
+    } catch (const std::exception&) {
+        return 1;
+    }
+    return 0;
+}
+
+// smallest_eigs_of_H (jacobi.hpp:29-30) on a host k x k MP block (no device).
+extern "C" int hk_block_eigenvalues(int k, int limbs, const uint32_t* l, const int32_t* e, const int32_t* sg, int s,
+                                    double* lam_hi, double* lam_lo, double* trunc) {
+    if (k < 1 || limbs < 1 || !l || !e || !sg || !lam_hi || !lam_lo || !trunc) return 3;
+    const char* why = "";
+    return hk_block_eigs_impl(k, limbs, l, e, sg, s, lam_hi, lam_lo, trunc, &why);
+}

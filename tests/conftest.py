@@ -32,3 +32,10 @@ def ref_driver():
             pytest.skip("oracle/_ref not built and /root/reference absent")
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True, capture_output=True)
     return path
+
+
+@pytest.fixture(scope="session")
+def facade_bin():
+    """tests/cpp/test_facade.cpp: the reference's unit cases through include/hankel_b200.hpp."""
+    _ensure_built("build/test_facade")
+    return os.path.join(ROOT, "build", "test_facade")
