@@ -104,6 +104,8 @@ struct hk_ctx {
     std::map<long long, cudaGraphExec_t> inv_graphs;         // L^{-1} step graphs keyed by (n, m)
     std::map<long long, long long> inv_graph_launches;
     const void* inv_bufs[3] = {nullptr, nullptr, nullptr};   // S, X, TC scratch they were captured on
+    const void* inv_flow_buf = nullptr;                      // dataflow flags they were captured on
+    bool inv_flow_mode = false;
     std::vector<uint32_t> h_limbs;
     std::vector<int32_t> h_e, h_s;
     // ---- tensor-core bulk products (large p): scratch of short products
@@ -115,6 +117,8 @@ struct hk_ctx {
     cudaEvent_t prof_mid = nullptr; // hk_profile_ldlt: recorded between TC products and rounding
     int* tc_fb_count = nullptr;   // uncertified items: [0] / [1] by step parity, [2] sharded path
     long long* tc_fb = nullptr;
+    int* flow_ready = nullptr;    // dataflow L^-1: per-entry flags + entry counter
+    long long flow_cap = 0;
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
     struct Shard {
         int rank = 0;
@@ -473,6 +477,131 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
         ck(cudaMemsetAsync(nxt, 0, sizeof(int), st), "memset fb");
 }
 
+// ---- L^{-1} as a dataflow (small p, IMAD path): one warp per entry X(j,c),
+// c < min(j, m), runs that entry's whole chain of the reference's row
+// elimination (inversion.cpp:93-102) in order:
+//     X(j,c) = -L(j,c);  for i = c+1 .. j-1:  X(j,c) = RNE(X(j,c) - L(j,i) X(i,c))
+// waiting for X(i,c) to be final (a per-entry flag, release/acquire at gpu
+// scope).  The per-entry order of the roundings is the reference's, so the
+// result is bit-identical to the N-step schedule; the N dependent launches
+// (latency-bound: a few hundred FMAs per step at C2) become one kernel whose
+// critical path is the c = 0 column, one FMA + one flag hand-off per row.
+// Entries are taken from a global counter in increasing (row-major) order, so
+// a warp only ever waits on entries already held by running warps: no
+// deadlock whatever the residency.
+struct InvFlowArgs {
+    MpArr S, X;
+    int N, L, m;
+    int* ready;                 // [N * m] 0 pending / 1 final (cleared per run)
+    unsigned long long* next;   // entry counter (cleared per run)
+    long long E;                // entries: sum_j min(j, m)
+    int ws_words;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// entry e -> (j, c): rows 1..m-1 hold j entries, rows >= m hold m
+__device__ __forceinline__ void inv_flow_decode(long long e, int m, int& j, int& c) {
+    const long long t0 = (long long)m * (m - 1) / 2;
+    if (e >= t0) {
+        j = m + int((e - t0) / m);
+        c = int((e - t0) % m);
+        return;
+    }
+    int jj = int((1.0 + sqrt(1.0 + 8.0 * double(e))) * 0.5);
+    while ((long long)jj * (jj - 1) / 2 > e) --jj;
+    while ((long long)(jj + 1) * jj / 2 <= e) ++jj;
+    j = jj;
+    c = int(e - (long long)jj * (jj - 1) / 2);
+}
+
+__global__ void __launch_bounds__(256) k_inv_flow(InvFlowArgs a) {
+    extern __shared__ __align__(16) uint32_t fsm_[];
+    const int L = a.L, m = a.m, N = a.N, ln = int(threadIdx.x & 31);
+    uint32_t* acc = fsm_ + (size_t)(threadIdx.x >> 5) * a.ws_words;
+    uint32_t* xs = acc + hk::align4(L);
+    uint32_t* ows = xs + hk::align4(L);
+    for (;;) {
+        unsigned long long e = 0;
+        if (ln == 0) e = atomicAdd(a.next, 1ull);
+        e = __shfl_sync(0xffffffffu, e, 0);
+        if ((long long)e >= a.E) return;
+        int j, c;
+        inv_flow_decode((long long)e, m, j, c);
+        const long long el = hk::tri_idx(j, c, N);
+        for (int q = ln; q < L; q += 32) acc[q] = a.S.limbs(el, L)[q];
+        Meta am = a.S.m[el];
+        am.sign = -am.sign;
+        __syncwarp();
+        for (int i = c + 1; i < j; ++i) {
+            const long long xi = (long long)i * m + c;
+            if (ln == 0)
+                while (ld_acquire_gpu(a.ready + xi) == 0) {
+                }
+            __syncwarp();
+            // L2 reads (X(i,c) was written by another SM during this kernel)
+            for (int q = ln; q < L; q += 32) xs[q] = __ldcg(a.X.limbs(xi, L) + q);
+            const int2 xm2 = __ldcg(reinterpret_cast<const int2*>(a.X.m + xi));
+            __syncwarp();
+            const long long eli = hk::tri_idx(j, i, N);
+            am = hk::warp_fms(acc, am, a.S.limbs(eli, L), a.S.m[eli], xs, Meta{xm2.x, xm2.y}, acc, L,
+                              hk::opws_carve(ows, L));
+        }
+        const long long xd = (long long)j * m + c;
+        for (int q = ln; q < L; q += 32) a.X.limbs(xd, L)[q] = acc[q];
+        if (ln == 0) a.X.m[xd] = am;
+        __threadfence();
+        __syncwarp();
+        if (ln == 0) st_release_gpu(a.ready + xd, 1);
+        __syncwarp();
+    }
+}
+
+int inv_flow_ws_words(int L) { return 2 * hk::align4(L) + hk::opws_words(L); }
+
+// flags + counter of the dataflow L^{-1}, (re)sized for n*m entries
+void ensure_inv_flow(hk_ctx* c, long long nm) {
+    if (c->flow_cap >= nm) return;
+    if (c->flow_ready) cudaFree(c->flow_ready);
+    c->flow_ready = nullptr;
+    ck(cudaMalloc(&c->flow_ready, size_t(nm) * sizeof(int) + 16), "cudaMalloc flow flags");
+    c->flow_cap = nm;
+}
+
+void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
+    const int N = c->n, L = c->L, m = c->m;
+    const long long nm = (long long)N * m;
+    long long E = 0;
+    for (int j = 1; j < N; ++j) E += j < m ? j : m;
+    unsigned long long* next = reinterpret_cast<unsigned long long*>(c->flow_ready + nm + (nm & 1));
+    ck(cudaMemsetAsync(c->flow_ready, 0, size_t(nm + (nm & 1)) * sizeof(int) + 8, st), "memset flow flags");
+    if (E == 0) return;
+    const int wsw = inv_flow_ws_words(L);
+    const size_t per_warp = size_t(wsw) * sizeof(uint32_t);
+    const int wpb = std::max(1, std::min(8, int((200 * 1024) / per_warp)));
+    static bool cfg = false;
+    if (!cfg) {
+        ck(cudaFuncSetAttribute(k_inv_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "flow attr");
+        ck(cudaFuncSetAttribute(k_inv_flow, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        cfg = true;
+    }
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow, 32 * wpb, per_warp * wpb), "occupancy");
+    const long long want = (E + wpb - 1) / wpb, cap = (long long)std::max(1, per_sm) * c->sm_count;
+    const unsigned grid = unsigned(std::max(1LL, std::min(want, cap)));
+    InvFlowArgs a{c->S.view(), c->X.view(), N, L, m, c->flow_ready, next, E, wsw};
+    k_inv_flow<<<grid, 32 * wpb, per_warp * wpb, st>>>(a);
+    ck(cudaGetLastError(), "flow launch");
+    ++c->launches;
+}
+
 // Tensor-core scratch for up to `items` products per step (+ the A operand of N rows).
 void ensure_tc_items(hk_ctx* c, size_t items) {
     if (c->tc_A_n < c->n) {
@@ -675,6 +804,7 @@ void hk_destroy(hk_ctx* c) {
     if (c->tc_fb_count) cudaFree(c->tc_fb_count);
     if (c->tc_A) cudaFree(c->tc_A);
     if (c->tc_gcarry) cudaFree(c->tc_gcarry);
+    if (c->flow_ready) cudaFree(c->flow_ready);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);
@@ -801,9 +931,16 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
         c->m = m;
         c->X.ensure((long long)N * m, L);
         const bool tc = use_tc_inv(c);
+        // small p: the dataflow kernel (HK_INV_FLOW=0 forces the N-step schedule)
+        const char* fe = getenv("HK_INV_FLOW");
+        const bool flow = !tc && (fe ? fe[0] == '1' : true);
+        if (flow) ensure_inv_flow(c, (long long)N * m);
         ensure_tc_scratch(c, m);
         // all N steps in one cached graph (invalidated when a buffer moves)
-        if (c->inv_bufs[0] != c->S.d || c->inv_bufs[1] != c->X.d || c->inv_bufs[2] != c->tc_P) {
+        if (c->inv_bufs[0] != c->S.d || c->inv_bufs[1] != c->X.d || c->inv_bufs[2] != c->tc_P ||
+            c->inv_flow_buf != c->flow_ready || c->inv_flow_mode != flow) {
+            c->inv_flow_buf = c->flow_ready;
+            c->inv_flow_mode = flow;
             for (auto& kv : c->inv_graphs) cudaGraphExecDestroy(kv.second);
             c->inv_graphs.clear();
             c->inv_bufs[0] = c->S.d;
@@ -818,7 +955,8 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
             ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
             if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), c->st), "memset fb counters");
             launch(c, hk::ItemInvInit{c->S.view(), c->X.view(), N, L, m}, (long long)N * m, 64);
-            for (int i = 0; i < N; ++i) {
+            if (flow) enqueue_inv_flow(c, c->st);
+            for (int i = 0; i < N && !flow; ++i) {
                 const int b = i < m ? i : m;
                 const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
                 if (tc) {
