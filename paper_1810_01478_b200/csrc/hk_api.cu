@@ -105,7 +105,7 @@ struct hk_ctx {
     std::map<long long, long long> inv_graph_launches;
     const void* inv_bufs[3] = {nullptr, nullptr, nullptr};   // S, X, TC scratch they were captured on
     const void* inv_flow_buf = nullptr;                      // dataflow flags they were captured on
-    bool inv_flow_mode = false;
+    bool inv_flow_mode = false;                              // dataflow kernel instead of N steps
     std::vector<uint32_t> h_limbs;
     std::vector<int32_t> h_e, h_s;
     // ---- tensor-core bulk products (large p): scratch of short products
@@ -477,7 +477,7 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
         ck(cudaMemsetAsync(nxt, 0, sizeof(int), st), "memset fb");
 }
 
-// ---- L^{-1} as a dataflow (small p, IMAD path): one warp per entry X(j,c),
+// ---- L^{-1} as a dataflow (small p, IMAD path): one CTA per entry X(j,c),
 // c < min(j, m), runs that entry's whole chain of the reference's row
 // elimination (inversion.cpp:93-102) in order:
 //     X(j,c) = -L(j,c);  for i = c+1 .. j-1:  X(j,c) = RNE(X(j,c) - L(j,i) X(i,c))
@@ -487,7 +487,7 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
 // (latency-bound: a few hundred FMAs per step at C2) become one kernel whose
 // critical path is the c = 0 column, one FMA + one flag hand-off per row.
 // Entries are taken from a global counter in increasing (row-major) order, so
-// a warp only ever waits on entries already held by running warps: no
+// a CTA only ever waits on entries already held by running CTAs: no
 // deadlock whatever the residency.
 struct InvFlowArgs {
     MpArr S, X;
@@ -496,6 +496,8 @@ struct InvFlowArgs {
     unsigned long long* next;   // entry counter (cleared per run)
     long long E;                // entries: sum_j min(j, m)
     int ws_words;
+    int fstride;                // flag stride in ints (a 128-byte line per flag: no false sharing)
+    int sleep_ns;               // poll back-off
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -522,56 +524,58 @@ __device__ __forceinline__ void inv_flow_decode(long long e, int m, int& j, int&
     c = int(e - (long long)jj * (jj - 1) / 2);
 }
 
-__global__ void __launch_bounds__(256) k_inv_flow(InvFlowArgs a) {
-    extern __shared__ __align__(16) uint32_t fsm_[];
-    const int L = a.L, m = a.m, N = a.N, ln = int(threadIdx.x & 31);
-    uint32_t* acc = fsm_ + (size_t)(threadIdx.x >> 5) * a.ws_words;
+// One CTA per entry (cta_fms: the products on all 8 warps — the per-entry chain
+// is latency-bound, a warp per entry measured 2x slower at C2).
+__global__ void __launch_bounds__(256) k_inv_flow_cta(InvFlowArgs a) {
+    extern __shared__ __align__(16) uint32_t fsm2_[];
+    __shared__ unsigned long long e_s;
+    const int L = a.L, m = a.m, N = a.N, tid = int(threadIdx.x);
+    uint32_t* acc = fsm2_;
     uint32_t* xs = acc + hk::align4(L);
-    uint32_t* ows = xs + hk::align4(L);
+    uint32_t* ws = xs + hk::align4(L);
     for (;;) {
-        unsigned long long e = 0;
-        if (ln == 0) e = atomicAdd(a.next, 1ull);
-        e = __shfl_sync(0xffffffffu, e, 0);
+        if (tid == 0) e_s = atomicAdd(a.next, 1ull);
+        __syncthreads();
+        const unsigned long long e = e_s;
+        __syncthreads();
         if ((long long)e >= a.E) return;
         int j, c;
         inv_flow_decode((long long)e, m, j, c);
         const long long el = hk::tri_idx(j, c, N);
-        for (int q = ln; q < L; q += 32) acc[q] = a.S.limbs(el, L)[q];
+        for (int q = tid; q < L; q += blockDim.x) acc[q] = a.S.limbs(el, L)[q];
         Meta am = a.S.m[el];
         am.sign = -am.sign;
-        __syncwarp();
+        __syncthreads();
         for (int i = c + 1; i < j; ++i) {
             const long long xi = (long long)i * m + c;
-            if (ln == 0)
-                while (ld_acquire_gpu(a.ready + xi) == 0) {
-                }
-            __syncwarp();
-            // L2 reads (X(i,c) was written by another SM during this kernel)
-            for (int q = ln; q < L; q += 32) xs[q] = __ldcg(a.X.limbs(xi, L) + q);
+            if (tid == 0)
+                while (ld_acquire_gpu(a.ready + xi * a.fstride) == 0) __nanosleep(a.sleep_ns);
+            __syncthreads();
+            for (int q = tid; q < L; q += blockDim.x) xs[q] = __ldcg(a.X.limbs(xi, L) + q);
             const int2 xm2 = __ldcg(reinterpret_cast<const int2*>(a.X.m + xi));
-            __syncwarp();
+            __syncthreads();
             const long long eli = hk::tri_idx(j, i, N);
-            am = hk::warp_fms(acc, am, a.S.limbs(eli, L), a.S.m[eli], xs, Meta{xm2.x, xm2.y}, acc, L,
-                              hk::opws_carve(ows, L));
+            am = hk::cta_fms(acc, am, a.S.limbs(eli, L), a.S.m[eli], xs, Meta{xm2.x, xm2.y}, acc, L,
+                             hk::ctaws_carve(ws, L));
+            __syncthreads();
         }
         const long long xd = (long long)j * m + c;
-        for (int q = ln; q < L; q += 32) a.X.limbs(xd, L)[q] = acc[q];
-        if (ln == 0) a.X.m[xd] = am;
+        for (int q = tid; q < L; q += blockDim.x) a.X.limbs(xd, L)[q] = acc[q];
+        if (tid == 0) a.X.m[xd] = am;
         __threadfence();
-        __syncwarp();
-        if (ln == 0) st_release_gpu(a.ready + xd, 1);
-        __syncwarp();
+        __syncthreads();
+        if (tid == 0) st_release_gpu(a.ready + xd * a.fstride, 1);
     }
 }
 
-int inv_flow_ws_words(int L) { return 2 * hk::align4(L) + hk::opws_words(L); }
+constexpr int kFlowStride = 32; // one 128-byte line per flag
 
 // flags + counter of the dataflow L^{-1}, (re)sized for n*m entries
 void ensure_inv_flow(hk_ctx* c, long long nm) {
     if (c->flow_cap >= nm) return;
     if (c->flow_ready) cudaFree(c->flow_ready);
     c->flow_ready = nullptr;
-    ck(cudaMalloc(&c->flow_ready, size_t(nm) * sizeof(int) + 16), "cudaMalloc flow flags");
+    ck(cudaMalloc(&c->flow_ready, size_t(nm) * kFlowStride * sizeof(int) + 16), "cudaMalloc flow flags");
     c->flow_cap = nm;
 }
 
@@ -580,24 +584,25 @@ void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
     const long long nm = (long long)N * m;
     long long E = 0;
     for (int j = 1; j < N; ++j) E += j < m ? j : m;
-    unsigned long long* next = reinterpret_cast<unsigned long long*>(c->flow_ready + nm + (nm & 1));
-    ck(cudaMemsetAsync(c->flow_ready, 0, size_t(nm + (nm & 1)) * sizeof(int) + 8, st), "memset flow flags");
+    unsigned long long* next = reinterpret_cast<unsigned long long*>(c->flow_ready + nm * kFlowStride);
+    ck(cudaMemsetAsync(c->flow_ready, 0, size_t(nm) * kFlowStride * sizeof(int) + 8, st), "memset flow flags");
     if (E == 0) return;
-    const int wsw = inv_flow_ws_words(L);
-    const size_t per_warp = size_t(wsw) * sizeof(uint32_t);
-    const int wpb = std::max(1, std::min(8, int((200 * 1024) / per_warp)));
-    static bool cfg = false;
-    if (!cfg) {
-        ck(cudaFuncSetAttribute(k_inv_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "flow attr");
-        ck(cudaFuncSetAttribute(k_inv_flow, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        cfg = true;
+    const char* sl = getenv("HK_FLOW_SLEEP");
+    const int sleep_ns = sl ? atoi(sl) : 100;
+    const int wsw = 2 * hk::align4(L) + hk::ctaws_words(L);
+    const size_t smem = size_t(wsw) * sizeof(uint32_t);
+    static bool cfg2 = false;
+    if (!cfg2) {
+        ck(cudaFuncSetAttribute(k_inv_flow_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+           "flow attr");
+        ck(cudaFuncSetAttribute(k_inv_flow_cta, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+        cfg2 = true;
     }
     int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow, 32 * wpb, per_warp * wpb), "occupancy");
-    const long long want = (E + wpb - 1) / wpb, cap = (long long)std::max(1, per_sm) * c->sm_count;
-    const unsigned grid = unsigned(std::max(1LL, std::min(want, cap)));
-    InvFlowArgs a{c->S.view(), c->X.view(), N, L, m, c->flow_ready, next, E, wsw};
-    k_inv_flow<<<grid, 32 * wpb, per_warp * wpb, st>>>(a);
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow_cta, 256, smem), "occupancy");
+    const unsigned grid = unsigned(std::max(1LL, std::min(E, (long long)std::max(1, per_sm) * c->sm_count)));
+    InvFlowArgs a{c->S.view(), c->X.view(), N, L, m, c->flow_ready, next, E, wsw, kFlowStride, sleep_ns};
+    k_inv_flow_cta<<<grid, 256, smem, st>>>(a);
     ck(cudaGetLastError(), "flow launch");
     ++c->launches;
 }
@@ -933,7 +938,7 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
         const bool tc = use_tc_inv(c);
         // small p: the dataflow kernel (HK_INV_FLOW=0 forces the N-step schedule)
         const char* fe = getenv("HK_INV_FLOW");
-        const bool flow = !tc && (fe ? fe[0] == '1' : true);
+        const bool flow = !tc && (fe ? fe[0] != '0' : true);
         if (flow) ensure_inv_flow(c, (long long)N * m);
         ensure_tc_scratch(c, m);
         // all N steps in one cached graph (invalidated when a buffer moves)

@@ -418,6 +418,7 @@ HK_DEV Meta cta_round_with_product(const Opd& X, const uint32_t* xd, const uint3
                                    uint32_t* out, int L, const CtaWs& w) {
     const int t0 = L > kGuardLimbs ? L - kGuardLimbs : 0;
     cta_stage_and_mul(xd, yd, L, w, t0);
+    HK_TRACE(10);
     if (t0 > 0) {
         RMeta r{0, 0};
         bool ok = false;
@@ -426,6 +427,7 @@ HK_DEV Meta cta_round_with_product(const Opd& X, const uint32_t* xd, const uint3
             r = warp_round_sum(X, Yh, w.op.G, out, L, lsbP + 32 * t0 + 46, &ok);
         }
         r = cta_bcast_meta(w, r, ok, &ok);
+        HK_TRACE(11);
         if (ok) return Meta{r.exp, r.sign};
         cta_stage_and_mul(xd, yd, L, w, 0); // exact product (the window overwrote A / Bp)
     }
@@ -482,11 +484,12 @@ struct FxRecipWs {
     RecipWs rw;       // A / Bp / P / Z (= z) / E (= |e|) double as the Newton buffers
     uint32_t *CS, *Z2;
     int* sh;
+    uint32_t* RS;     // 160 words: warp 0's operand staging for the register levels
 };
 
 // ~64 L + 1 KB bytes: fits the 227 KB per-CTA limit up to L = 3600 (p = 115200).
 HK_HD int ctarecipws_words(int L) {
-    return recipws_words(L) + cta_cs_words(2 * (L + 4)) + align4(L + 4) + 8;
+    return recipws_words(L) + cta_cs_words(2 * (L + 4)) + align4(L + 4) + 8 + 160;
 }
 
 HK_DEV FxRecipWs fxrecipws_carve(uint32_t* b, int L) {
@@ -498,21 +501,35 @@ HK_DEV FxRecipWs fxrecipws_carve(uint32_t* b, int L) {
     w.Z2 = b;
     b += align4(L + 4);
     w.sh = reinterpret_cast<int*>(b);
+    w.RS = b + 8;
     return w;
 }
 
-// Register product for the small Newton levels: lane s holds A[s] / B[s] (a, b
-// <= 32 limbs, a + b <= 64); returns C[lane] in lo and C[32 + lane] in hi.
-HK_DEV void reg_mul(uint32_t A, int a, uint32_t B, int b, uint32_t& lo, uint32_t& hi) {
+// Register product for the small Newton levels: lane s holds A[s] / B[s] (a <= 32,
+// b <= 32 limbs); returns C[lane] in lo and C[32 + lane] in hi.  The operands
+// are parked in the warp's 160-word buffer RS (A at 0..31, B at 64.. with 32 zero
+// words either side), so every column sum is a straight, unrolled run of
+// broadcast / consecutive shared loads and two independent MAC chains.
+HK_DEV void reg_mul(uint32_t A, int a, uint32_t B, int b, uint32_t& lo, uint32_t& hi, uint32_t* RS) {
     const int ln = lane();
+    uint32_t* SA = RS;
+    uint32_t* SB = RS + 32; // SB[32 + i] = B[i]
+    SA[ln] = ln < a ? A : 0u;
+    SB[ln] = 0u;
+    SB[32 + ln] = ln < b ? B : 0u;
+    SB[64 + ln] = 0u;
+    SB[96 + ln] = 0u;
+    wsync();
     uint32_t c0 = 0, c1 = 0, c2 = 0, d0 = 0, d1 = 0, d2 = 0;
-    for (int s = 0; s < a; ++s) {
-        const uint32_t as = shfl(A, s);
-        const int i0 = ln - s, i1 = ln + 32 - s;
-        const uint32_t b0 = shfl(B, i0 & 31), b1 = shfl(B, i1 & 31);
-        if (i0 >= 0 && i0 < b) mac96(c0, c1, c2, as, b0);
-        if (i1 >= 0 && i1 < b) mac96(d0, d1, d2, as, b1);
+    for (int s = 0; s < a; s += 4) { // SA is zero-padded to 32 words
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t as = SA[s + u];
+            mac96(c0, c1, c2, as, SB[32 + ln - (s + u)]);
+            mac96(d0, d1, d2, as, SB[64 + ln - (s + u)]);
+        }
     }
+    wsync(); // RS is rewritten by the next product
     CarryState cs;
     lo = carry_group(cs, c0, c1, c2);
     hi = carry_group(cs, d0, d1, d2);
@@ -561,19 +578,20 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
             Zr = ln == 0 ? uint32_t(lo) : ln == 1 ? uint32_t(lo >> 32) : ln == 2 ? uint32_t(mant >> (64 - sh)) : 0u;
         }
         int nfr = 2;
+        HK_TRACE(13);
         for (int r = 0; r < nreg; ++r) {
             const int nk = sched[ns - 1 - r];
             const int mn = nk >= L ? L : nk;
             const uint32_t mv = shfl(Mt, (L - mn - mbase + ln) & 31);
             const uint32_t mtop = ln < mn ? mv : 0u;
             uint32_t tlo, thi;
-            reg_mul(Zr, nfr + 1, mtop, mn, tlo, thi); // T = m_top * z
+            reg_mul(Zr, nfr + 1, mtop, mn, tlo, thi, w.RS); // T = m_top * z
             const int FT = mn + nfr;
             const bool neg = reg_limb(tlo, thi, FT) != 0u; // T >= 1  ->  e <= 0
             const uint32_t ev = reg_limb(tlo, thi, FT - nk + ln);
             const uint32_t E = ln < nk ? (neg ? ev : ~ev) : 0u;
             uint32_t dlo, dhi;
-            reg_mul(Zr, nfr + 1, E, nk, dlo, dhi); // D = z * |e|
+            reg_mul(Zr, nfr + 1, E, nk, dlo, dhi, w.RS); // D = z * |e|
             const int shl = nk - nfr;
             const uint32_t zs = shfl(Zr, (ln - shl) & 31);
             const uint32_t zv = (ln >= shl && ln - shl <= nfr) ? zs : 0u;
@@ -589,10 +607,12 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
             }
             Zr = ln <= nk ? r2 : 0u;
             nfr = nk;
+            HK_TRACE(12);
         }
         if (ln <= nfr + 1) w.rw.Z[ln] = ln <= nfr ? Zr : 0u;
     }
     cta_sync();
+    HK_TRACE(14);
     int nf = nreg ? sched[ns - nreg] : 2;
     uint32_t* Z = w.rw.Z;
     uint32_t* Zn = w.Z2;

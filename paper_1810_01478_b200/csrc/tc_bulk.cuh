@@ -374,6 +374,21 @@ HK_DEV void warp_stage_wait() {
     wsync();
 }
 
+// each chunk group of the product kernel started from carry 0: add the carries
+// (gc[z] out of group z) back in, from the first limb of group z + 1 upwards
+HK_DEV void join_group_carries(uint32_t* Ys, int L, int G, const uint64_t* gc) {
+    if (lane() == 0)
+        for (int z = 0; z + 1 < G; ++z) {
+            uint64_t v = gc[z];
+            for (int q = 64 * tc_group_first_chunk(L, G, z + 1); v != 0 && q < tc_scratch_limbs(L); ++q) {
+                v += Ys[q];
+                Ys[q] = uint32_t(v);
+                v >>= 32;
+            }
+        }
+    wsync();
+}
+
 struct ItemTcRound {
     MpArr S, B;
     const uint32_t* P;
@@ -460,18 +475,7 @@ struct ItemTcRoundInv {
         warp_stage16(Xs, o, L);
         warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
         warp_stage_wait();
-        if (G > 1) { // each chunk group started from carry 0: add the carries back in
-            if (lane() == 0)
-                for (int z = 0; z + 1 < G; ++z) {
-                    uint64_t v = gcarry[w * (G - 1) + z];
-                    for (int q = 64 * tc_group_first_chunk(L, G, z + 1); v != 0 && q < tc_scratch_limbs(L); ++q) {
-                        v += Ys[q];
-                        Ys[q] = uint32_t(v);
-                        v >>= 32;
-                    }
-                }
-            wsync();
-        }
+        if (G > 1) join_group_carries(Ys, L, G, gcarry + w * (G - 1));
         const Opd Xo{Xs, L, cm.exp - 32 * L, cm.sign, 32 * L};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
