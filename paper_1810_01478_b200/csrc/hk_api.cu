@@ -442,9 +442,11 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
     // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
     int* cnt = c->tc_fb_count + (i & 1);
     int* nxt = c->tc_fb_count + ((i + 1) & 1);
+    hk::ItemTcRound ri{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, cnt, c->tc_fb};
+    static const char* rd = getenv("HK_ROUND_DIRECT");
+    ri.direct = !rd || rd[0] == '1';
     if (!dev_skip("round"))
-        launch_cols(c, hk::ItemTcRound{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, cnt, c->tc_fb},
-                    ncols, ncols, hk::tcround_words(L), st);
+        launch_cols(c, ri, ncols, ncols, ri.direct ? hk::align4(L + 16) : hk::tcround_words(L), st);
     if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st, cnt, nxt);
 }
 

@@ -41,6 +41,7 @@
 struct uint4 {
     uint32_t x, y, z, w;
 };
+inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return uint4{x, y, z, w}; }
 namespace hk {
 HK_DEV int lane() { return hk_emu::cur_lane(); }
 HK_DEV uint32_t ballot(bool p) { return hk_emu::ballot(p); }
@@ -397,6 +398,32 @@ HK_DEV void read4(const uint32_t* d, int n, int off, int w0, uint32_t (&v)[4]) {
     for (int t = 0; t < 4; ++t) v[t] = fshr(x[t], x[t + 1], sh);
 }
 
+// read4 split in two: the five raw words (issued one iteration ahead by the
+// streaming passes, so global-memory operands are prefetched) and the shift.
+// b0: the warp's first window word this iteration (w0 = b0 + 4 lane): when the
+// whole warp's range is inside [0, n) the loads go unchecked (the interior
+// iterations; the bounds tests were the rounding pass's largest ALU cost).
+HK_DEV void load5(const uint32_t* d, int n, int off, int b0, int w0, uint32_t (&x)[5]) {
+    const int q = (off >> 5) + w0;
+    const int lo = (off >> 5) + b0;
+    if (lo >= 0 && lo + 128 < n) {
+#pragma unroll
+        for (int t = 0; t < 5; ++t) x[t] = d[q + t];
+        return;
+    }
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        const int idx = q + t;
+        x[t] = (idx >= 0 && idx < n) ? d[idx] : 0u;
+    }
+}
+HK_DEV bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+HK_DEV void shift4(const uint32_t (&x)[5], int off, uint32_t (&v)[4]) {
+    const int sh = off & 31;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = fshr(x[t], x[t + 1], sh);
+}
+
 // Carry-lookahead over lanes holding 4-limb groups: g = carry (or borrow) out
 // of the lane's own chain, p = a carry (borrow) into the lane would pass through
 // all four limbs.  Returns the carry into this lane; cio: carry into lane 0 in,
@@ -519,19 +546,30 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
     const int offB = (base - 32) - Big.lsb, offS = (base - 32) - Small.lsb;
     const int nS = small_live ? Small.n : 0;
     uint32_t c = 0;
+    uint32_t xb[5], xs[5];
+    load5(Big.d, Big.n, offB, 0, 4 * ln, xb);
+    load5(Small.d, nS, offS, 0, 4 * ln, xs);
+    const bool g16 = aligned16(G);
     for (int b0 = 0; b0 < nw; b0 += 128) {
         const int w0 = b0 + 4 * ln;
+        const bool edge = b0 == 0 || b0 + 128 > W; // warp-uniform: limb 0 or limbs past W in range
         uint32_t vb[4], vs[4], r[4];
-        read4(Big.d, Big.n, offB, w0, vb);
-        read4(Small.d, nS, offS, w0, vs);
+        shift4(xb, offB, vb);
+        shift4(xs, offS, vs);
+        if (b0 + 128 < nw) { // the next iteration's words, in flight during this one
+            load5(Big.d, Big.n, offB, b0 + 128, w0 + 128, xb);
+            load5(Small.d, nS, offS, b0 + 128, w0 + 128, xs);
+        }
+        if (edge) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int w = w0 + t;
-            if (w == 0) {
-                vb[t] = 0u;
-                vs[t] = sticky ? 1u : 0u;
-            } else if (w > W) {
-                vb[t] = vs[t] = 0u;
+            for (int t = 0; t < 4; ++t) {
+                const int w = w0 + t;
+                if (w == 0) {
+                    vb[t] = 0u;
+                    vs[t] = sticky ? 1u : 0u;
+                } else if (w > W) {
+                    vb[t] = vs[t] = 0u;
+                }
             }
         }
         if (eff_sub) {
@@ -555,9 +593,13 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
             const uint32_t ci = lane_carry_in(cr != 0u, (r[0] & r[1] & r[2] & r[3]) == 0xffffffffu, c);
             ripple_add4(r, ci);
         }
+        if (!edge && g16) {
+            *reinterpret_cast<uint4*>(G + w0) = make_uint4(r[0], r[1], r[2], r[3]);
+        } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (w0 + t <= W) G[w0 + t] = r[t];
+            for (int t = 0; t < 4; ++t)
+                if (w0 + t <= W) G[w0 + t] = r[t];
+        }
     }
     int sign = Big.sign;
     if (eff_sub && c) { // negative: two's-complement negate
@@ -627,21 +669,30 @@ HK_DEV RMeta warp_round_sum(const Opd& Xin, const Opd& Yin, uint32_t* G, uint32_
     wsync(); // every read of X / Y done before `out` (which may alias X or Y) is written
     uint32_t cc = inc ? 1u : 0u;
     bool ovf = false;
+    const bool o16 = aligned16(out);
     for (int b0 = 0; b0 <= nout; b0 += 128) {
         const int j0 = b0 + 4 * ln;
-        uint32_t r[4];
-        read4(G, nw, lsbpos, j0, r);
+        const bool inner = b0 + 128 <= nout - 1; // warp-uniform: every j < nout, none == nout
+        uint32_t x[5], r[4];
+        load5(G, nw, lsbpos, b0, j0, x);
+        shift4(x, lsbpos, r);
+        if (!inner) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (j0 + t >= nout) r[t] = 0u;
+            for (int t = 0; t < 4; ++t)
+                if (j0 + t >= nout) r[t] = 0u;
+        }
         const uint32_t ci = lane_carry_in(false, (r[0] & r[1] & r[2] & r[3]) == 0xffffffffu, cc);
         ripple_add4(r, ci);
         bool o = false;
+        if (inner && o16) {
+            *reinterpret_cast<uint4*>(out + j0) = make_uint4(r[0], r[1], r[2], r[3]);
+        } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int j = j0 + t;
-            if (j < nout) out[j] = r[t];
-            if (j == nout) o = r[t] != 0u;
+            for (int t = 0; t < 4; ++t) {
+                const int j = j0 + t;
+                if (j < nout) out[j] = r[t];
+                if (j == nout) o = r[t] != 0u;
+            }
         }
         ovf |= ballot(o) != 0u;
     }

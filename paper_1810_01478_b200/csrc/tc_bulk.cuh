@@ -396,6 +396,7 @@ struct ItemTcRound {
     const int* err;
     int* fb_count;
     long long* fb;
+    int direct = 0; // 1: operands read in place from global memory, only the window in shared memory
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         const int n2 = N - jfirst;
         int jj, kk;
@@ -416,16 +417,24 @@ struct ItemTcRound {
         if (sp == 0) return; // x or y zero: RNE(c - 0) = c, nothing to write
         const int t0 = L - kTcGuard;
         const int lsbP = xm.exp + ym.exp - 64 * L;
-        uint32_t* Xs = ws;
-        uint32_t* Ys = ws + align4(L);
-        warp_stage16(Xs, c, L);
-        warp_stage16(Ys, P + w * (long long)tc_scratch_limbs(L), tc_scratch_limbs(L));
-        warp_stage_wait();
+        const uint32_t* Pw = P + w * (long long)tc_scratch_limbs(L);
+        const uint32_t* Xs = c;
+        const uint32_t* Ys = Pw;
+        uint32_t* Gw = ws;
+        if (!direct) {
+            uint32_t* xs = ws;
+            uint32_t* ys = ws + align4(L);
+            warp_stage16(xs, c, L);
+            warp_stage16(ys, Pw, tc_scratch_limbs(L));
+            warp_stage_wait();
+            Xs = xs;
+            Ys = ys;
+            Gw = ys + align4(L + kTcGuard);
+        }
         const Opd X{Xs, L, cm.exp - 32 * L, cm.sign, 32 * L};
         const Opd Y{Ys, tc_scratch_limbs(L), lsbP + 32 * t0, sp};
         bool ok = false;
-        const RMeta rr = warp_round_sum(X, Y, Ys + align4(L + kTcGuard), c, L,
-                                             lsbP + 32 * t0 + 46, &ok);
+        const RMeta rr = warp_round_sum(X, Y, Gw, c, L, lsbP + 32 * t0 + 46, &ok);
         if (lane() == 0) {
             if (ok) {
                 S.m[ec] = Meta{rr.exp, rr.sign};
