@@ -375,6 +375,8 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
         ck(cudaFuncSetAttribute(hk::k_tc_prep, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         configured = true;
     }
+    static const char* dv = getenv("HK_DEV_TCB"); // dev what-if (tools only): bits of TcBulkArgs::dev
+    a.dev = dv ? atoi(dv) : 0;
     const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
     const long long nprep = prep.count();
     hk::k_tc_prep<<<unsigned((nprep + 255) / 256), 256, 0, st>>>(prep, nprep);

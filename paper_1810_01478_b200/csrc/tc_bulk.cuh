@@ -141,6 +141,7 @@ struct TcBulkArgs {
     const long long* off = nullptr;
     long long e0 = 0;
     int first_loc = 0;
+    int dev = 0; // dev what-if knobs (results wrong; tools only): 1 no window build, 2 no TMA of A, 4 no drain, 8 no P stores
 };
 
 #if !defined(HK_WARP_EMU)
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                     pcn = nblk_of(pc);
                 }
             };
-            while (qt < Q && qt < kTcStages - 1) issue_tma();
+            while (qt < Q && qt < kTcStages - 1 && !(a.dev & 2)) issue_tma();
             int q = 0;
             for (int c = c_lo; c < nch; ++c) {
                 const int cl = c - c_lo; // local chunk index (accumulator / phase)
@@ -251,8 +252,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                 const int nblk = nblk_of(c);
                 for (int b = 0; b < nblk; ++b, ++q) {
                     const int s = q % kTcStages;
-                    tc::mbar_wait(&full[s], uint32_t(q / kTcStages) & 1u);
-                    if (ewin) tc::mbar_wait(&efull[s], uint32_t(q / kTcStages) & 1u);
+                    if (!(a.dev & 2)) tc::mbar_wait(&full[s], uint32_t(q / kTcStages) & 1u);
+                    if (ewin && !(a.dev & 1)) tc::mbar_wait(&efull[s], uint32_t(q / kTcStages) & 1u);
                     tc::fence_after();
 #pragma unroll
                     for (int sub = 0; sub < kTcKB; ++sub) {
@@ -266,14 +267,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                         }
                     }
                     tc::commit(&empty[s]);
-                    if (qt < Q) issue_tma(); // refills the slot block q - 1 used
+                    if (qt < Q && !(a.dev & 2)) issue_tma(); // refills the slot block q - 1 used
                 }
                 tc::commit(&accF[ab]);
             }
         }
         __syncwarp();
     } else if (warp < 4) {
-        if (ewin) { // warps 1-3: the x window of every block, in issue order
+        if (ewin && !(a.dev & 1)) { // warps 1-3: the x window of every block, in issue order
             const int bt = tid - 32;
             int q = 0;
             for (int c = c_lo; c < nch; ++c) {
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
             const int ab = cl % nacc;
             tc::mbar_wait(&accF[ab], uint32_t(cl / nacc) & 1u);
             tc::fence_after();
-            for (int c32 = 0; c32 < kTcN; c32 += 32) {
+            for (int c32 = 0; c32 < kTcN && !(a.dev & 4); c32 += 32) {
                 uint32_t v[32];
                 tc::tmem_ld32(lane_base + uint32_t(ab * kTcN + c32), v);
                 tc::tmem_ld_wait();
@@ -320,8 +321,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                     carry = s >> 32;
                 }
                 const int lq = c * 64 + (c32 >> 2); // limb index relative to L - 8 (multiple of 8)
-                if (row_ok) {
-                    if (lq + 8 <= tc_scratch_limbs(L)) {
+                if (row_ok && !(a.dev & 8)) {
+                    if (lq + 8 <= tc_scratch_limbs(L) && (L & 7) == 0) {
+                        tc::st_global_v8(Pout + lq, o); // item stride (L+8) limbs: 32-byte aligned
+                    } else if (lq + 8 <= tc_scratch_limbs(L)) {
                         reinterpret_cast<uint4*>(Pout + lq)[0] = make_uint4(o[0], o[1], o[2], o[3]);
                         reinterpret_cast<uint4*>(Pout + lq)[1] = make_uint4(o[4], o[5], o[6], o[7]);
                     } else {
