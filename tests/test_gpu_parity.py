@@ -82,7 +82,9 @@ def run_path(api, beta, n, L, k):
 
 @pytest.mark.parametrize("beta,n,L,k", [((1, 2), 1, 2, 1), ((1, 2), 2, 4, 2), ((1, 2), 8, 4, 4), ((1, 1), 24, 6, 8),
                                         ((1, 3), 20, 24, 12), ((1, 2), 64, 96, 8)])
-def test_path_bit_exact_vs_model(api, beta, n, L, k):
+@pytest.mark.parametrize("inv_flow", ["1", "0"])  # small-p L^-1: dataflow kernel / N-step schedule
+def test_path_bit_exact_vs_model(api, beta, n, L, k, inv_flow, monkeypatch):
+    monkeypatch.setenv("HK_INV_FLOW", inv_flow)
     p = 32 * L
     mu = [R.moment_integer(beta, j) for j in range(2 * n - 1)]
     D, Lf, Rr = F.ldlt(mu, n, p)
