@@ -602,11 +602,13 @@ void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
         ck(cudaFuncSetAttribute(k_inv_flow_cta, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         cfg2 = true;
     }
+    static const char* tb = getenv("HK_FLOW_THREADS"); // dev sweep
+    const int threads = tb ? atoi(tb) : 128; // 4 warps per entry: C2 invL 3.67 (256) -> 3.24 ms
     int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow_cta, 256, smem), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow_cta, threads, smem), "occupancy");
     const unsigned grid = unsigned(std::max(1LL, std::min(E, (long long)std::max(1, per_sm) * c->sm_count)));
     InvFlowArgs a{c->S.view(), c->X.view(), N, L, m, c->flow_ready, next, E, wsw, kFlowStride, sleep_ns};
-    k_inv_flow_cta<<<grid, 256, smem, st>>>(a);
+    k_inv_flow_cta<<<grid, threads, smem, st>>>(a);
     ck(cudaGetLastError(), "flow launch");
     ++c->launches;
 }

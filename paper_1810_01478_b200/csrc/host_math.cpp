@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <exception>
+#include <thread>
 #include <vector>
 
 namespace hk_host {
@@ -214,14 +216,32 @@ extern "C" int hk_block_eigs_impl(int k, int limbs, const uint32_t* l, const int
         std::vector<q128> M(size_t(k) * size_t(k));
         for (int i = 0; i < k * k; ++i) M[size_t(i)] = mpf_to_q(l + size_t(i) * limbs, limbs, e[i], sg[i]);
         const double tol = 1e-32;
-        const std::vector<q128> mu = jacobi_q(M, k, tol, 100);
+        // the k and (k-1) blocks are independent solves: the second on its own thread
+        // (software binary128 is slow: ~0.2 ms per 8x8 solve)
         std::vector<q128> mum;
+        std::exception_ptr err2;
+        std::thread t2;
         if (k > 1) {
             std::vector<q128> Mm(size_t(k - 1) * size_t(k - 1));
             for (int i = 0; i < k - 1; ++i)
                 for (int j = 0; j < k - 1; ++j) Mm[size_t(i) * size_t(k - 1) + size_t(j)] = M[size_t(i) * size_t(k) + size_t(j)];
-            mum = jacobi_q(Mm, k - 1, tol, 100);
+            t2 = std::thread([&, Mm = std::move(Mm)] {
+                try {
+                    mum = jacobi_q(Mm, k - 1, tol, 100);
+                } catch (...) {
+                    err2 = std::current_exception();
+                }
+            });
         }
+        std::vector<q128> mu;
+        try {
+            mu = jacobi_q(M, k, tol, 100);
+        } catch (...) {
+            if (t2.joinable()) t2.join();
+            throw;
+        }
+        if (t2.joinable()) t2.join();
+        if (err2) std::rethrow_exception(err2);
         for (int i = 1; i <= s; ++i) {
             const q128 mi = mu[size_t(k - i)];
             if (mi <= 0) {
