@@ -603,7 +603,7 @@ void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
         cfg2 = true;
     }
     static const char* tb = getenv("HK_FLOW_THREADS"); // dev sweep
-    const int threads = tb ? atoi(tb) : 128; // 4 warps per entry: C2 invL 3.67 (256) -> 3.24 ms
+    const int threads = tb ? atoi(tb) : 96; // 3 warps per entry: C2 invL 3.67 (256) / 3.14 (128) / 2.99 ms
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow_cta, threads, smem), "occupancy");
     const unsigned grid = unsigned(std::max(1LL, std::min(E, (long long)std::max(1, per_sm) * c->sm_count)));
