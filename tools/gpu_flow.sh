@@ -1,2 +1,2 @@
 #!/bin/bash
-for t in 128 192 256; do echo "cta threads=$t"; HK_CTA_THREADS=$t timeout 200 python tools/gpu_timing.py c2 2>/dev/null | head -1; HK_CTA_THREADS=$t timeout 200 python tools/gpu_timing.py c3 2>/dev/null | head -1; done
+for d in 1 2; do echo "depth=$d"; for c in c1 c2 c3; do HK_LA_DEPTH=$d timeout 300 python tools/gpu_timing.py $c 2>/dev/null | head -1; done; done
