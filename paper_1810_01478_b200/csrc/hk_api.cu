@@ -83,9 +83,10 @@ struct hk_ctx {
     cudaStream_t st = nullptr;  // bulk / default stream of the context
     cudaStream_t st2 = nullptr; // high-priority look-ahead stream
     cudaStream_t st3 = nullptr; // high-priority: off-diagonal part of the look-ahead column
+    cudaStream_t st4 = nullptr; // side stream: StoreL (L in place), off both critical streams
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
     std::vector<cudaEvent_t> evP, evR, evU, evD, evO, evC, evB1; // per-step dependencies (graph capture)
-    cudaEvent_t evJoin2 = nullptr;
+    cudaEvent_t evJoin2 = nullptr, evJoin3 = nullptr;
     DevArr mu, S, R, B, X, Y, T, T2, M;
     int* d_err = nullptr;
     std::string err;
@@ -346,6 +347,13 @@ bool dev_skip(const char* what) {
     return e && strstr(e, what);
 }
 
+// Tests only (HK_TC_FORCE_FIX=1): the rounding passes hand every 7th certified
+// item to the exact fix-up kernel too, so that path is exercised and checked.
+bool force_fix() {
+    const char* e = getenv("HK_TC_FORCE_FIX");
+    return e && e[0] == '1';
+}
+
 bool use_tc_inv(const hk_ctx* c) {
     if (!use_tc(c)) return false;
     if (getenv("HK_TC")) return true;
@@ -447,6 +455,7 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
     hk::ItemTcRound ri{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, cnt, c->tc_fb};
     static const char* rd = getenv("HK_ROUND_DIRECT");
     ri.direct = !rd || rd[0] == '1';
+    ri.force_fb = force_fix();
     if (!dev_skip("round"))
         launch_cols(c, ri, ncols, ncols, ri.direct ? hk::align4(L + 16) : hk::tcround_words(L), st);
     if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st, cnt, nxt);
@@ -474,6 +483,7 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
     hk::ItemTcRoundInv ri{c->S.view(), c->X.view(), c->tc_P, N, L, m, i, b, cnt, c->tc_fb};
     ri.G = G;
     ri.gcarry = c->tc_gcarry;
+    ri.force_fb = force_fix();
     launch(c, ri, items, hk::tcround_words(L), st);
     if (b > 0)
         launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st, cnt, nxt);
@@ -655,10 +665,11 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     std::vector<cudaEvent_t>& evO = c->evO;
     std::vector<cudaEvent_t>& evC = c->evC;
     std::vector<cudaEvent_t>& evB1 = c->evB1;
-    cudaStream_t la2 = c->st3;
+    cudaStream_t la2 = c->st3, side = c->st4;
     if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), bulk), "memset fb counters");
     ck(cudaEventRecord(c->evFork, bulk), "fork");
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
+    ck(cudaStreamWaitEvent(side, c->evFork, 0), "fork wait side");
     const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
     (void)wr;
     launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, 0, c->d_err}, 1, wcr, la);
@@ -671,9 +682,13 @@ void enqueue_ldlt_steps(hk_ctx* c) {
         enqueue_bulk(c, i, i + 2, bulk);
         ck(cudaEventRecord(evU[i], bulk), "evU");
         if (i >= 1) {
+            // StoreL(i-1) on the side stream: column i-1 was last read by U(i-1)
+            // (x operands) and P(i) (the look-ahead update of column i)
+            ck(cudaStreamWaitEvent(side, evU[i - 1], 0), "wait U side");
+            ck(cudaStreamWaitEvent(side, evP[i], 0), "wait P side");
             if (!dev_skip("storel"))
-                launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i - 1), N, L, i - 1}, N - i, 64, bulk);
-            ck(cudaEventRecord(evR[i - 1], bulk), "evR");
+                launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i - 1), N, L, i - 1}, N - i, 64, side);
+            ck(cudaEventRecord(evR[i - 1], side), "evR");
         }
         if (i + 1 < N) {
             // P(i+1): the diagonal entry -> reciprocal on `la`, the rest of the
@@ -713,6 +728,8 @@ void enqueue_ldlt_steps(hk_ctx* c) {
         ck(cudaEventRecord(c->evJoin2, la2), "join2");
         ck(cudaStreamWaitEvent(bulk, c->evJoin2, 0), "join2 wait");
     }
+    ck(cudaEventRecord(c->evJoin3, side), "join3");
+    ck(cudaStreamWaitEvent(bulk, c->evJoin3, 0), "join3 wait");
 }
 
 void ensure_step_events(hk_ctx* c, int N) {
@@ -775,6 +792,8 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->evJoin2, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->evJoin3, cudaEventDisableTiming), "event");
+        ck(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking), "cudaStreamCreate side");
         ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
         ck(cudaEventCreate(&c->ev[0]), "event");
         ck(cudaEventCreate(&c->ev[1]), "event");
@@ -826,6 +845,8 @@ void hk_destroy(hk_ctx* c) {
     for (auto e : c->evC) cudaEventDestroy(e);
     for (auto e : c->evB1) cudaEventDestroy(e);
     if (c->evJoin2) cudaEventDestroy(c->evJoin2);
+    if (c->evJoin3) cudaEventDestroy(c->evJoin3);
+    if (c->st4) cudaStreamDestroy(c->st4);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
     if (c->st2) cudaStreamDestroy(c->st2);
@@ -1505,7 +1526,9 @@ void dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st) {
     // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
     int* cnt = s.d_fb + (i & 1);
     int* nxt = s.d_fb + ((i + 1) & 1);
-    launch(c, hk::ItemTcRoundD{s.S.view(), panel, B, s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err, cnt, c->tc_fb}, n,
+    hk::ItemTcRoundD rd{s.S.view(), panel, B, s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err, cnt, c->tc_fb};
+    rd.force_fb = force_fix();
+    launch(c, rd, n,
            hk::tcround_words(L), st);
     launch_fix(c, hk::FixD{s.S.view(), panel, B, s.d_erow, s.d_ecol, L, i, e0}, st, cnt, nxt);
 }

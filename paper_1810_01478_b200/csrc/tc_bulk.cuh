@@ -377,6 +377,18 @@ HK_DEV void warp_stage_wait() {
     wsync();
 }
 
+// tests (HK_TC_FORCE_FIX): the item goes to the exact fix-up list without rounding
+HK_DEV void force_to_fix(long long w, int* fb_count, long long* fb) {
+    if (lane() == 0) {
+#if defined(HK_WARP_EMU)
+        fb[(*fb_count)++] = w;
+#else
+        fb[atomicAdd(fb_count, 1)] = w;
+#endif
+    }
+    wsync();
+}
+
 // each chunk group of the product kernel started from carry 0: add the carries
 // (gc[z] out of group z) back in, from the first limb of group z + 1 upwards
 HK_DEV void join_group_carries(uint32_t* Ys, int L, int G, const uint64_t* gc) {
@@ -399,6 +411,7 @@ struct ItemTcRound {
     const int* err;
     int* fb_count;
     long long* fb;
+    int force_fb = 0; // tests: every 7th certified item is sent to the exact fix-up anyway (HK_TC_FORCE_FIX)
     int direct = 0; // 1: operands read in place from global memory, only the window in shared memory
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         const int n2 = N - jfirst;
@@ -418,6 +431,7 @@ struct ItemTcRound {
         uint32_t* c = S.limbs(ec, L);
         const int sp = -(xm.sign * ym.sign);
         if (sp == 0) return; // x or y zero: RNE(c - 0) = c, nothing to write
+        if (force_fb && w % 7 == 3) return force_to_fix(w, fb_count, fb);
         const int t0 = L - kTcGuard;
         const int lsbP = xm.exp + ym.exp - 64 * L;
         const uint32_t* Pw = P + w * (long long)tc_scratch_limbs(L);
@@ -461,6 +475,7 @@ struct ItemTcRoundInv {
     int N, L, m, i, b;
     int* fb_count;
     long long* fb;
+    int force_fb = 0; // tests: every 7th certified item is sent to the exact fix-up anyway (HK_TC_FORCE_FIX)
     int G = 1;                       // chunk groups of the product kernel
     const uint64_t* gcarry = nullptr; // their carries, added here
     HK_DEV void operator()(long long w, uint32_t* ws) const {
@@ -479,6 +494,7 @@ struct ItemTcRoundInv {
         const Meta cm = X.m[xc], xm = S.m[el], ym = X.m[xi];
         const int sp = -(xm.sign * ym.sign);
         if (sp == 0) return;
+        if (force_fb && w % 7 == 3) return force_to_fix(w, fb_count, fb);
         uint32_t* o = X.limbs(xc, L);
         const int t0 = L - kTcGuard;
         const int lsbP = xm.exp + ym.exp - 64 * L;
@@ -520,6 +536,7 @@ struct ItemTcRoundD {
     const int* err;
     int* fb_count;
     long long* fb;
+    int force_fb = 0; // tests: every 7th certified item is sent to the exact fix-up anyway (HK_TC_FORCE_FIX)
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         if (*(volatile const int*)err >= 0) return;
         const long long e = e0 + w;
@@ -527,6 +544,7 @@ struct ItemTcRoundD {
         const Meta cm = S.m[e], xm = panel.m[j - i], ym = B.m[k];
         const int sp = -(xm.sign * ym.sign);
         if (sp == 0) return;
+        if (force_fb && w % 7 == 3) return force_to_fix(w, fb_count, fb);
         uint32_t* c = S.limbs(e, L);
         const int t0 = L - kTcGuard;
         const int lsbP = xm.exp + ym.exp - 64 * L;

@@ -101,6 +101,25 @@ def test_path_bit_exact_vs_model(api, beta, n, L, k, inv_flow, monkeypatch):
         assert from_arr(ctx.block()) == M
 
 
+@pytest.mark.parametrize("beta,n,L,k", [((1, 1), 24, 8, 8), ((1, 3), 20, 24, 12), ((1, 2), 64, 96, 8)])
+def test_tc_fixup_path_bit_exact(api, beta, n, L, k, monkeypatch):
+    """The tensor-core path with every 7th item of each certified rounding pass
+    (LDLT and L^-1) sent to the exact fix-up kernels (HK_TC_FORCE_FIX): the rare
+    uncertified path must give the same bits."""
+    monkeypatch.setenv("HK_TC", "1")
+    monkeypatch.setenv("HK_TC_FORCE_FIX", "1")
+    p = 32 * L
+    mu = [R.moment_integer(beta, j) for j in range(2 * n - 1)]
+    D, Lf, Rr = F.ldlt(mu, n, p)
+    X = F.invert_L_partial(Lf, n, k, p)
+    M = F.block(X, Rr, n, k, p)
+    with run_path(api, beta, n, L, k) as ctx:
+        assert from_arr(ctx.D()) == D
+        gx = from_arr(ctx.Linv())
+        assert all(gx[r * k + c] == X[r][c] for r in range(n) for c in range(min(r, k)))
+        assert from_arr(ctx.block()) == M
+
+
 def digest(vals):
     import hashlib
 

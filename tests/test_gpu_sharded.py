@@ -83,11 +83,13 @@ def test_virtual_sharded_precision_error(api):
         assert ctx.bad_column == want
 
 
-@pytest.mark.parametrize("world", [1, 3])
-def test_virtual_sharded_tensor_core_path(api, single, world, monkeypatch):
+@pytest.mark.parametrize("world,force_fix", [(1, "0"), (3, "0"), (3, "1")])
+def test_virtual_sharded_tensor_core_path(api, single, world, force_fix, monkeypatch):
     """The sharded look-ahead schedule with the tensor-core bulk products forced
-    (mode 2 of the product kernel + certified rounding), against the 1-GPU path."""
+    (mode 2 of the product kernel + certified rounding; with force_fix every 7th
+    item also through the exact fix-up), against the 1-GPU path."""
     monkeypatch.setenv("HK_TC", "1")
+    monkeypatch.setenv("HK_TC_FORCE_FIX", force_fix)
     for (beta, n, L, k), (mu, (r0, D0, X0, M0)) in single.items():
         if L % 4:
             continue
