@@ -159,6 +159,27 @@ def workload_config(args, cfg, world):
             "l2": "256 MB L2 flush before every timed step (C2 working set 25 MB would fit L2)"}
 
 
+def lambda_parity(name, cfg, lam):
+    """Digits of this run's lambda_min (hi + lo) against the reference's golden
+    value for the config (tests/golden/<config>.json: the reference built from
+    its own sources, lambda from its fixed-point block at 80 digits)."""
+    path = os.path.join(ROOT, "tests", "golden", f"{name}.json")
+    if not os.path.exists(path):
+        return {"golden": None}
+    from decimal import Decimal, getcontext
+
+    getcontext().prec = 60
+    g = json.load(open(path))
+    if g.get("n") != cfg["n"] or g.get("p") != cfg["p"]:
+        return {"golden": None}
+    want = Decimal(g["lambda"][0])
+    got = Decimal(repr(lam[0][0])) + Decimal(repr(lam[1][0]))
+    rel = abs(got / want - 1)
+    digits = float(-rel.log10()) if rel > 0 else 60.0
+    return {"lambda1_digits_vs_reference": round(digits, 2), "required_digits": 20,
+            "golden": f"tests/golden/{name}.json (reference at K={g.get('K')}, lambda at 80 digits)"}
+
+
 def bench_ours(args, cfg):
     import torch
 
@@ -319,6 +340,7 @@ def bench_ours(args, cfg):
         "config": workload_config(args, cfg, world),
         "time_to_lambda_ms": ms,
         "lambda_min": repr(lam[0][0] + lam[1][0]),
+        "parity": lambda_parity(args.config, cfg, lam) if rank == 0 else None,
         "e2e": {"value": fmas(n) / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "roofline": roofline,
