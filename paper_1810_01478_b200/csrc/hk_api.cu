@@ -42,6 +42,24 @@ __global__ void __launch_bounds__(256) k_items(long long n, int ws_words, F f) {
     for (long long it = (long long)blockIdx.x * wpb + wib; it < n; it += nw) f(it, ws);
 }
 
+// Launch through cudaLaunchKernelEx, optionally with programmatic stream
+// serialization (the kernel must begin with griddepcontrol.wait before it
+// reads its same-stream predecessor's outputs).
+template <class K, class... Args>
+void launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 struct HkError {
     int code;
     std::string msg;
@@ -221,6 +239,9 @@ void launch_hot(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t s
 template <class F>
 __global__ void __launch_bounds__(256) k_cta_items(long long n, F f) {
     extern __shared__ __align__(16) uint32_t cta_smem[];
+    // programmatic dependent launch (the look-ahead chain): this grid may be
+    // launched before its predecessor finishes; wait for it before any read
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (long long it = blockIdx.x; it < n; it += gridDim.x) {
         f(it, cta_smem);
         __syncthreads();
@@ -230,7 +251,7 @@ __global__ void __launch_bounds__(256) k_cta_items(long long n, F f) {
 constexpr int kCtaThreads = 256;
 
 template <class F>
-void launch_cta(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = nullptr) {
+void launch_cta(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = nullptr, bool pdl = false) {
     if (n <= 0) return;
     if (!st) st = c->st;
     const size_t smem = size_t(ws_words) * sizeof(uint32_t);
@@ -248,7 +269,21 @@ void launch_cta(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t s
         configured[key] = v;
     }
     const long long blocks = n < (1LL << 30) ? n : (1LL << 30);
-    k_cta_items<F><<<unsigned(blocks), kCtaThreads, smem, st>>>(n, f);
+    if (pdl) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(blocks));
+        cfg.blockDim = dim3(kCtaThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        ck(cudaLaunchKernelEx(&cfg, k_cta_items<F>, n, f), "kernel launch (PDL)");
+    } else {
+        k_cta_items<F><<<unsigned(blocks), kCtaThreads, smem, st>>>(n, f);
+    }
     ck(cudaGetLastError(), "kernel launch");
     ++c->launches;
 }
@@ -362,7 +397,7 @@ bool use_tc_inv(const hk_ctx* c) {
 
 // A operand preformat + the tcgen05 product kernel (one CTA per SM: it owns all
 // 512 TMEM columns).  `rows` is the row-operand source (ItemTcPrep).
-void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaStream_t st) {
+void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaStream_t st, bool pdl = false) {
     const int N = c->n, L = c->L;
     // small p: one TMEM accumulator and two CTAs per SM (one CTA's prologue and
     // epilogue overlap the other's MMAs); large p: two accumulators, one CTA per SM
@@ -387,19 +422,19 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     a.dev = dv ? atoi(dv) : 0;
     const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
     const long long nprep = prep.count();
-    hk::k_tc_prep<<<unsigned((nprep + 255) / 256), 256, 0, st>>>(prep, nprep);
+    launch_ex(hk::k_tc_prep, dim3(unsigned((nprep + 255) / 256)), dim3(256), 0, st, pdl, prep, nprep);
     ck(cudaGetLastError(), "tc prep launch");
     ++c->launches;
     const int first_row = a.mode != 1 ? a.jfirst : a.i + 1;
     const dim3 grid(gx, unsigned(hk::tc_ntiles(N) - first_row / hk::kTcRows), unsigned(a.groups));
-    hk::k_tc_bulk<<<grid, hk::kTcThreads, smem, st>>>(a);
+    launch_ex(hk::k_tc_bulk, grid, dim3(hk::kTcThreads), smem, st, pdl, a);
     ck(cudaGetLastError(), "tc bulk launch");
     ++c->launches;
 }
 
 // Per-(column, row) items over `ncols` columns of at most `maxrows` rows (k_cols).
 template <class F>
-void launch_cols(hk_ctx* c, const F& f, int ncols, int maxrows, int ws_words, cudaStream_t st) {
+void launch_cols(hk_ctx* c, const F& f, int ncols, int maxrows, int ws_words, cudaStream_t st, bool pdl = false) {
     if (ncols <= 0 || maxrows <= 0) return;
     const size_t per_warp = size_t(ws_words) * sizeof(uint32_t);
     int wpb = int((96 * 1024) / per_warp);
@@ -412,14 +447,14 @@ void launch_cols(hk_ctx* c, const F& f, int ncols, int maxrows, int ws_words, cu
         cfg = true;
     }
     const unsigned gx = unsigned((maxrows + wpb - 1) / wpb);
-    hk::k_cols<F><<<dim3(gx, unsigned(ncols)), unsigned(32 * wpb), smem, st>>>(f, ws_words);
+    launch_ex(hk::k_cols<F>, dim3(gx, unsigned(ncols)), dim3(unsigned(32 * wpb)), smem, st, pdl, f, ws_words);
     ck(cudaGetLastError(), "cols launch");
     ++c->launches;
 }
 
 // Exact redo of the items the rounding pass could not certify (device-side count).
 template <class F>
-void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset) {
+void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset, bool pdl = false) {
     const int wo = ws_op_words(c->L);
     const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
     static bool cfg = false;
@@ -428,15 +463,15 @@ void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset) 
         ck(cudaFuncSetAttribute(hk::k_tc_fix<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         cfg = true;
     }
-    hk::k_tc_fix<F><<<unsigned(c->sm_count), unsigned(32 * wpb), size_t(wo) * 4 * wpb, st>>>(f, count, c->tc_fb, wo,
-                                                                                            reset);
+    launch_ex(hk::k_tc_fix<F>, dim3(unsigned(c->sm_count)), dim3(unsigned(32 * wpb)), size_t(wo) * 4 * wpb, st, pdl, f,
+              (const int*)count, (const long long*)c->tc_fb, wo, reset);
     ck(cudaGetLastError(), "tc fix launch");
     ++c->launches;
 }
 
 // Step-i update of columns jfirst..N-1 (bulk): IMAD paired warp FMAs, or the
 // tcgen05 product kernel followed by the certified rounding pass.
-void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
+void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = false) {
     const int N = c->n, L = c->L;
     const int ncols = N - jfirst;
     if (ncols <= 0) return;
@@ -447,7 +482,7 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
     }
     if (!dev_skip("prod"))
         tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
-                    b_buf(c, i), unsigned(ncols), st);
+                    b_buf(c, i), unsigned(ncols), st, pdl);
     if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
     // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
     int* cnt = c->tc_fb_count + (i & 1);
@@ -457,8 +492,8 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st) {
     ri.direct = !rd || rd[0] == '1';
     ri.force_fb = force_fix();
     if (!dev_skip("round"))
-        launch_cols(c, ri, ncols, ncols, ri.direct ? hk::align4(L + 16) : hk::tcround_words(L), st);
-    if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st, cnt, nxt);
+        launch_cols(c, ri, ncols, ncols, ri.direct ? hk::align4(L + 16) : hk::tcround_words(L), st, pdl);
+    if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st, cnt, nxt, pdl);
 }
 
 // L^-1 step i on the tensor cores (same product kernel, mode 1).
@@ -666,6 +701,8 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     std::vector<cudaEvent_t>& evC = c->evC;
     std::vector<cudaEvent_t>& evB1 = c->evB1;
     cudaStream_t la2 = c->st3, side = c->st4;
+    static const char* pe = getenv("HK_PDL"); // programmatic dependent launch on the chain (default on)
+    const bool pdl = !pe || pe[0] != '0';
     if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), bulk), "memset fb counters");
     ck(cudaEventRecord(c->evFork, bulk), "fork");
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
@@ -679,7 +716,7 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     // MulB(i+1) (overwrites buffer (i+1) % 3 = that of B_{i-2}) after [evR(i-2)].
     for (int i = 0; i < N; ++i) {
         ck(cudaStreamWaitEvent(bulk, evP[i], 0), "wait P");
-        enqueue_bulk(c, i, i + 2, bulk);
+        enqueue_bulk(c, i, i + 2, bulk, pdl);
         ck(cudaEventRecord(evU[i], bulk), "evU");
         if (i >= 1) {
             // StoreL(i-1) on the side stream: column i-1 was last read by U(i-1)
@@ -697,12 +734,13 @@ void enqueue_ldlt_steps(hk_ctx* c) {
             ck(cudaEventRecord(evD[i + 1], la), "evD");
             ck(cudaStreamWaitEvent(la2, evD[i + 1], 0), "wait D");
             if (!dev_skip("coloff"))
-                launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 1}, N - i - 2, wc, la2);
+                launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 1}, N - i - 2, wc, la2,
+                           pdl);
             ck(cudaEventRecord(evO[i + 1], la2), "evO");
             if (!dev_skip("coldiag"))
-                launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 0}, 1, wc, la);
+                launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 0}, 1, wc, la, pdl);
             if (!dev_skip("recip"))
-                launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la);
+                launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la, pdl);
             ck(cudaEventRecord(evC[i + 1], la), "evC");
             // B_{i+1}: the first entry (all the next diagonal update needs) on `la`,
             // the rest on `la2`; B buffer (i+1) % 3 was last read by StoreL(i-2)
@@ -710,13 +748,13 @@ void enqueue_ldlt_steps(hk_ctx* c) {
             ck(cudaStreamWaitEvent(la, evO[i + 1], 0), "wait O");
             if (!dev_skip("mulb") && N - i - 2 > 0)
                 launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err, 1}, 1,
-                           wc, la);
+                           wc, la, pdl);
             ck(cudaEventRecord(evB1[i + 1], la), "evB1");
             ck(cudaStreamWaitEvent(la2, evC[i + 1], 0), "wait C");
             if (i >= 2) ck(cudaStreamWaitEvent(la2, evR[i - 2], 0), "wait R2");
             if (!dev_skip("mulb") && N - i - 3 > 0)
                 launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, i + 1), N, L, i + 1, c->d_err, 2},
-                           N - i - 3, wc, la2);
+                           N - i - 3, wc, la2, pdl);
             ck(cudaStreamWaitEvent(la2, evB1[i + 1], 0), "wait B1");
             ck(cudaEventRecord(evP[i + 1], la2), "evP");
         }

@@ -113,7 +113,14 @@ struct ItemTcPrep {
 };
 
 #if !defined(HK_WARP_EMU)
+// griddepcontrol.wait: under programmatic dependent launch (the LDLT bulk
+// stream) a grid may start before its predecessor finishes; it waits here for
+// the predecessor's completion and memory before touching its outputs (no-op
+// for an ordinary launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) k_tc_prep(ItemTcPrep f, long long n) {
+    pdl_wait();
     const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (u < n) f(u);
 }
@@ -239,6 +246,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                     pcn = nblk_of(pc);
                 }
             };
+            pdl_wait(); // the A operand comes from the preceding k_tc_prep
             while (qt < Q && qt < kTcStages - 1 && !(a.dev & 2)) issue_tma();
             int q = 0;
             for (int c = c_lo; c < nch; ++c) {
@@ -623,6 +631,7 @@ struct FixD {
 template <class F>
 __global__ void __launch_bounds__(256) k_cols(F f, int ws_words) {
     extern __shared__ __align__(16) uint32_t csm[];
+    pdl_wait();
     const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     uint32_t* ws = csm + (size_t)wib * ws_words;
     const int jj = int(blockIdx.y), rows = f.rows(jj);
@@ -632,6 +641,7 @@ __global__ void __launch_bounds__(256) k_cols(F f, int ws_words) {
 template <class F>
 __global__ void __launch_bounds__(256) k_tc_fix(F f, const int* fb_count, const long long* fb, int ws_words,
                                                 int* reset) {
+    pdl_wait();
     extern __shared__ uint32_t fsm[];
     const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     uint32_t* ws = fsm + (size_t)wib * ws_words;
