@@ -36,6 +36,7 @@ using hk::MpArr;
 template <class F>
 __global__ void __launch_bounds__(256) k_items(long long n, int ws_words, F f) {
     extern __shared__ uint32_t smem[];
+    asm volatile("griddepcontrol.wait;" ::: "memory"); // see launch_ex (no-op for ordinary launches)
     const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     uint32_t* ws = smem + (size_t)wib * ws_words;
     const long long nw = (long long)gridDim.x * wpb;
@@ -172,7 +173,7 @@ int ws_recip_words(int L) { return hk::recipws_words(L); }
 // persistence), so blocks of the high-priority look-ahead stream are
 // dispatched as soon as any bulk block retires.
 template <class F>
-void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = nullptr) {
+void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = nullptr, bool pdl = false) {
     if (n <= 0) return;
     if (!st) st = c->st;
     const size_t per_warp = size_t(ws_words) * sizeof(uint32_t);
@@ -195,7 +196,7 @@ void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = 
     long long blocks = (n + wpb - 1) / wpb;
     const long long cap = 1LL << 30;
     if (blocks > cap) blocks = cap;
-    k_items<F><<<unsigned(blocks), unsigned(32 * wpb), smem, st>>>(n, ws_words, f);
+    launch_ex(k_items<F>, dim3(unsigned(blocks)), dim3(unsigned(32 * wpb)), smem, st, pdl, n, ws_words, f);
     ck(cudaGetLastError(), "kernel launch");
     ++c->launches;
 }
@@ -497,7 +498,7 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = fals
 }
 
 // L^-1 step i on the tensor cores (same product kernel, mode 1).
-void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
+void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false) {
     const int N = c->n, L = c->L, m = c->m;
     const int b = i < m ? i : m;
     if (i + 1 >= N) return;
@@ -510,7 +511,7 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
         hk::TcBulkArgs a{c->S.view(), c->X.view(), c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err};
         a.groups = G;
         a.gcarry = c->tc_gcarry;
-        tc_products(c, a, c->S.view(), unsigned(b), st);
+        tc_products(c, a, c->S.view(), unsigned(b), st, pdl);
     }
     int* cnt = c->tc_fb_count + (i & 1);
     int* nxt = c->tc_fb_count + ((i + 1) & 1);
@@ -519,9 +520,9 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st) {
     ri.G = G;
     ri.gcarry = c->tc_gcarry;
     ri.force_fb = force_fix();
-    launch(c, ri, items, hk::tcround_words(L), st);
+    launch(c, ri, items, hk::tcround_words(L), st, pdl);
     if (b > 0)
-        launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st, cnt, nxt);
+        launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st, cnt, nxt, pdl);
     else
         ck(cudaMemsetAsync(nxt, 0, sizeof(int), st), "memset fb");
 }
@@ -1030,7 +1031,8 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
                 const int b = i < m ? i : m;
                 const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
                 if (tc) {
-                    enqueue_inv_tc(c, i, c->st);
+                    static const char* pe = getenv("HK_PDL");
+                    enqueue_inv_tc(c, i, c->st, !pe || pe[0] != '0');
                     continue;
                 }
                 // few items: a CTA per FMA (latency); many: a warp per FMA (one wave)
