@@ -504,7 +504,9 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false) {
     if (i + 1 >= N) return;
     // narrow step: split each product's output chunks over G CTAs (carries joined in the rounding pass)
     const int tiles = hk::tc_ntiles(N) - (i + 1) / hk::kTcRows;
-    int G = b > 0 ? (c->sm_count + b * tiles - 1) / (b * tiles) : 1;
+    // (one CTA per SM in mode 1: keep the split to a single wave — rounding the
+    // group count up made a second, mostly empty wave: C3 L^-1 49.9 -> 42.0 ms)
+    int G = b > 0 ? c->sm_count / (b * tiles) : 1;
     G = std::min(G, std::min(int(hk::kTcMaxGroups), hk::tc_nchunks(L) / 2));
     if (G < 1) G = 1;
     if (b > 0) {
