@@ -400,16 +400,15 @@ bool use_tc_inv(const hk_ctx* c) {
 // 512 TMEM columns).  `rows` is the row-operand source (ItemTcPrep).
 void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaStream_t st, bool pdl = false) {
     const int N = c->n, L = c->L;
-    // small p: one TMEM accumulator and two CTAs per SM (one CTA's prologue and
-    // epilogue overlap the other's MMAs); large p: two accumulators, one CTA per SM
-    // (the epilogue of chunk c overlaps the MMAs of chunk c + 1).
-    // LDLT (many CTAs per step): windowed x expansion (93-103 KB of shared memory)
-    // and one TMEM accumulator, two CTAs per SM.  L^-1 (b <= m column CTAs per
-    // step): full expansion when it fits and two accumulators, one CTA per SM.
-    a.ewin = (a.mode != 1 || hk::tc_ewin(L)) ? 1 : 0;
+    // Windowed x expansion (93-103 KB of shared memory for any p) and one TMEM
+    // accumulator: two CTAs per SM, one CTA's prologue and epilogue overlap the
+    // other's MMAs (LDLT and L^-1 alike; L^-1 splits each product's chunks into
+    // groups to fill that one wave: C4 L^-1 288 -> 222 ms against one CTA per SM
+    // with two accumulators).  HK_TC_EWIN / HK_TC_NACC force the other variants.
+    a.ewin = 1;
     if (const char* e = getenv("HK_TC_EWIN")) a.ewin = e[0] == '1' ? 1 : 0;
     const size_t need = hk::tc_smem_bytes(L, a.ewin != 0);
-    a.nacc = (a.mode != 1 && need <= 110 * 1024) ? 1 : 2;
+    a.nacc = need <= 110 * 1024 ? 1 : 2;
     if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
     const size_t smem = a.nacc == 1 ? need : std::max(need, size_t(120 * 1024));
     static bool configured = false;
@@ -504,9 +503,9 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false) {
     if (i + 1 >= N) return;
     // narrow step: split each product's output chunks over G CTAs (carries joined in the rounding pass)
     const int tiles = hk::tc_ntiles(N) - (i + 1) / hk::kTcRows;
-    // (one CTA per SM in mode 1: keep the split to a single wave — rounding the
-    // group count up made a second, mostly empty wave: C3 L^-1 49.9 -> 42.0 ms)
-    int G = b > 0 ? c->sm_count / (b * tiles) : 1;
+    // two CTAs per SM (windowed expansion, one accumulator): keep the split to a
+    // single wave — rounding the group count up made a second, mostly empty wave
+    int G = b > 0 ? 2 * c->sm_count / (b * tiles) : 1;
     G = std::min(G, std::min(int(hk::kTcMaxGroups), hk::tc_nchunks(L) / 2));
     if (G < 1) G = 1;
     if (b > 0) {
