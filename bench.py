@@ -173,10 +173,11 @@ def lambda_parity(name, cfg, lam):
     if g.get("n") != cfg["n"] or g.get("p") != cfg["p"]:
         return {"golden": None}
     want = Decimal(g["lambda"][0])
-    got = Decimal(repr(lam[0][0])) + Decimal(repr(lam[1][0]))
+    got = Decimal(lam[0][0]) + Decimal(lam[1][0])  # exact binary values of hi and lo
     rel = abs(got / want - 1)
     digits = float(-rel.log10()) if rel > 0 else 60.0
     return {"lambda1_digits_vs_reference": round(digits, 2), "required_digits": 20,
+            "lambda1_hi_plus_lo": f"{got:.33e}",
             "golden": f"tests/golden/{name}.json (reference at K={g.get('K')}, lambda at 80 digits)"}
 
 
