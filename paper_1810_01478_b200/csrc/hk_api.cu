@@ -43,6 +43,15 @@ __global__ void __launch_bounds__(256) k_items(long long n, int ws_words, F f) {
     for (long long it = (long long)blockIdx.x * wpb + wib; it < n; it += nw) f(it, ws);
 }
 
+struct HkError {
+    int code;
+    std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw HkError{HK_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
 // Launch through cudaLaunchKernelEx, optionally with programmatic stream
 // serialization (the kernel must begin with griddepcontrol.wait before it
 // reads its same-stream predecessor's outputs).
@@ -58,16 +67,8 @@ void launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bo
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kernel, args...);
-}
-
-struct HkError {
-    int code;
-    std::string msg;
-};
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw HkError{HK_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e)};
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+    if (e != cudaSuccess) throw HkError{HK_ERR_RUNTIME, std::string("kernel launch: ") + cudaGetErrorString(e)};
 }
 
 struct DevArr {
