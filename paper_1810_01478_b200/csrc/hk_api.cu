@@ -578,6 +578,9 @@ __device__ __forceinline__ void inv_flow_decode(long long e, int m, int& j, int&
 
 // One CTA per entry (cta_fms: the products on all 8 warps — the per-entry chain
 // is latency-bound, a warp per entry measured 2x slower at C2).
+// 3 warps per entry (C2 invL: 256 threads 3.67 ms, 128 3.14, 96 2.99; capping
+// registers so that every C2 entry is resident at once spilled: 4.31 ms)
+constexpr int kFlowThreads = 96;
 __global__ void __launch_bounds__(256) k_inv_flow_cta(InvFlowArgs a) {
     extern __shared__ __align__(16) uint32_t fsm2_[];
     __shared__ unsigned long long e_s;
@@ -650,8 +653,7 @@ void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
         ck(cudaFuncSetAttribute(k_inv_flow_cta, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
         cfg2 = true;
     }
-    static const char* tb = getenv("HK_FLOW_THREADS"); // dev sweep
-    const int threads = tb ? atoi(tb) : 96; // 3 warps per entry: C2 invL 3.67 (256) / 3.14 (128) / 2.99 ms
+    const int threads = kFlowThreads;
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow_cta, threads, smem), "occupancy");
     const unsigned grid = unsigned(std::max(1LL, std::min(E, (long long)std::max(1, per_sm) * c->sm_count)));
