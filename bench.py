@@ -2,27 +2,35 @@
 """bench.py — the driver's benchmark contract for the extreme-precision Hankel path.
 
 Metric (BASELINE.json): time to lambda_min and MP-FMA/s of the Hankel LDLT.
-One *step* = one pass of the hot path over one input: moments mu (resident) ->
-LDLT -> first k columns of L^{-1} -> k x k block of H^{-1} -> eigensolve ->
-lambda_min.  Reported throughput = N(N^2-1)/6 LDLT MP-FMAs (the reference's
-update_count, ldlt.cpp:128) per step time, i.e. MP-FMA/s over time-to-lambda.
+One *step* = one pass of the hot path over one input: moments mu -> LDLT ->
+first k columns of L^{-1} -> k x k block of H^{-1} -> eigensolve -> lambda_min.
+Reported throughput = N(N^2-1)/6 LDLT MP-FMAs (the reference's update_count,
+ldlt.cpp:128) per step time, i.e. MP-FMA/s over time-to-lambda.
 
-Workload (default): BASELINE configs[1] = C2, beta = 1 (Laguerre), N = 256,
-p = 6144 bits, k = 8 — the largest single-GPU config the metric is quoted on
-that runs in seconds (configs[0] = C1 is the CPU-runnable oracle case).
+Workload (default): BASELINE configs[3] = C4, beta = 1/2, N = 1024,
+p = 49152 bits, k = 16 — the configuration the metric is quoted on "at
+1/2/4/8 B200" and the largest that fits one GPU (C5 is the 8-GPU run).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c5]
 
-N > 1 is launched by torchrun (one rank per GPU): the LDLT is column-sharded
-across the ranks (boustrophedon ownership, ncclBroadcast of the pivot column
-each step, gather to rank 0 for L^{-1}/block/eigen) — the same job split over
-N GPUs (strong scaling); timing is the max over ranks.
+N > 1: one rank per GPU (torchrun; `--gpus N` without WORLD_SIZE re-launches
+itself under torch.distributed.run).  The LDLT is column-sharded across the
+ranks (boustrophedon ownership, ncclBroadcast of the pivot column each step,
+gather to rank 0 for L^{-1}/block/eigen) — the same job split over N GPUs
+(strong scaling); timing is the max over ranks.
+
+`value` times the path with the moments resident on the device; `e2e` times the
+public call a user makes (hk_moments on the host into pinned buffers, then
+hk_compute: H2D of the moments, the whole path, D2H of the block and lambdas)
+— the same span as the reference's RunRecord::wall_s, which includes its
+build_hankel (pipeline.cpp:39-41).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,18 +41,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 
-CONFIGS = {  # BASELINE.json configs
-    "c1": dict(beta=(1, 2), n=64, p=3072, k=8, K_ref=2048),
-    "c2": dict(beta=(1, 1), n=256, p=6144, k=8, K_ref=2048),
-    "c3": dict(beta=(1, 3), n=512, p=36864, k=12, K_ref=3072),
-    # c4 / c5: the reference's full run takes ~4 min / hours on the host, so its CPU
-    # rate is sampled on the leading N=512 block at the same K (smaller operands:
-    # this overstates the reference's MP-FMA/s, i.e. it is conservative for us)
-    "c4": dict(beta=(1, 2), n=1024, p=49152, k=16, K_ref=4096, cpu_n=512),
-    "c5": dict(beta=(1, 2), n=2048, p=114688, k=16, K_ref=6144, cpu_n=512),
+# BASELINE.json configs.  K_ref = the reference's K of the golden runs
+# (1024 ceil(N/500) + 1024); K_equiv = (p - bits(mu_{2N-2})) / 2, the fixed-point
+# K whose 2K fraction bits equal the float's absolute precision on the largest
+# entry — the like-for-like precision for timing the reference.
+CONFIGS = {
+    "c1": dict(beta=(1, 2), n=64, p=3072, k=8, K_ref=2048, K_equiv=705),
+    "c2": dict(beta=(1, 1), n=256, p=6144, k=8, K_ref=2048, K_equiv=1143),
+    "c3": dict(beta=(1, 3), n=512, p=36864, k=12, K_ref=3072, K_equiv=2872),
+    "c4": dict(beta=(1, 2), n=1024, p=49152, k=16, K_ref=4096, K_equiv=2968),
+    "c5": dict(beta=(1, 2), n=2048, p=114688, k=16, K_ref=6144, K_equiv=10020),
 }
 METRIC = "MP-FMA/s of Hankel LDLT over time to lambda_min (N(N^2-1)/6 FMAs per step)"
 UNIT = "MP-FMA/s"
+# CPU-baseline leg of our own line: a bounded sample (~10-30 s of host work) of
+# the same workload — the reference on the leading N_s x N_s block of H_N (the
+# LDLT of H_N begins with exactly that factorisation), at K_equiv
+CPU_SAMPLE_N = {"c1": 64, "c2": 256, "c3": 256, "c4": 512, "c5": 512}
 
 
 def dist_env():
@@ -98,65 +111,100 @@ def ref_driver_path():
     return os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 
 
-def run_reference_once(cfg, workers):
-    """hankel::compute() of the unmodified reference (oracle/_ref) -> its RunRecord JSON
-    (on the bounded sample N = cfg['cpu_n'] when the config sets one)."""
+def run_reference_once(cfg, workers, K, n=None):
+    """hankel::compute() of the unmodified reference (oracle/_ref/ref_driver) -> its RunRecord JSON."""
     b = cfg["beta"]
-    out = subprocess.run([ref_driver_path(), "time", "--beta", f"{b[0]}/{b[1]}", "--n", str(cfg.get("cpu_n", cfg["n"])),
-                          "--bits",
-                          str(cfg["K_ref"]), "--k", str(cfg["k"]), "--workers", str(workers)],
+    out = subprocess.run([ref_driver_path(), "time", "--beta", f"{b[0]}/{b[1]}", "--n", str(n or cfg["n"]),
+                          "--bits", str(K), "--k", str(cfg["k"]), "--workers", str(workers)],
                          capture_output=True, text=True, check=True)
     return json.loads(out.stdout)
 
 
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
 def hbm_peak_gbps():
     """Measured HBM copy bandwidth of this pool (MEASURED_PEAKS.json), else the recipe's fallback."""
-    try:
-        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
-    except Exception:
-        return 6650.0  # B200_PROFILING.md fallback
+    return float(measured_peaks().get("hbm_gbs", 6650.0))
 
 
 def fmas(n):
     return n * (n * n - 1) // 6
 
 
+def workload_config(args, cfg, world):
+    b = cfg["beta"]
+    return {"workload": f"{args.config.upper()}: beta={b[0]}/{b[1]} Hankel N={cfg['n']}, p={cfg['p']} bits, "
+                        f"k={cfg['k']} -> lambda_min", "n": cfg["n"], "p_bits": cfg["p"], "k": cfg["k"],
+            "beta": f"{b[0]}/{b[1]}",
+            "parallelism": f"column-sharded LDLT x{world} GPUs (NCCL pivot-column broadcast)" if world > 1 else "1 GPU",
+            "l2": "256 MB written between timed steps (L2 flush); the LDLT working set is "
+                  f"{cfg['n'] * (cfg['n'] + 1) // 2 * (cfg['p'] // 8 + 8) / 1e6:.0f} MB"}
+
+
+# ---------------------------------------------------------------- reference arm
+
+
 def bench_reference(args, cfg):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified sources
+    compiled against the GMP shim) through its public hankel::compute, with every
+    host core as a worker, on the same config.  A full C4 run takes minutes on
+    the box's cores, so the step count is bounded by --ref-budget-s: full runs
+    only (never a smaller N), as many as fit, at least one."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    times = []
+    budget = args.ref_budget_s
+    t_start = time.perf_counter()
+    warm, times, recs = 0, [], []
     for i in range(args.warmup + args.steps):
-        rec = run_reference_once(cfg, cores)
-        if i >= args.warmup:
-            times.append(rec["timing"]["wall_s"])
+        rec = run_reference_once(cfg, cores, cfg["K_equiv"])
+        if i < args.warmup and rec["timing"]["wall_s"] < 0.05 * budget:
+            warm += 1
+            continue
+        times.append(rec["timing"]["wall_s"])
+        recs.append(rec)
+        elapsed = time.perf_counter() - t_start
+        if len(times) >= args.steps or elapsed + times[-1] > budget:
+            break
     t = statistics.mean(times)
-    n_s = cfg.get("cpu_n", cfg["n"])
-    v = fmas(n_s) / t
-    sample = (f"{args.steps} full runs of hankel::compute (reference, fixed point K={cfg['K_ref']}) on "
-              f"{args.config}" + (f" restricted to its leading N={n_s} block" if n_s != cfg["n"] else "") +
-              f"; mean wall_s {t:.3f}")
+    v = fmas(cfg["n"]) / t
+    # the golden runs' precision (K_ref) beside it, on request (one more full run)
+    k_ref = None
+    if args.ref_golden_precision and cfg["K_ref"] != cfg["K_equiv"]:
+        r2 = run_reference_once(cfg, cores, cfg["K_ref"])
+        k_ref = {"K": cfg["K_ref"], "wall_s": r2["timing"]["wall_s"], "ldlt_s": r2["timing"]["ldlt_s"],
+                 "value": fmas(cfg["n"]) / r2["timing"]["wall_s"]}
+    sample = (f"{len(times)} full run(s) of the reference's hankel::compute (oracle/_ref, fixed point "
+              f"K={cfg['K_equiv']} = K_equiv, workers={cores}) on the whole {args.config} workload "
+              f"(N={cfg['n']}); mean wall_s {t:.3f}, ldlt_s {statistics.mean(r['timing']['ldlt_s'] for r in recs):.3f}"
+              + (f"; {warm} warm-up run(s)" if warm else "; no warm-up runs (a full run exceeds 5% of the budget)")
+              + (f"; steps bounded by the {budget:.0f} s budget ({args.steps} requested)" if len(times) < args.steps
+                 else ""))
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": f"fixed-point mpz, K={cfg['K_ref']} (2K={2 * cfg['K_ref']} in LDLT)",
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(times),
+        "steps_requested": args.steps, "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": f"fixed-point mpz, K={cfg['K_equiv']} (2K={2 * cfg['K_equiv']} in LDLT)",
         "data": "exact-integer moments (deterministic, no dataset)",
-        "config": workload_config(args, cfg, world),
+        "config": workload_config(args, cfg, 1),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "time_to_lambda_s": t,
+        "reference_timing": recs[-1]["timing"],
+        "lambda_min": recs[-1]["lambda"][0] if recs[-1]["lambda"] else None,
+        "at_golden_precision": k_ref,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(args, cfg, world):
-    b = cfg["beta"]
-    return {"workload": f"{args.config.upper()}: beta={b[0]}/{b[1]} Hankel N={cfg['n']}, p={cfg['p']} bits, "
-                        f"k={cfg['k']} -> lambda_min", "n": cfg["n"], "p_bits": cfg["p"], "k": cfg["k"],
-            "beta": f"{b[0]}/{b[1]}", "parallelism": f"column-sharded LDLT x{world} GPUs (NCCL pivot-column broadcast)" if world > 1 else "1 GPU",
-            "l2": "256 MB L2 flush before every timed step (C2 working set 25 MB would fit L2)"}
+# ---------------------------------------------------------------- our arm
 
 
 def lambda_parity(name, cfg, lam):
@@ -181,156 +229,164 @@ def lambda_parity(name, cfg, lam):
             "golden": f"tests/golden/{name}.json (reference at K={g.get('K')}, lambda at 80 digits)"}
 
 
+def max_over_ranks(x, world, local):
+    if world == 1:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def bench_ours(args, cfg):
+    import numpy as np
     import torch
 
     from paper_1810_01478_b200 import api
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, p, k = cfg["n"], cfg["p"], cfg["k"]
     L = p // 32
-    s = min(3, min(k, n))
-    mu, exact = api.build_hankel(cfg["beta"], n, L)
-    assert exact, "moments must be exact at this precision"
+    kk = min(k, n)
+    s = min(3, kk)
     if world > 1 or args.sharded:  # column-sharded LDLT over NCCL (hk_create_sharded), results on rank 0
         import torch.distributed as dist
 
-        if not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [api.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx = api.Context(L, device=local, rank=rank, world=world, nccl_id=obj[0])
     else:
         ctx = api.Context(L, device=local)
+    ctx.set_kernel_timing(True)  # event-record nodes around every step's bulk kernels (graph-resident)
     ext = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")
 
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
     # ---- value: device-resident inputs (moments uploaded once, before timing)
+    mu, exact = api.build_hankel(cfg["beta"], n, L)
+    assert exact, "moments must be exact at this precision"
     ctx.load_moments(mu)
 
     def step():
         ctx.decompose()
         if rank != 0:
             return [float("nan")], [0.0], [0.0]
-        ctx.invert_L_partial(min(k, n))
-        ctx.assemble_truncated_inverse(min(k, n))
+        ctx.invert_L_partial(kk)
+        ctx.assemble_truncated_inverse(kk)
         return ctx.smallest_eigs_of_H(s)
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+    barrier()
     sampler = ClockSampler(local)
     total_ms = 0.0
     launches0 = ctx.launch_count()
+    kt_sum = {}
     with sampler:
         for _ in range(args.steps):
             flush.zero_()
-            torch.cuda.synchronize()
+            barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(ext)
             lam = step()
             e1.record(ext)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
-    torch.cuda.synchronize()
+            for kk_, v in ctx.kernel_times().items():  # this step's LDLT graph (event nodes)
+                kt_sum[kk_] = kt_sum.get(kk_, 0.0) + v
+    barrier()
     launches = ctx.launch_count() - launches0
-    ms = total_ms / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(total_ms / args.steps, world, local)
     value = fmas(n) / (ms * 1e-3)  # one job split over `world` GPUs (strong scaling)
+    kt = {kk_: v / args.steps for kk_, v in kt_sum.items()}
 
-    # ---- e2e: the public API call with host buffers (pinned), H2D + D2H inside the timed region
-    import numpy as np
+    # ---- e2e: the public call with host buffers: moments generated on the host
+    # into pinned arrays (hk_moments), then hk_compute (H2D, path, D2H of the
+    # block + lambdas) — the span of the reference's wall_s incl. build_hankel
+    def pinned(shape, dtype):
+        t = torch.empty(shape, dtype=torch.int32, pin_memory=True)
+        return t, t.numpy().view(dtype)
 
-    def pinned_like(a):
-        t = torch.empty(a.shape, dtype={np.uint32: torch.int32, np.int32: torch.int32}[a.dtype.type], pin_memory=True)
-        arr = t.numpy().view(a.dtype)
-        arr[...] = a
-        return t, arr
-
-    keep = [pinned_like(x) for x in (mu.limbs, mu.exps, mu.signs)]
+    keep = [pinned((2 * n - 1, L), np.uint32), pinned((2 * n - 1,), np.int32), pinned((2 * n - 1,), np.int32)]
     mu_pinned = api.MPArray(keep[0][1], keep[1][1], keep[2][1])
-    for _ in range(max(1, args.warmup)):
-        ctx.compute(mu_pinned, k)
-    torch.cuda.synchronize()
+
+    def e2e_step():
+        _, ex = api.build_hankel(cfg["beta"], n, L, out=mu_pinned)
+        assert ex
+        return ctx.compute(mu_pinned, k)
+
+    e2e_step()  # graphs are cached per context: one warm-up suffices
+    barrier()
     e2e_ms = 0.0
     for _ in range(args.steps):
         flush.zero_()
-        torch.cuda.synchronize()
+        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(ext)
-        rec = ctx.compute(mu_pinned, k)
+        rec = e2e_step()
         e1.record(ext)
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
-    e2e_ms /= args.steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    kk = min(k, n)
+    e2e_ms = max_over_ranks(e2e_ms / args.steps, world, local)
     h2d = mu.limbs.nbytes + mu.exps.nbytes + mu.signs.nbytes
-    d2h = kk * kk * (4 * L + 8) + 3 * 3 * 8
+    d2h = kk * kk * (4 * L + 8) + 9 * 8 if rank == 0 else 11 * 8
 
-    # ---- roofline of the dominant kernel (trailing update), instrumented eager run
-    if rank == 0:  # eager single-GPU instrumented run on rank 0 (no communication)
-        prof, n_tr = ctx.profile_ldlt()
-    else:
-        prof, n_tr = {"trailing": 1.0, "total": 1.0}, 1
-    ms_tr, ms_ldlt = prof["trailing"], prof["total"]
+    # ---- roofline of the dominant kernel: its graph-resident event times over the timed steps
     alg_macs = fmas(n) * L * L  # L^2 limb-MACs per MP-FMA
-    tc_path = prof.get("tc_products", 0.0) > 0.0
-    if tc_path:
-        # dominant kernel: the tcgen05 limb-product kernel (k_tc_bulk + its A preformat)
-        ms_k = prof["tc_products"]
-        achieved = alg_macs / (ms_k * 1e-3) / 1e12
-        peak = api.peak_i8mma(local) / 16.0 / 1e12  # u8 MAC/s -> limb-MAC/s (16 u8 MACs per limb-MAC)
-        ncu_file = os.path.join(ROOT, "profiles", f"ncu_tc_bulk_{args.config}.json")
-        round_bytes = fmas(n) * (12 * L + 32)  # read c, read product, write c (4 B limbs)
-        round_gbps = round_bytes / (max(prof["tc_round"], 1e-9) * 1e-3) / 1e9
-        roofline = {
-            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "Tlimb-MAC/s",
-            "frac": achieved / peak, "traffic": None,
-            "kernel": "k_tc_bulk: tcgen05.mma kind::i8 limb products of the trailing update (ldlt.cpp:122-129)",
-            "per_launch": f"avg over {n_tr} steps: {ms_k / n_tr:.4f} ms, {alg_macs / n_tr:.3e} algorithmic limb-MACs",
-            "algorithmic_units": "L^2 limb-MACs per MP-FMA (SURVEY 8d); the kernel forms the short product "
-                                 "(byte columns >= limb L-8, ~half of L^2), so frac can exceed the MMA utilisation",
-            "share_of_ldlt": ms_k / ms_ldlt,
-            "eager_ldlt_kernel_ms": prof,
-            "peak_how": "hk_peak_i8mma: back-to-back tcgen05.mma.kind::i8 M128 N256 K32 on every SM, best of 5, "
-                        "/16 u8 MACs per limb-MAC (MEASURED_PEAKS.json has no integer peak)",
-            "imad_peak": api.peak_imad(local) / 1e12,
-            "rounding_pass": {"kernel": "k_items<ItemTcRound> (+ k_tc_fix)", "ms": prof["tc_round"], "bound": "hbm",
-                              "achieved_GBps": round_gbps, "peak_GBps": hbm_peak_gbps(),
-                              "frac": round_gbps / hbm_peak_gbps(),
-                              "bytes": "12 L + 32 per MP-FMA (read c, read product, write c)"},
-        }
-    else:
-        ms_k = ms_tr
-        achieved = alg_macs / (ms_k * 1e-3) / 1e12
-        peak = api.peak_imad(local) / 1e12
-        ncu_file = os.path.join(ROOT, "profiles", f"ncu_trailing_{args.config}.json")
-        roofline = {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "Tlimb-MAC/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "kernel": "trailing update k_items_hot<ItemTrailing2> (ldlt.cpp:122-129)",
-                    "per_launch": f"avg over {n_tr} launches: {ms_k / n_tr:.4f} ms, "
-                                  f"{alg_macs / n_tr:.3e} algorithmic limb-MACs",
-                    "share_of_ldlt": ms_k / ms_ldlt,
-                    "eager_ldlt_kernel_ms": prof,
-                    "peak_how": "hk_peak_imad: register-only IMAD.WIDE carry-chain microkernel on this GPU, "
-                                "best of 5 (MEASURED_PEAKS.json has no integer peak)"}
-    if os.path.exists(ncu_file):
-        roofline["traffic"] = json.load(open(ncu_file)).get("dram_bytes_per_launch")
+    tc_path = L >= 128 and L % 4 == 0
+    steps_k = max(kt.get("steps", 0.0), 1.0)
+    ms_k = kt.get("products_ms", 0.0)
+    ldlt_ms = kt.get("ldlt_ms", 0.0)
+    roofline = None
+    if ms_k > 0:
+        # the look-ahead column (ldlt.cpp:122-129 for j = i+1) runs on the chain, not in these launches
+        bulk_macs = sum((n - i - 2) * (n - i - 1) // 2 for i in range(n)) * L * L
+        achieved = bulk_macs / (ms_k * 1e-3) / 1e12
+        if tc_path:
+            peak = api.peak_i8mma(local) / 16.0 / 1e12  # u8 MAC/s -> limb-MAC/s (16 u8 MACs per limb-MAC)
+            ncu_file = os.path.join(ROOT, "profiles", f"ncu_tc_bulk_{args.config}.json")
+            roofline = {"bound": "tensor", "unit": "Tlimb-MAC/s",
+                        "kernel": "k_tc_prep + k_tc_bulk: tcgen05.mma kind::i8 limb products of the trailing "
+                                  "update (ldlt.cpp:122-129)",
+                        "peak_how": "hk_peak_i8mma: back-to-back tcgen05.mma.kind::i8 M128 N256 K32 on every SM, "
+                                    "best of 5, /16 u8 MACs per limb-MAC (MEASURED_PEAKS.json has no integer peak)",
+                        "imad_peak": api.peak_imad(local) / 1e12}
+        else:
+            peak = api.peak_imad(local) / 1e12
+            ncu_file = os.path.join(ROOT, "profiles", f"ncu_trailing_{args.config}.json")
+            roofline = {"bound": "imad", "unit": "Tlimb-MAC/s",
+                        "kernel": "trailing update k_items_hot<ItemTrailing2> (ldlt.cpp:122-129)",
+                        "peak_how": "hk_peak_imad: register-only IMAD.WIDE carry-chain microkernel, best of 5 "
+                                    "(MEASURED_PEAKS.json has no integer peak)"}
+        roofline.update({
+            "achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
+            "per_launch": f"{int(steps_k)} launches per step (one per LDLT step i with columns >= i+2), "
+                          f"avg {ms_k / steps_k:.4f} ms, {bulk_macs / steps_k:.3e} algorithmic limb-MACs",
+            "algorithmic_units": "L^2 limb-MACs per MP-FMA (SURVEY 8d); the tensor-core kernel forms the short "
+                                 "product (byte columns >= limb L-8, ~half of L^2), so frac can exceed the MMA "
+                                 "utilisation (up to ~2x)",
+            "how_timed": "event-record nodes in the captured LDLT graph around each step's product launches, "
+                         "summed over the step and averaged over the timed steps",
+            "share_of_ldlt": ms_k / ldlt_ms if ldlt_ms > 0 else None,
+            "kernel_ms_per_step": kt,
+        })
+        if kt.get("round_ms", 0.0) > 0:
+            round_bytes = sum((n - i - 2) * (n - i - 1) // 2 for i in range(n)) * (12 * L + 32)
+            gbps = round_bytes / (kt["round_ms"] * 1e-3) / 1e9
+            roofline["rounding_pass"] = {"kernel": "k_cols<ItemTcRound> + k_tc_fix", "ms": kt["round_ms"],
+                                         "bound": "hbm", "achieved_GBps": gbps, "peak_GBps": hbm_peak_gbps(),
+                                         "frac": gbps / hbm_peak_gbps(),
+                                         "bytes": "12 L + 32 per MP-FMA (read c, read product, write c)"}
+        if os.path.exists(ncu_file):
+            roofline["traffic"] = json.load(open(ncu_file)).get("dram_bytes_per_launch")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -340,25 +396,30 @@ def bench_ours(args, cfg):
         "data": "exact-integer moments (deterministic, no dataset)",
         "config": workload_config(args, cfg, world),
         "time_to_lambda_ms": ms,
-        "lambda_min": repr(lam[0][0] + lam[1][0]),
+        "lambda_min": repr(lam[0][0] + lam[1][0]) if rank == 0 else None,
         "parity": lambda_parity(args.config, cfg, lam) if rank == 0 else None,
         "e2e": {"value": fmas(n) / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "includes": "host moment generation (hk_moments into pinned memory) + hk_compute"},
         "roofline": roofline,
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }
+    if world > 1:
+        line["comm"] = {"broadcast_ms_per_step_rank0": kt.get("comm_ms"), "broadcasts": kt.get("comm_steps"),
+                        "what": "device time of this rank's pivot-column ncclBroadcasts incl. the wait for their "
+                                "root (WorkerTimings::comm_s, ldlt.cpp:214-263)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = os.cpu_count() or 1
-            rec = run_reference_once(cfg, cores)
-            n_s = cfg.get("cpu_n", n)
+            n_s = CPU_SAMPLE_N[args.config]
+            rec = run_reference_once(cfg, cores, cfg["K_equiv"], n=n_s)
             line["cpu_baseline"] = {
                 "value": fmas(n_s) / rec["timing"]["wall_s"], "unit": UNIT, "cores": cores, "kind": "reference",
-                "sample": f"1 full hankel::compute of {args.config}"
-                          + (f" restricted to its leading N={n_s} block" if n_s != n else "")
-                          + f" (reference via oracle/_ref, K={cfg['K_ref']}, workers={cores}): "
-                            f"wall_s {rec['timing']['wall_s']:.3f}, ldlt_s {rec['timing']['ldlt_s']:.3f}"}
+                "sample": f"1 hankel::compute of the reference (oracle/_ref, K={cfg['K_equiv']} = K_equiv, "
+                          f"workers={cores}) on the leading N={n_s} block of {args.config}'s H_N (bounded sample; "
+                          f"`--impl reference` times the whole workload): wall_s {rec['timing']['wall_s']:.3f}, "
+                          f"ldlt_s {rec['timing']['ldlt_s']:.3f}"}
         except Exception as e:  # the baseline is reported, not required
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"unavailable: {e}"}
@@ -370,16 +431,32 @@ def bench_ours(args, cfg):
     return 0
 
 
+def relaunch_distributed(n):
+    """`bench.py --gpus N` outside torchrun: one rank per GPU via torch.distributed.run."""
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the NCCL column-sharded path even on 1 GPU")
+    ap.add_argument("--ref-budget-s", type=float, default=480.0,
+                    help="reference arm: wall-clock budget for its full runs (at least one runs)")
+    ap.add_argument("--ref-golden-precision", action="store_true",
+                    help="reference arm: also time one full run at the golden runs' K (K_ref)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args.gpus)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return bench_reference(args, cfg)

@@ -59,6 +59,12 @@ const char* hk_last_error(const hk_ctx* ctx);
 int hk_bad_column(const hk_ctx* ctx);
 int hk_limbs(const hk_ctx* ctx);
 
+/* Change the context's precision p = 32*limbs (drops the cached buffers and
+ * graphs, keeps the device streams and — for a sharded context — the NCCL
+ * communicator, so auto_precision / scan (pipeline.cpp:74-122) re-run at a new
+ * K on the same communicator).  A no-op when limbs is unchanged. */
+int hk_set_limbs(hk_ctx* ctx, int limbs);
+
 /* Host-side exact moments mu_0..mu_{count-1} of w(x)=exp(-x^beta) as p-bit
  * floats (moments.cpp:80-111: gamma_exact + moment, the factorial path; the
  * half-integer sqrt(pi) path is not implemented -> HK_ERR_INVALID).
@@ -142,6 +148,18 @@ void* hk_stream(const hk_ctx* ctx);
  * *n_trailing the number of trailing steps. */
 int hk_profile_ldlt(hk_ctx* ctx, double* ms7, long long* n_trailing);
 
+/* Measurement hook: with hk_set_kernel_timing(ctx, 1) the captured LDLT graph
+ * carries event-record nodes around every step's bulk kernels, and
+ * hk_kernel_times returns, for the last hk_ldlt: out6[0] summed milliseconds of
+ * the limb-product kernels (tensor-core A preformat + products, or the IMAD
+ * trailing kernel), [1] of the certified rounding + fix-up pass, [2] the number
+ * of timed steps; for a sharded context (always recorded) [3] summed ms of the
+ * pivot-column broadcasts including the wait for their root — the reference's
+ * WorkerTimings::comm_s (ldlt.cpp:214-263, 341) — and [4] their count; [5] the
+ * LDLT's own time (ms). */
+int hk_set_kernel_timing(hk_ctx* ctx, int on);
+int hk_kernel_times(hk_ctx* ctx, double* out6);
+
 /* Measured integer-MAC peak of the device: 32x32->64-bit limb MACs per second
  * of the IMAD.WIDE carry chain the MP kernels use (register-only microkernel
  * over all SMs).  The roofline denominator for the IMAD path. */
@@ -164,7 +182,8 @@ int hk_peak_i8mma(int device, double* u8_macs_per_s);
  * With nccl_id128 == NULL all `world` ranks are emulated inside this one
  * context on one device (broadcast = device-to-device copy): the sharded
  * kernels and maps, testable on a single GPU; rank must then be 0.
- * On ranks != 0, hk_compute returns HK_OK with *s_out = 0 (no lambdas). */
+ * hk_compute returns rank 0's status and lambdas on every rank (one small
+ * broadcast), so the callers' precision-search loops agree across ranks. */
 int hk_nccl_unique_id(void* out128);
 int hk_create_sharded(int device, int limbs, int rank, int world, const void* nccl_id128, hk_ctx** out);
 int hk_world(const hk_ctx* ctx, int* rank, int* world);

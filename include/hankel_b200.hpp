@@ -265,6 +265,19 @@ public:
 
     hk_ctx* handle() const noexcept { return h_; }
     int limbs() const { return hk_limbs(h_); }
+    // new precision on the same device / communicator (invalidates earlier factor handles)
+    void set_limbs(int limbs) {
+        if (limbs == this->limbs()) return;
+        check(hk_set_limbs(h_, limbs));
+        ++gen_;
+        ++inv_gen_;
+    }
+    // kernel_times()[3]: device ms of this rank's pivot-column broadcasts in the last LDLT
+    std::vector<double> kernel_times() const {
+        std::vector<double> t(6);
+        check(hk_kernel_times(h_, t.data()));
+        return t;
+    }
     int bits() const { return 32 * limbs(); }
     int rank() const {
         int r = 0, w = 1;
@@ -372,9 +385,10 @@ inline LdltFactors decompose_parallel(Device& dev, const MomentTable& table, Wor
         f.D = MpVector(size_t(n), f.limbs);
         dev.check(hk_get_D(dev.handle(), f.D.pl(), f.D.pe(), f.D.ps()));
     }
-    if (host_timings) {
-        host_timings->arith_s = dev.timings()[1];
-        host_timings->comm_s = 0.0;
+    if (host_timings) { // ldlt.cpp:214-263, 341: comm = waiting on / moving the pivot column
+        const double comm = dev.kernel_times()[3] * 1e-3;
+        host_timings->comm_s = comm;
+        host_timings->arith_s = dev.timings()[1] - comm;
     }
     return f;
 }
@@ -618,6 +632,25 @@ inline int precision_bits(const WeightSpec& spec, int n, long K) {
     return int(128 * ((need + 127) / 128));
 }
 
+namespace detail {
+// One Device per (device, rank, workers, communicator id), reused by every
+// compute() call of this thread: auto_precision / scan change only p
+// (hk_set_limbs), so buffers are re-sized, not re-created, and a multi-GPU
+// group keeps its one NCCL communicator (an ncclUniqueId serves one init).
+inline Device& compute_device(const ComputeOptions& o, int limbs) {
+    thread_local std::map<std::string, std::unique_ptr<Device>> devs;
+    std::string key = std::to_string(o.device) + "/" + std::to_string(o.rank) + "/" + std::to_string(o.workers) + "/";
+    if (o.nccl_id128) key.append(static_cast<const char*>(o.nccl_id128), 128);
+    auto& d = devs[key];
+    if (!d)
+        d = o.workers == 1 && !o.nccl_id128 ? std::make_unique<Device>(limbs, o.device)
+                                            : std::make_unique<Device>(limbs, o.device, o.rank, o.workers, o.nccl_id128);
+    else
+        d->set_limbs(limbs);
+    return *d;
+}
+} // namespace detail
+
 // pipeline.cpp:26-72: upload -> LDLT -> L^{-1} -> block -> eigen, one device call
 inline RunRecord compute(const ComputeOptions& opts) {
     if (opts.n < 1) throw std::invalid_argument("compute: need N >= 1");
@@ -627,9 +660,7 @@ inline RunRecord compute(const ComputeOptions& opts) {
     const int p = precision_bits(opts.beta, opts.n, opts.bits);
     const MomentTable table = build_hankel(opts.beta, opts.n, p / 32);
     if (!table.exact()) throw precision_error("compute: moments not exact at p bits");
-    Device dev = opts.workers == 1 && !opts.nccl_id128
-                     ? Device(p / 32, opts.device)
-                     : Device(p / 32, opts.device, opts.rank, opts.workers, opts.nccl_id128);
+    Device& dev = detail::compute_device(opts, p / 32);
     double hi[3], lo[3], te[3];
     int s = 0;
     const MpVector& mu = table.moments();

@@ -71,6 +71,9 @@ def lib():
             "hk_nccl_unique_id": (C.c_int, [C.c_char_p]),
             "hk_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]),
             "hk_world": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+            "hk_set_limbs": (C.c_int, [vp, C.c_int]),
+            "hk_set_kernel_timing": (C.c_int, [vp, C.c_int]),
+            "hk_kernel_times": (C.c_int, [vp, f64p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -142,9 +145,13 @@ def _check(rc: int, ctx=None):
     raise RuntimeError(msg)
 
 
-def build_hankel(beta: tuple[int, int], n: int, limbs: int) -> tuple[MPArray, bool]:
-    """The 2n-1 exact moments as p-bit floats (moments.cpp:102-133 / build_hankel)."""
-    out = MPArray.empty(2 * n - 1, limbs)
+def build_hankel(beta: tuple[int, int], n: int, limbs: int, out: MPArray | None = None) -> tuple[MPArray, bool]:
+    """The 2n-1 exact moments as p-bit floats (moments.cpp:102-133 / build_hankel),
+    written into `out` when given (e.g. pinned host arrays)."""
+    if out is None:
+        out = MPArray.empty(2 * n - 1, limbs)
+    elif len(out) != 2 * n - 1 or out.L != limbs:
+        raise ValueError("build_hankel: `out` has the wrong shape")
     exact = C.c_int(0)
     _check(lib().hk_moments(beta[0], beta[1], 2 * n - 1, limbs, *out.ptrs(), C.byref(exact)))
     return out, bool(exact.value)
@@ -329,6 +336,22 @@ class Context:
         _check(lib().hk_profile_ldlt(self.h, ms.ctypes.data_as(C.POINTER(C.c_double)), C.byref(n)), self.h)
         keys = ("trailing", "recip", "mulB", "storeL", "total", "tc_products", "tc_round")
         return dict(zip(keys, ms.tolist())), n.value
+
+    def set_limbs(self, limbs: int):
+        """New precision on the same device / communicator (hk_set_limbs)."""
+        _check(lib().hk_set_limbs(self.h, limbs), self.h)
+        self.L = limbs
+
+    def set_kernel_timing(self, on: bool = True):
+        _check(lib().hk_set_kernel_timing(self.h, 1 if on else 0), self.h)
+
+    def kernel_times(self) -> dict:
+        """hk_kernel_times of the last LDLT: summed device ms of the product kernels, the rounding
+        pass, timed steps, the pivot-column broadcasts (sharded) and their count, LDLT ms."""
+        t = np.zeros(6)
+        _check(lib().hk_kernel_times(self.h, t.ctypes.data_as(C.POINTER(C.c_double))), self.h)
+        keys = ("products_ms", "round_ms", "steps", "comm_ms", "comm_steps", "ldlt_ms")
+        return dict(zip(keys, t.tolist()))
 
     def launch_count(self) -> int:
         return int(lib().hk_launch_count(self.h))

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -71,6 +72,66 @@ void launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bo
     if (e != cudaSuccess) throw HkError{HK_ERR_RUNTIME, std::string("kernel launch: ") + cudaGetErrorString(e)};
 }
 
+// Dynamic shared-memory limit (>= 48 KB) and the maximal carveout of kernel
+// `fn`, set once per (device, kernel): the attribute belongs to the current
+// device's context, so a process driving several GPUs sets it on each.
+void func_smem(const void* fn, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    const size_t v = smem < 48 * 1024 ? 48 * 1024 : smem;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = done[{dev, fn}];
+    if (cur >= v) return;
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v)), "cudaFuncSetAttribute");
+    // every kernel asks for the same (maximal) shared-memory carveout, so the
+    // critical-path CTAs can start on SMs busy with bulk work without an L1/smem
+    // reconfiguration (which waits for the SM to drain)
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+    cur = v;
+}
+
+// Stream capture that always ends: if recording throws, the capture (and every
+// stream forked into it) is closed and the partial graph dropped, so the
+// context stays usable after a failed launch.
+struct Capture {
+    cudaStream_t st;
+    bool open = false;
+    explicit Capture(cudaStream_t s) : st(s) {
+        ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+        open = true;
+    }
+    cudaGraph_t end() {
+        cudaGraph_t g = nullptr;
+        open = false;
+        ck(cudaStreamEndCapture(st, &g), "end capture");
+        return g;
+    }
+    ~Capture() {
+        if (!open) return;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError(); // clear the sticky-free capture error
+    }
+};
+
+cudaGraphExec_t instantiate(cudaGraph_t g, unsigned long long flags) {
+    cudaGraphExec_t ge = nullptr;
+    const cudaError_t e = cudaGraphInstantiateWithFlags(&ge, g, flags);
+    cudaGraphDestroy(g);
+    ck(e, "graph instantiate");
+    return ge;
+}
+
+// D_i = S(i, i) of the jagged triangle -> contiguous out[0..N) (one copy back)
+__global__ void k_gather_diag(MpArr S, MpArr out, int N, int L) {
+    const long long e = hk::tri_idx(int(blockIdx.x), int(blockIdx.x), N);
+    for (int q = threadIdx.x; q < L; q += blockDim.x) out.limbs(blockIdx.x, L)[q] = S.limbs(e, L)[q];
+    if (threadIdx.x == 0) out.m[blockIdx.x] = S.m[e];
+}
+
 struct DevArr {
     uint32_t* d = nullptr;
     Meta* m = nullptr;
@@ -107,7 +168,7 @@ struct hk_ctx {
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
     std::vector<cudaEvent_t> evP, evR, evU, evD, evO, evC, evB1; // per-step dependencies (graph capture)
     cudaEvent_t evJoin2 = nullptr, evJoin3 = nullptr;
-    DevArr mu, S, R, B, X, Y, T, T2, M;
+    DevArr mu, S, R, B, X, Y, T, T2, M, Dg;
     int* d_err = nullptr;
     std::string err;
     int bad_col = -1;
@@ -119,16 +180,19 @@ struct hk_ctx {
     // LDLT graph cache keyed by n
     std::map<int, cudaGraphExec_t> graphs;
     std::map<int, long long> graph_launches;
-    const void* graph_bufs[3] = {nullptr, nullptr, nullptr}; // S, R, B the graphs were captured on
-    const void* graph_tcp = nullptr;                         // tc scratch they were captured on
-    bool graph_tc = false;
+    std::vector<const void*> graph_sig;                      // buffers / modes the graphs were captured on
     std::map<long long, cudaGraphExec_t> inv_graphs;         // L^{-1} step graphs keyed by (n, m)
     std::map<long long, long long> inv_graph_launches;
-    const void* inv_bufs[3] = {nullptr, nullptr, nullptr};   // S, X, TC scratch they were captured on
-    const void* inv_flow_buf = nullptr;                      // dataflow flags they were captured on
-    bool inv_flow_mode = false;                              // dataflow kernel instead of N steps
+    std::vector<const void*> inv_sig;                        // buffers / modes they were captured on
     std::vector<uint32_t> h_limbs;
     std::vector<int32_t> h_e, h_s;
+    // ---- kernel timing inside the captured graphs (external event-record nodes)
+    bool kprof = false;                 // hk_set_kernel_timing: events around every step's bulk kernels
+    std::vector<cudaEvent_t> kev;       // 3 per LDLT step: before products, after products, after rounding
+    int kev_steps = 0;                  // steps recorded in the LDLT graph launched last
+    std::map<int, int> kev_steps_by_n;  // ... per cached graph (keyed by n)
+    std::vector<cudaEvent_t> cev;       // sharded: 2 per step around the pivot-column broadcast (always on)
+    int cev_steps = 0;
     // ---- tensor-core bulk products (large p): scratch of short products
     uint32_t* tc_P = nullptr;
     size_t tc_P_words = 0;
@@ -161,6 +225,7 @@ struct hk_ctx {
     int world = 1, rank = 0;
     bool virt = false;               // all `world` ranks emulated in this one context
     void* nccl_comm = nullptr;       // ncclComm_t (one rank per process)
+    void* bcast_buf = nullptr;       // device staging of the root's result broadcast
     std::vector<Shard> shards;
     std::vector<int> owner;          // assign_columns(n, world)
 };
@@ -183,17 +248,9 @@ void launch(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t st = 
     if (wpb < 1) wpb = 1;
     if ((long long)wpb > n) wpb = int(n);
     const size_t smem = per_warp * wpb;
-    static std::map<const void*, size_t> configured;
-    const void* key = (const void*)&k_items<F>;
-    auto it = configured.find(key);
-    if (it == configured.end() || it->second < smem) {
-        ck(cudaFuncSetAttribute(k_items<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem < 48 * 1024 ? 48 * 1024 : smem)),
-           "cudaFuncSetAttribute");
-        // all of the unified L1/shared array as shared memory: residency is then
-        // register-bound (5 x 256-thread blocks at <= 48 registers)
-        ck(cudaFuncSetAttribute(k_items<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        configured[key] = smem < 48 * 1024 ? 48 * 1024 : smem;
-    }
+    // all of the unified L1/shared array as shared memory: residency is then
+    // register-bound (5 x 256-thread blocks at <= 48 registers)
+    func_smem((const void*)&k_items<F>, smem);
     long long blocks = (n + wpb - 1) / wpb;
     const long long cap = 1LL << 30;
     if (blocks > cap) blocks = cap;
@@ -222,15 +279,7 @@ void launch_hot(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t s
     if (wpb < 1) wpb = 1;
     if ((long long)wpb > n) wpb = int(n);
     const size_t smem = per_warp * wpb;
-    static std::map<const void*, size_t> configured;
-    const void* key = (const void*)&k_items_hot<F>;
-    auto it = configured.find(key);
-    if (it == configured.end() || it->second < smem) {
-        const size_t v = smem < 48 * 1024 ? 48 * 1024 : smem;
-        ck(cudaFuncSetAttribute(k_items_hot<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v)), "attr");
-        ck(cudaFuncSetAttribute(k_items_hot<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        configured[key] = v;
-    }
+    func_smem((const void*)&k_items_hot<F>, smem);
     const long long blocks = (n + wpb - 1) / wpb;
     k_items_hot<F><<<unsigned(blocks), unsigned(32 * wpb), smem, st>>>(n, ws_words, f);
     ck(cudaGetLastError(), "kernel launch");
@@ -257,19 +306,7 @@ void launch_cta(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t s
     if (n <= 0) return;
     if (!st) st = c->st;
     const size_t smem = size_t(ws_words) * sizeof(uint32_t);
-    static std::map<const void*, size_t> configured;
-    const void* key = (const void*)&k_cta_items<F>;
-    auto it = configured.find(key);
-    if (it == configured.end() || it->second < smem) {
-        const size_t v = smem < 48 * 1024 ? 48 * 1024 : smem;
-        ck(cudaFuncSetAttribute(k_cta_items<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v)),
-           "cudaFuncSetAttribute");
-        // every kernel asks for the same (maximal) shared-memory carveout, so the
-        // critical-path CTAs can start on SMs busy with bulk work without an L1/smem
-        // reconfiguration (which waits for the SM to drain)
-        ck(cudaFuncSetAttribute(k_cta_items<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        configured[key] = v;
-    }
+    func_smem((const void*)&k_cta_items<F>, smem);
     const long long blocks = n < (1LL << 30) ? n : (1LL << 30);
     if (pdl) {
         cudaLaunchConfig_t cfg{};
@@ -318,20 +355,6 @@ void h2d_soa(hk_ctx* c, DevArr& a, long long n, const uint32_t* l, const int32_t
     for (long long i = 0; i < n; ++i) hm[size_t(i)] = Meta{e[i], s[i]};
     ck(cudaMemcpyAsync(a.m, hm.data(), size_t(n) * sizeof(Meta), cudaMemcpyHostToDevice, c->st), "H2D meta");
     ck(cudaStreamSynchronize(c->st), "sync");
-}
-
-// Gather `n` entries (device indices idx[]) into host SoA.
-void d2h_gather(hk_ctx* c, const DevArr& a, const std::vector<long long>& idx, uint32_t* l, int32_t* e, int32_t* s) {
-    const int L = c->L;
-    std::vector<Meta> hm(1);
-    for (size_t q = 0; q < idx.size(); ++q) {
-        ck(cudaMemcpyAsync(l + q * L, a.d + idx[q] * L, size_t(L) * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st),
-           "D2H limbs");
-        ck(cudaMemcpyAsync(&hm[0], a.m + idx[q], sizeof(Meta), cudaMemcpyDeviceToHost, c->st), "D2H meta");
-        ck(cudaStreamSynchronize(c->st), "sync");
-        e[q] = hm[0].exp;
-        s[q] = hm[0].sign;
-    }
 }
 
 void d2h_range(hk_ctx* c, const DevArr& a, long long first, long long n, uint32_t* l, int32_t* e, int32_t* s) {
@@ -412,13 +435,8 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     a.nacc = need <= 110 * 1024 ? 1 : 2;
     if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
     const size_t smem = a.nacc == 1 ? need : std::max(need, size_t(120 * 1024));
-    static bool configured = false;
-    if (!configured) {
-        ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024), "tc attr");
-        ck(cudaFuncSetAttribute(hk::k_tc_bulk, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        ck(cudaFuncSetAttribute(hk::k_tc_prep, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        configured = true;
-    }
+    func_smem((const void*)hk::k_tc_bulk, 220 * 1024);
+    func_smem((const void*)hk::k_tc_prep, 0);
     static const char* dv = getenv("HK_DEV_TCB"); // dev what-if (tools only): bits of TcBulkArgs::dev
     a.dev = dv ? atoi(dv) : 0;
     const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
@@ -441,12 +459,7 @@ void launch_cols(hk_ctx* c, const F& f, int ncols, int maxrows, int ws_words, cu
     int wpb = int((96 * 1024) / per_warp);
     wpb = std::max(1, std::min(8, wpb));
     const size_t smem = per_warp * wpb;
-    static bool cfg = false;
-    if (!cfg) {
-        ck(cudaFuncSetAttribute(hk::k_cols<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024), "cols attr");
-        ck(cudaFuncSetAttribute(hk::k_cols<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        cfg = true;
-    }
+    func_smem((const void*)hk::k_cols<F>, 96 * 1024);
     const unsigned gx = unsigned((maxrows + wpb - 1) / wpb);
     launch_ex(hk::k_cols<F>, dim3(gx, unsigned(ncols)), dim3(unsigned(32 * wpb)), smem, st, pdl, f, ws_words);
     ck(cudaGetLastError(), "cols launch");
@@ -458,33 +471,54 @@ template <class F>
 void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset, bool pdl = false) {
     const int wo = ws_op_words(c->L);
     const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
-    static bool cfg = false;
-    if (!cfg) {
-        ck(cudaFuncSetAttribute(hk::k_tc_fix<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "fix attr");
-        ck(cudaFuncSetAttribute(hk::k_tc_fix<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        cfg = true;
-    }
+    func_smem((const void*)hk::k_tc_fix<F>, 200 * 1024);
     launch_ex(hk::k_tc_fix<F>, dim3(unsigned(c->sm_count)), dim3(unsigned(32 * wpb)), size_t(wo) * 4 * wpb, st, pdl, f,
               (const int*)count, (const long long*)c->tc_fb, wo, reset);
     ck(cudaGetLastError(), "tc fix launch");
     ++c->launches;
 }
 
+void grow_events(std::vector<cudaEvent_t>& v, size_t n, unsigned flags) {
+    while (v.size() < n) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, flags), "event");
+        v.push_back(e);
+    }
+}
+
+// an event-record node of the graph being captured on `st` (timing events)
+void graph_event(cudaEvent_t e, cudaStream_t st) {
+    ck(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "event record node");
+}
+
+float event_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+    return ms;
+}
+
 // Step-i update of columns jfirst..N-1 (bulk): IMAD paired warp FMAs, or the
-// tcgen05 product kernel followed by the certified rounding pass.
-void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = false) {
+// tcgen05 product kernel followed by the certified rounding pass.  kslot >= 0:
+// timing events kev[3 kslot ..] around the products and the rounding pass.
+void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = false, int kslot = -1) {
     const int N = c->n, L = c->L;
     const int ncols = N - jfirst;
     if (ncols <= 0) return;
+    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot)], st);
     if (!use_tc(c)) {
         launch_hot(c, hk::ItemTrailing2{c->S.view(), b_buf(c, i), N, L, i, jfirst, c->d_err},
                    hk::trailing2_items(N, jfirst), hk::opws2_words(L), st);
+        if (kslot >= 0) {
+            graph_event(c->kev[size_t(3 * kslot + 1)], st);
+            graph_event(c->kev[size_t(3 * kslot + 2)], st);
+        }
         return;
     }
     if (!dev_skip("prod"))
         tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
                     b_buf(c, i), unsigned(ncols), st, pdl);
     if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
+    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 1)], st);
     // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
     int* cnt = c->tc_fb_count + (i & 1);
     int* nxt = c->tc_fb_count + ((i + 1) & 1);
@@ -495,6 +529,7 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = fals
     if (!dev_skip("round"))
         launch_cols(c, ri, ncols, ncols, ri.direct ? hk::align4(L + 16) : hk::tcround_words(L), st, pdl);
     if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st, cnt, nxt, pdl);
+    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 2)], st);
 }
 
 // L^-1 step i on the tensor cores (same product kernel, mode 1).
@@ -646,13 +681,7 @@ void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
     const int sleep_ns = sl ? atoi(sl) : 100;
     const int wsw = 2 * hk::align4(L) + hk::ctaws_words(L);
     const size_t smem = size_t(wsw) * sizeof(uint32_t);
-    static bool cfg2 = false;
-    if (!cfg2) {
-        ck(cudaFuncSetAttribute(k_inv_flow_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-           "flow attr");
-        ck(cudaFuncSetAttribute(k_inv_flow_cta, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-        cfg2 = true;
-    }
+    func_smem((const void*)k_inv_flow_cta, 200 * 1024);
     const int threads = kFlowThreads;
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inv_flow_cta, threads, smem), "occupancy");
@@ -719,9 +748,13 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     ck(cudaEventRecord(evP[0], la), "evP");
     // bulk: U(i) -> evU(i) -> StoreL(i-1) -> evR(i-1);  LA: [evU(i-1)] P(i+1) with
     // MulB(i+1) (overwrites buffer (i+1) % 3 = that of B_{i-2}) after [evR(i-2)].
+    c->kev_steps = 0;
+    if (c->kprof) grow_events(c->kev, size_t(3 * N), cudaEventDefault);
     for (int i = 0; i < N; ++i) {
         ck(cudaStreamWaitEvent(bulk, evP[i], 0), "wait P");
-        enqueue_bulk(c, i, i + 2, bulk, pdl);
+        const bool timed = c->kprof && N - i - 2 > 0;
+        enqueue_bulk(c, i, i + 2, bulk, pdl, timed ? c->kev_steps : -1);
+        if (timed) ++c->kev_steps;
         ck(cudaEventRecord(evU[i], bulk), "evU");
         if (i >= 1) {
             // StoreL(i-1) on the side stream: column i-1 was last read by U(i-1)
@@ -807,6 +840,19 @@ int check_pivots(hk_ctx* c) {
 }
 
 int dist_ldlt(hk_ctx* c); // multi-GPU factorisation (below)
+int share_root_result(hk_ctx* c, int* rc, int s, double* hi, double* lo, double* te); // (below)
+
+void drop_graphs(hk_ctx* c) {
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : c->inv_graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    c->inv_graphs.clear();
+    c->graph_sig.clear();
+    c->inv_sig.clear();
+    if (c->dist_graph) cudaGraphExecDestroy(c->dist_graph);
+    c->dist_graph = nullptr;
+    c->dist_sig.clear();
+}
 
 } // namespace
 
@@ -853,9 +899,8 @@ int hk_create(int device, int limbs, hk_ctx** out) {
 void hk_destroy(hk_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
-    for (auto& kv : c->inv_graphs) cudaGraphExecDestroy(kv.second);
-    for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M}) a->release();
+    drop_graphs(c);
+    for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg}) a->release();
     for (auto& s : c->shards) {
         for (DevArr* a : {&s.S, &s.panel, &s.R, &s.B}) a->release();
         if (s.d_erow) cudaFree(s.d_erow);
@@ -865,13 +910,13 @@ void hk_destroy(hk_ctx* c) {
         if (s.d_off) cudaFree(s.d_off);
         if (s.d_fb) cudaFree(s.d_fb);
     }
-    if (c->dist_graph) cudaGraphExecDestroy(c->dist_graph);
     if (c->nccl_comm) {
         void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         auto destroy = h ? (int (*)(void*))dlsym(h, "ncclCommDestroy") : nullptr;
         if (destroy) destroy(c->nccl_comm);
     }
     if (c->d_err) cudaFree(c->d_err);
+    if (c->bcast_buf) cudaFree(c->bcast_buf);
     if (c->tc_P) cudaFree(c->tc_P);
     if (c->tc_fb) cudaFree(c->tc_fb);
     if (c->tc_fb_count) cudaFree(c->tc_fb_count);
@@ -887,6 +932,8 @@ void hk_destroy(hk_ctx* c) {
     for (auto e : c->evO) cudaEventDestroy(e);
     for (auto e : c->evC) cudaEventDestroy(e);
     for (auto e : c->evB1) cudaEventDestroy(e);
+    for (auto e : c->kev) cudaEventDestroy(e);
+    for (auto e : c->cev) cudaEventDestroy(e);
     if (c->evJoin2) cudaEventDestroy(c->evJoin2);
     if (c->evJoin3) cudaEventDestroy(c->evJoin3);
     if (c->st4) cudaStreamDestroy(c->st4);
@@ -939,32 +986,29 @@ int hk_ldlt(hk_ctx* c) {
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         ck(cudaEventRecord(c->ev[0], c->st), "event");
         launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
-        if (c->graph_bufs[0] != c->S.d || c->graph_bufs[1] != c->R.d || c->graph_bufs[2] != c->B.d ||
-            c->graph_tcp != c->tc_P || c->graph_tc != use_tc(c)) {
-            c->graph_tcp = c->tc_P;
-            c->graph_tc = use_tc(c);
+        // the cached step graphs are valid for the buffers and modes they were captured on
+        const std::vector<const void*> sig{c->S.d, c->S.m, c->R.d, c->B.d, c->mu.d, c->tc_P, c->tc_A, c->tc_fb,
+                                           c->tc_fb_count, (const void*)(long long)use_tc(c),
+                                           (const void*)(long long)c->kprof};
+        if (sig != c->graph_sig) {
             for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
             c->graphs.clear();
-            c->graph_bufs[0] = c->S.d;
-            c->graph_bufs[1] = c->R.d;
-            c->graph_bufs[2] = c->B.d;
+            c->graph_sig = sig;
         }
         auto it = c->graphs.find(N);
         if (it == c->graphs.end()) {
-            cudaGraph_t g;
             const long long before = c->launches;
-            ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            Capture cap(c->st);
             enqueue_ldlt_steps(c);
-            ck(cudaStreamEndCapture(c->st, &g), "end capture");
-            cudaGraphExec_t ge;
-            ck(cudaGraphInstantiateWithFlags(&ge, g, cudaGraphInstantiateFlagUseNodePriority), "graph instantiate");
-            cudaGraphDestroy(g);
+            const cudaGraphExec_t ge = instantiate(cap.end(), cudaGraphInstantiateFlagUseNodePriority);
             it = c->graphs.emplace(N, ge).first;
             c->graph_launches[N] = c->launches - before;
+            c->kev_steps_by_n[N] = c->kev_steps;
             c->launches = before;
         }
         ck(cudaGraphLaunch(it->second, c->st), "graph launch");
         c->launches += c->graph_launches[N];
+        c->kev_steps = c->kev_steps_by_n[N];
         ck(cudaEventRecord(c->ev[1], c->st), "event");
         ck(cudaEventSynchronize(c->ev[1]), "sync");
         float ms = 0;
@@ -981,9 +1025,10 @@ int hk_ldlt(hk_ctx* c) {
 int hk_get_D(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
     return guarded(c, [&] {
         if (!c->factored) return fail(c, HK_ERR_INVALID, "hk_get_D: not factored");
-        std::vector<long long> idx(size_t(c->n));
-        for (int i = 0; i < c->n; ++i) idx[size_t(i)] = hk::tri_idx(i, i, c->n);
-        d2h_gather(c, c->S, idx, limbs, exps, signs);
+        c->Dg.ensure(c->n, c->L);
+        k_gather_diag<<<unsigned(c->n), 128, 0, c->st>>>(c->S.view(), c->Dg.view(), c->n, c->L);
+        ck(cudaGetLastError(), "gather launch");
+        d2h_range(c, c->Dg, 0, c->n, limbs, exps, signs);
         return HK_OK;
     });
 }
@@ -1011,23 +1056,20 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
         const bool flow = !tc && (fe ? fe[0] != '0' : true);
         if (flow) ensure_inv_flow(c, (long long)N * m);
         ensure_tc_scratch(c, m);
-        // all N steps in one cached graph (invalidated when a buffer moves)
-        if (c->inv_bufs[0] != c->S.d || c->inv_bufs[1] != c->X.d || c->inv_bufs[2] != c->tc_P ||
-            c->inv_flow_buf != c->flow_ready || c->inv_flow_mode != flow) {
-            c->inv_flow_buf = c->flow_ready;
-            c->inv_flow_mode = flow;
+        // all N steps in one cached graph (invalidated when a buffer or mode changes)
+        const std::vector<const void*> sig{c->S.d, c->S.m, c->X.d, c->tc_P, c->tc_A, c->tc_fb, c->tc_fb_count,
+                                           c->tc_gcarry, c->flow_ready, (const void*)(long long)flow,
+                                           (const void*)(long long)tc};
+        if (sig != c->inv_sig) {
             for (auto& kv : c->inv_graphs) cudaGraphExecDestroy(kv.second);
             c->inv_graphs.clear();
-            c->inv_bufs[0] = c->S.d;
-            c->inv_bufs[1] = c->X.d;
-            c->inv_bufs[2] = c->tc_P;
+            c->inv_sig = sig;
         }
         const long long key = ((long long)N << 20) | m;
         auto it = c->inv_graphs.find(key);
         if (it == c->inv_graphs.end()) {
             const long long before = c->launches;
-            cudaGraph_t g;
-            ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            Capture cap(c->st);
             if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), c->st), "memset fb counters");
             launch(c, hk::ItemInvInit{c->S.view(), c->X.view(), N, L, m}, (long long)N * m, 64);
             if (flow) enqueue_inv_flow(c, c->st);
@@ -1045,10 +1087,7 @@ int hk_invert_L_partial(hk_ctx* c, int m) {
                 else
                     launch(c, hk::ItemInvStep{c->S.view(), c->X.view(), N, L, m, i}, items, ws_op_words(L));
             }
-            ck(cudaStreamEndCapture(c->st, &g), "end capture");
-            cudaGraphExec_t ge;
-            ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
-            cudaGraphDestroy(g);
+            const cudaGraphExec_t ge = instantiate(cap.end(), 0);
             it = c->inv_graphs.emplace(key, ge).first;
             c->inv_graph_launches[key] = c->launches - before;
             c->launches = before;
@@ -1148,17 +1187,46 @@ int hk_compute(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, con
     const int s = kk < 3 ? kk : 3;   // pipeline.cpp:64
     int rc = hk_load_moments(c, n, limbs, exps, signs);
     if (rc == HK_OK) rc = hk_ldlt(c);
-    if (rc == HK_OK && c->rank != 0) { // results live on rank 0 (columns gathered there)
-        if (s_out) *s_out = 0;
-        c->t[0] = now_s() - t0;
-        return HK_OK;
+    // the columns are gathered on rank 0, which runs the rest of the path
+    const bool root = c->rank == 0;
+    if (rc == HK_OK && root) rc = hk_invert_L_partial(c, kk);
+    if (rc == HK_OK && root) rc = hk_assemble_block(c, kk);
+    if (rc == HK_OK && root) rc = hk_smallest_eigs(c, s, lambda_hi, lambda_lo, trunc_err);
+    // every rank returns rank 0's record (status, lambdas), so a caller's
+    // auto_precision / scan loop takes the same branch on every rank
+    if (c->nccl_comm && c->world > 1 && c->n == n) {
+        const int rb = share_root_result(c, &rc, s, lambda_hi, lambda_lo, trunc_err);
+        if (rb != HK_OK) rc = rb;
     }
-    if (rc == HK_OK) rc = hk_invert_L_partial(c, kk);
-    if (rc == HK_OK) rc = hk_assemble_block(c, kk);
-    if (rc == HK_OK) rc = hk_smallest_eigs(c, s, lambda_hi, lambda_lo, trunc_err);
-    if (s_out) *s_out = s;
+    if (s_out) *s_out = rc == HK_OK ? s : 0;
     c->t[0] = now_s() - t0;
     return rc;
+}
+
+int hk_set_limbs(hk_ctx* c, int limbs) {
+    if (!c || limbs < 1 || limbs > 8192) return HK_ERR_INVALID;
+    return guarded(c, [&] {
+        if (limbs == c->L) return HK_OK;
+        ck(cudaStreamSynchronize(c->st), "sync");
+        drop_graphs(c);
+        for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg}) a->release();
+        for (auto& sh : c->shards) {
+            for (DevArr* a : {&sh.S, &sh.panel, &sh.R, &sh.B}) a->release();
+            sh.setup_n = -1;
+        }
+        for (void* p : {(void*)c->tc_P, (void*)c->tc_A, (void*)c->tc_fb, (void*)c->tc_gcarry})
+            if (p) cudaFree(p);
+        c->tc_P = nullptr;
+        c->tc_A = nullptr;
+        c->tc_fb = nullptr;
+        c->tc_gcarry = nullptr;
+        c->tc_P_words = 0;
+        c->tc_A_n = 0;
+        c->L = limbs;
+        c->n = c->m = c->k = 0;
+        c->factored = c->inverted = c->assembled = false;
+        return HK_OK;
+    });
 }
 
 int hk_timings(const hk_ctx* c, double* out7) {
@@ -1549,17 +1617,22 @@ size_t first_owned(const Shard& s, int j0) {
 // column i+1 is done by P(i+1)); IMAD warp FMAs or the tensor-core products
 // (mode 2 of the product kernel) + the certified rounding pass — the same ops
 // as ItemDTrailing, bit-identical.
-void dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st) {
+bool dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st, int kslot = -1) {
     const int N = c->n, L = c->L;
     const size_t q = first_owned(s, i + 2);
     const int ncols = int(s.owned.size() - q);
-    if (ncols <= 0) return;
+    if (ncols <= 0) return false;
     const long long e0 = s.off[q], n = s.off.back() - e0;
     const MpArr panel = slot3(s.panel, N, L, i), B = slot3(s.B, N, L, i);
+    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot)], st);
     if (!tc) {
         launch(c, hk::ItemDTrailing{s.S.view(), panel, B, s.d_erow, s.d_ecol, L, i, e0, s.d_err}, n, ws_op_words(L),
                st);
-        return;
+        if (kslot >= 0) {
+            graph_event(c->kev[size_t(3 * kslot + 1)], st);
+            graph_event(c->kev[size_t(3 * kslot + 2)], st);
+        }
+        return true;
     }
     hk::TcBulkArgs a{s.S.view(), panel, c->tc_A, c->tc_P, N, L, i, s.owned[q], 2, 0, 0, s.d_err};
     a.owned = s.d_owned;
@@ -1567,6 +1640,7 @@ void dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st) {
     a.e0 = e0;
     a.first_loc = int(q);
     tc_products(c, a, B, unsigned(ncols), st);
+    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 1)], st);
     // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
     int* cnt = s.d_fb + (i & 1);
     int* nxt = s.d_fb + ((i + 1) & 1);
@@ -1575,6 +1649,8 @@ void dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st) {
     launch(c, rd, n,
            hk::tcround_words(L), st);
     launch_fix(c, hk::FixD{s.S.view(), panel, B, s.d_erow, s.d_ecol, L, i, e0}, st, cnt, nxt);
+    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 2)], st);
+    return true;
 }
 
 // make every shard's panel slot `col` hold column col (rows col..N-1): the
@@ -1613,6 +1689,37 @@ void dist_derive(hk_ctx* c, Shard& s, int i, cudaStream_t st) {
                    st);
 }
 
+// rank 0's (status, lambdas) to every rank: one ncclBroadcast of 11 doubles
+int share_root_result(hk_ctx* c, int* rc, int s, double* hi, double* lo, double* te) {
+    return guarded(c, [&] {
+        double h[11] = {double(*rc), double(s), 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (c->rank == 0 && *rc == HK_OK)
+            for (int q = 0; q < s && q < 3; ++q) {
+                h[2 + q] = hi[q];
+                h[5 + q] = lo[q];
+                h[8 + q] = te[q];
+            }
+        if (!c->bcast_buf) ck(cudaMalloc(&c->bcast_buf, sizeof(h)), "cudaMalloc bcast");
+        ck(cudaMemcpyAsync(c->bcast_buf, h, sizeof(h), cudaMemcpyHostToDevice, c->st), "H2D result");
+        nk(nccl_api()->Broadcast(c->bcast_buf, c->bcast_buf, sizeof(h), ncclUint8, 0, (ncclComm_t)c->nccl_comm, c->st),
+           "bcast result");
+        ck(cudaMemcpyAsync(h, c->bcast_buf, sizeof(h), cudaMemcpyDeviceToHost, c->st), "D2H result");
+        ck(cudaStreamSynchronize(c->st), "sync");
+        const int root_rc = int(h[0]);
+        if (c->rank != 0) {
+            if (root_rc != HK_OK && *rc == HK_OK) c->err = "rank 0 failed with status " + std::to_string(root_rc);
+            if (*rc == HK_OK) *rc = root_rc;
+            if (root_rc == HK_OK)
+                for (int q = 0; q < s && q < 3; ++q) {
+                    hi[q] = h[2 + q];
+                    lo[q] = h[5 + q];
+                    te[q] = h[8 + q];
+                }
+        }
+        return HK_OK;
+    });
+}
+
 void enqueue_dist_steps(hk_ctx* c, bool tc) {
     const int N = c->n, L = c->L;
     cudaStream_t bulk = c->st, la = c->st2;
@@ -1622,12 +1729,25 @@ void enqueue_dist_steps(hk_ctx* c, bool tc) {
     for (auto& s : c->shards)
         if (c->owner[0] == s.rank)
             launch(c, hk::ItemCopy{slot3(s.panel, N, L, 0), s.S.view(), 0, s.off[size_t(s.loc[0])], L}, N, 64, la);
-    dist_publish(c, 0, la);
+    grow_events(c->cev, size_t(2 * N), cudaEventDefault);
+    c->cev_steps = 0;
+    c->kev_steps = 0;
+    if (c->kprof) grow_events(c->kev, size_t(3 * N), cudaEventDefault);
+    auto publish = [&](int col) { // timed: the broadcast including the wait for its root (ldlt.cpp:248)
+        graph_event(c->cev[size_t(2 * c->cev_steps)], la);
+        dist_publish(c, col, la);
+        graph_event(c->cev[size_t(2 * c->cev_steps + 1)], la);
+        ++c->cev_steps;
+    };
+    publish(0);
     for (auto& s : c->shards) dist_derive(c, s, 0, la);
     ck(cudaEventRecord(c->evP[0], la), "evP");
     for (int i = 0; i < N; ++i) {
         ck(cudaStreamWaitEvent(bulk, c->evP[size_t(i)], 0), "wait P");
-        for (auto& s : c->shards) dist_bulk(c, s, i, tc, bulk);
+        // one real rank per process: its bulk kernels are timed when kprof is on
+        const bool timed = c->kprof && c->shards.size() == 1;
+        for (auto& s : c->shards)
+            if (dist_bulk(c, s, i, tc, bulk, timed ? c->kev_steps : -1) && timed) ++c->kev_steps;
         ck(cudaEventRecord(c->evU[size_t(i)], bulk), "evU");
         for (auto& s : c->shards)
             if (c->owner[size_t(i)] == s.rank)
@@ -1648,7 +1768,7 @@ void enqueue_dist_steps(hk_ctx* c, bool tc) {
                                         s.d_err},
                        N - i - 1, ws_cta_words(L), la);
         }
-        dist_publish(c, i + 1, la);
+        publish(i + 1);
         for (auto& s : c->shards) dist_derive(c, s, i + 1, la);
         ck(cudaEventRecord(c->evP[size_t(i + 1)], la), "evP");
     }
@@ -1736,7 +1856,8 @@ int dist_ldlt(hk_ctx* c) {
         launch(c, hk::ItemDInit{s.S.view(), c->mu.view(), s.d_erow, s.d_ecol, L}, s.off.back(), 64);
     }
     // the step graph is valid for the buffers it was captured on
-    std::vector<const void*> sig{(const void*)(long long)N, (const void*)(long long)tc, c->tc_A, c->tc_P, c->tc_fb};
+    std::vector<const void*> sig{(const void*)(long long)N, (const void*)(long long)tc, c->tc_A, c->tc_P, c->tc_fb,
+                                 (const void*)(long long)c->kprof, c->mu.d};
     for (auto& s : c->shards)
         for (const void* p : {(const void*)s.S.d, (const void*)s.panel.d, (const void*)s.B.d, (const void*)s.R.d,
                               (const void*)s.d_err, (const void*)s.d_fb, (const void*)s.d_erow, (const void*)s.d_owned})
@@ -1744,14 +1865,10 @@ int dist_ldlt(hk_ctx* c) {
     if (!c->dist_graph || sig != c->dist_sig) {
         if (c->dist_graph) cudaGraphExecDestroy(c->dist_graph);
         c->dist_graph = nullptr;
-        cudaGraph_t g;
         const long long before = c->launches;
-        ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        Capture cap(c->st);
         enqueue_dist_steps(c, tc);
-        ck(cudaStreamEndCapture(c->st, &g), "end capture");
-        ck(cudaGraphInstantiateWithFlags(&c->dist_graph, g, cudaGraphInstantiateFlagUseNodePriority),
-           "graph instantiate");
-        cudaGraphDestroy(g);
+        c->dist_graph = instantiate(cap.end(), cudaGraphInstantiateFlagUseNodePriority);
         c->dist_graph_launches = c->launches - before;
         c->launches = before;
         c->dist_sig = sig;
@@ -1829,6 +1946,33 @@ int hk_create_sharded(int device, int limbs, int rank, int world, const void* nc
         *out = nullptr;
     }
     return r2;
+}
+
+int hk_set_kernel_timing(hk_ctx* c, int on) {
+    if (!c) return HK_ERR_INVALID;
+    c->kprof = on != 0; // the LDLT graph signature includes it: recaptured on change
+    return HK_OK;
+}
+
+int hk_kernel_times(hk_ctx* c, double* out6) {
+    return guarded(c, [&] {
+        if (!out6) return fail(c, HK_ERR_INVALID, "hk_kernel_times: null output");
+        for (int q = 0; q < 6; ++q) out6[q] = 0.0;
+        const bool dist = c->world > 1 || c->virt || c->nccl_comm;
+        if (c->kprof && (dist ? c->dist_graph != nullptr : !c->graphs.empty())) {
+            for (int s = 0; s < c->kev_steps; ++s) {
+                out6[0] += event_ms(c->kev[size_t(3 * s)], c->kev[size_t(3 * s + 1)]);
+                out6[1] += event_ms(c->kev[size_t(3 * s + 1)], c->kev[size_t(3 * s + 2)]);
+            }
+            out6[2] = c->kev_steps;
+        }
+        if (dist && c->dist_graph) {
+            for (int s = 0; s < c->cev_steps; ++s) out6[3] += event_ms(c->cev[size_t(2 * s)], c->cev[size_t(2 * s + 1)]);
+            out6[4] = c->cev_steps;
+        }
+        out6[5] = c->t[1] * 1e3;
+        return HK_OK;
+    });
 }
 
 int hk_world(const hk_ctx* c, int* rank, int* world) {

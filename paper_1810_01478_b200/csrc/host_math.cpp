@@ -43,7 +43,28 @@ static bool big_bit(const Big& a, long b) {
     return q < a.size() && ((a[q] >> (b & 31)) & 1u);
 }
 
+// word w of (a >> shift) for any shift (negative: left shift), zero outside a
+static uint32_t big_word_shr(const Big& a, long shift, long w) {
+    const long b = shift + 32 * w; // bit of a that lands on bit 0 of word w
+    const long q = b >= 0 ? b / 32 : -((-b + 31) / 32);
+    const int r = int(b - 32 * q);
+    auto word = [&](long i) -> uint64_t { return (i >= 0 && size_t(i) < a.size()) ? a[size_t(i)] : 0u; };
+    const uint64_t two = word(q) | (word(q + 1) << 32);
+    return uint32_t(two >> r);
+}
+
+// any bit of a below bit `b` set?
+static bool big_sticky_below(const Big& a, long b) {
+    if (b <= 0) return false;
+    const size_t q = size_t(b >> 5);
+    for (size_t i = 0; i < q && i < a.size(); ++i)
+        if (a[i]) return true;
+    const int r = int(b & 31);
+    return r && q < a.size() && (a[q] & ((1u << r) - 1u));
+}
+
 // RNE of the positive integer `a` into `limbs` words; returns exp; sets exact.
+// Word-shifted (the conversion is a shift plus one rounding increment).
 static int big_to_mpf(const Big& a, int limbs, uint32_t* out, bool& exact) {
     const int p = 32 * limbs;
     const int nb = big_bitlen(a);
@@ -51,12 +72,10 @@ static int big_to_mpf(const Big& a, int limbs, uint32_t* out, bool& exact) {
     exact = true;
     if (nb == 0) return 0;
     const long shift = long(nb) - p; // out = a >> shift (shift may be negative)
-    for (int i = 0; i < p; ++i)
-        if (big_bit(a, shift + i)) out[i >> 5] |= 1u << (i & 31);
+    for (int w = 0; w < limbs; ++w) out[w] = big_word_shr(a, shift, w);
     if (shift > 0) {
         const bool rb = big_bit(a, shift - 1);
-        bool st = false;
-        for (long b = 0; b < shift - 1 && !st; ++b) st = big_bit(a, b);
+        const bool st = big_sticky_below(a, shift - 1);
         exact = !rb && !st;
         if (rb && (st || (out[0] & 1u))) {
             int i = 0;
@@ -94,9 +113,22 @@ extern "C" int hk_moments_impl(unsigned beta_num, unsigned beta_den, int count, 
     bool all_exact = true;
     for (int k = 0; k < count; ++k) {
         const unsigned long arg = (unsigned long)(k + 1) * q / 2 - 1;
-        while (have < arg) big_mul_small(f, uint32_t(++have));
-        Big mu = f;
-        big_mul_small(mu, uint32_t(q / 2));
+        while (have < arg) { // two factors per pass while their product fits a word
+            if (have + 2 <= arg && have + 2 < 65536) {
+                big_mul_small(f, uint32_t((have + 1) * (have + 2)));
+                have += 2;
+            } else {
+                big_mul_small(f, uint32_t(++have));
+            }
+        }
+        Big scaled;
+        const Big* mup = &f;
+        if (q / 2 != 1) {
+            scaled = f;
+            big_mul_small(scaled, uint32_t(q / 2));
+            mup = &scaled;
+        }
+        const Big& mu = *mup;
         bool ex = true;
         out_exps[k] = big_to_mpf(mu, limbs, out_limbs + size_t(k) * limbs, ex);
         out_signs[k] = 1;

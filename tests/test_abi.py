@@ -39,13 +39,14 @@ def test_host_moments_match_reference_moments():
         for j in range(2 * n - 1):
             assert mu.to_fraction(j) == R.moment_integer(beta, j)
     # precision too small -> correctly rounded, flagged inexact
-    mu, exact = api.build_hankel((1, 2), 30, 2)
-    assert not exact
     from oracle import mpfloat as F
 
-    for j in range(59):
-        s, m, e = mu.entry(j)
-        assert F.MPF(s, m, e) == F.from_int(R.moment_integer((1, 2), j), 64)
+    for beta, L, n in (((1, 2), 2, 30), ((1, 2), 1, 40), ((1, 1), 3, 60), ((1, 3), 5, 50), ((1, 1), 1, 90)):
+        mu, exact = api.build_hankel(beta, n, L)
+        assert not exact
+        for j in range(2 * n - 1):
+            s, m, e = mu.entry(j)
+            assert F.MPF(s, m, e) == F.from_int(R.moment_integer(beta, j), 32 * L), (beta, L, j)
     with pytest.raises(ValueError):
         api.build_hankel((2, 1), 4, 4)  # beta = 2: half-integer gamma path not implemented
     with pytest.raises(ValueError):

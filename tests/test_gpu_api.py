@@ -1,0 +1,121 @@
+"""GPU: host-API behaviour around the path — graph-resident kernel timing,
+re-use of one context across precisions (hk_set_limbs, as auto_precision /
+scan do, pipeline.cpp:74-122), and the multi-GPU group with >= 2 real NCCL
+ranks when the box has them (the reference's worker-count determinism,
+acceptance.cpp:176-218)."""
+import os
+import socket
+
+import pytest
+
+from tests.mpf_helpers import from_arr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1810_01478_b200 import api as a
+
+    return a
+
+
+def run(ctx, mu, k):
+    rec = ctx.compute(mu, k)
+    return rec, from_arr(ctx.D()), from_arr(ctx.block())
+
+
+@pytest.mark.parametrize("beta,n,L,k,tc", [((1, 2), 48, 8, 8, "0"), ((1, 1), 40, 192, 8, "1")])
+def test_kernel_timing_nodes_do_not_change_results(api, beta, n, L, k, tc, monkeypatch):
+    monkeypatch.setenv("HK_TC", tc)
+    mu, _ = api.build_hankel(beta, n, L)
+    with api.Context(L) as ctx:
+        r0, D0, M0 = run(ctx, mu, k)
+        ctx.set_kernel_timing(True)
+        r1, D1, M1 = run(ctx, mu, k)
+        kt = ctx.kernel_times()
+    assert D1 == D0 and M1 == M0 and r1.lambda_hi == r0.lambda_hi
+    assert kt["steps"] == n - 2  # one timed bulk launch per step with columns >= i+2
+    assert kt["products_ms"] > 0 and kt["round_ms"] >= 0
+    assert kt["products_ms"] + kt["round_ms"] <= kt["ldlt_ms"] * 1.05
+
+
+def test_set_limbs_reuses_context(api):
+    beta, n, k = (1, 2), 40, 8
+    mu1, _ = api.build_hankel(beta, n, 24)
+    mu2, _ = api.build_hankel(beta, n, 40)
+    with api.Context(40) as fresh:
+        want = run(fresh, mu2, k)
+    with api.Context(24) as ctx:
+        run(ctx, mu1, k)
+        ctx.set_limbs(40)
+        got = run(ctx, mu2, k)
+        ctx.set_limbs(40)  # no-op
+        again = run(ctx, mu2, k)
+    assert got[1] == want[1] and got[2] == want[2] and again[1] == want[1]
+
+
+def test_set_limbs_sharded_keeps_communicator(api):
+    """auto_precision on a sharded context: one ncclUniqueId, several precisions."""
+    beta, n, k = (1, 2), 30, 8
+    nid = api.nccl_unique_id()
+    with api.Context(16, rank=0, world=1, nccl_id=nid) as ctx:
+        for L in (16, 24, 16):
+            mu, _ = api.build_hankel(beta, n, L)
+            ctx.set_limbs(L)
+            got = run(ctx, mu, k)
+            with api.Context(L) as one:
+                want = run(one, mu, k)
+            assert got[1] == want[1] and got[2] == want[2] and got[0].lambda_hi == want[0].lambda_hi
+        kt = ctx.kernel_times()
+        assert kt["comm_steps"] == n and kt["comm_ms"] >= 0
+
+
+def _rank_main(rank, world, port, beta, n, L, k, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1810_01478_b200 import api as a
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    obj = [a.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    mu, _ = a.build_hankel(beta, n, L)
+    with a.Context(L, device=rank, rank=rank, world=world, nccl_id=obj[0]) as ctx:
+        rec = ctx.compute(mu, k)
+        out = (rec.lambda_hi, rec.lambda_lo)
+        if rank == 0:
+            out = out + (from_arr(ctx.D()), from_arr(ctx.block()))
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_real_nccl_ranks_bit_identical(api, world):
+    """>= 2 real NCCL ranks (one process per GPU) give the 1-GPU factors, block
+    and lambdas bit for bit, and every rank returns rank 0's lambdas."""
+    import torch
+    import torch.multiprocessing as mp
+
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs (this box has {torch.cuda.device_count()})")
+    beta, n, L, k = (1, 2), 96, 192, 16
+    mu, _ = api.build_hankel(beta, n, L)
+    with api.Context(L) as one:
+        want = run(one, mu, k)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, beta, n, L, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    assert res[0][2] == want[1] and res[0][3] == want[2]
+    for r in range(world):
+        assert res[r][0] == want[0].lambda_hi and res[r][1] == want[0].lambda_lo

@@ -1,0 +1,26 @@
+#!/bin/bash
+# One GPU pass (dev): GPU tests, the default bench (C4), C2 bench, ncu of the
+# product / rounding kernels at C4, and the reference arm at C4.
+#   tools/gpu_pass.sh TAG [tests] [bench] [c2] [ncu] [ref]
+tag=${1:-r02}; shift
+what=${*:-tests bench c2 ncu ref}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${tag}_smi.txt 2>&1
+nproc > gpurun_out/${tag}_nproc.txt; lscpu | grep "Model name" >> gpurun_out/${tag}_nproc.txt
+for w in $what; do
+  case $w in
+    tests) timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_gputests.log 2>&1; echo "tests rc=$?";;
+    bench) timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/${tag}_bench_c4.json 2> gpurun_out/${tag}_bench_c4.err; echo "bench rc=$?";;
+    c2) timeout 300 python bench.py --config c2 --steps 10 --warmup 3 > gpurun_out/${tag}_bench_c2.json 2> gpurun_out/${tag}_bench_c2.err; echo "c2 rc=$?";;
+    c3) timeout 300 python bench.py --config c3 --steps 3 --warmup 3 > gpurun_out/${tag}_bench_c3.json 2> gpurun_out/${tag}_bench_c3.err; echo "c3 rc=$?";;
+    ncu)
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tc_bulk -s 300 -c 1 \
+        -o gpurun_out/${tag}_prof_tcb_c4 -f python tools/one_run.py c4 1 > gpurun_out/${tag}_ncu_tcb_c4.log 2>&1; echo "ncu tcb rc=$?"
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ItemTcRound -s 300 -c 1 \
+        -o gpurun_out/${tag}_prof_round_c4 -f python tools/one_run.py c4 1 > gpurun_out/${tag}_ncu_round_c4.log 2>&1; echo "ncu round rc=$?";;
+    launches)
+      timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 5000 \
+        --log-file gpurun_out/${tag}_launches_c4.csv python tools/one_run.py c4 1 > gpurun_out/${tag}_launches_c4.log 2>&1; echo "launches rc=$?";;
+    ref) timeout 1500 python bench.py --impl reference --steps 1 --warmup 0 --ref-golden-precision > gpurun_out/${tag}_ref_c4.json 2> gpurun_out/${tag}_ref_c4.err; echo "ref rc=$?";;
+  esac
+done
