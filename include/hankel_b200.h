@@ -158,6 +158,11 @@ int hk_profile_ldlt(hk_ctx* ctx, double* ms7, long long* n_trailing);
  * WorkerTimings::comm_s (ldlt.cpp:214-263, 341) — and [4] their count; [5] the
  * LDLT's own time (ms). */
 int hk_set_kernel_timing(hk_ctx* ctx, int on);
+
+/* Test hook: how many items of the fused tensor-core rounding (csrc/tc_fused.cuh)
+ * failed its final normalisation check since the context was created.  The
+ * exponent prediction is certified, so this must stay 0; tests assert it. */
+int hk_fused_violations(hk_ctx* ctx, long long* out);
 int hk_kernel_times(hk_ctx* ctx, double* out6);
 
 /* Measured integer-MAC peak of the device: 32x32->64-bit limb MACs per second

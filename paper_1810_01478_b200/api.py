@@ -74,6 +74,7 @@ def lib():
             "hk_set_limbs": (C.c_int, [vp, C.c_int]),
             "hk_set_kernel_timing": (C.c_int, [vp, C.c_int]),
             "hk_kernel_times": (C.c_int, [vp, f64p]),
+            "hk_fused_violations": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -352,6 +353,11 @@ class Context:
         _check(lib().hk_kernel_times(self.h, t.ctypes.data_as(C.POINTER(C.c_double))), self.h)
         keys = ("products_ms", "round_ms", "steps", "comm_ms", "comm_steps", "ldlt_ms")
         return dict(zip(keys, t.tolist()))
+
+    def fused_violations(self) -> int:
+        v = C.c_longlong()
+        _check(lib().hk_fused_violations(self.h, C.byref(v)), self.h)
+        return v.value
 
     def launch_count(self) -> int:
         return int(lib().hk_launch_count(self.h))

@@ -196,6 +196,7 @@ struct hk_ctx {
     // ---- tensor-core bulk products (large p): scratch of short products
     uint32_t* tc_P = nullptr;
     size_t tc_P_words = 0;
+    size_t tc_fb_cap = 0;         // fix-up list capacity (items)
     uint8_t* tc_A = nullptr;      // preformatted A operand of the current step
     int tc_A_n = 0;               // rows it was sized for
     uint64_t* tc_gcarry = nullptr; // L^-1 chunk-group carries
@@ -414,6 +415,14 @@ bool force_fix() {
     return e && e[0] == '1';
 }
 
+// The certified rounding fused into the product kernel's epilogue (LDLT bulk
+// steps; tc_fused.cuh).  HK_TC_FUSE=0 keeps the separate rounding pass.
+bool use_fuse(const hk_ctx* c) {
+    if (!hk::tc_fusable(c->L)) return false;
+    const char* e = getenv("HK_TC_FUSE");
+    return !e || e[0] != '0';
+}
+
 bool use_tc_inv(const hk_ctx* c) {
     if (!use_tc(c)) return false;
     if (getenv("HK_TC")) return true;
@@ -431,14 +440,17 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     // with two accumulators).  HK_TC_EWIN / HK_TC_NACC force the other variants.
     a.ewin = 1;
     if (const char* e = getenv("HK_TC_EWIN")) a.ewin = e[0] == '1' ? 1 : 0;
-    const size_t need = hk::tc_smem_bytes(L, a.ewin != 0);
-    a.nacc = need <= 110 * 1024 ? 1 : 2;
+    if (a.fuse) a.ewin = 1;
+    const size_t need = hk::tc_smem_bytes(L, a.ewin != 0, a.fuse != 0);
+    a.nacc = need <= 113 * 1024 ? 1 : 2;
     if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
     const size_t smem = a.nacc == 1 ? need : std::max(need, size_t(120 * 1024));
     func_smem((const void*)hk::k_tc_bulk, 220 * 1024);
     func_smem((const void*)hk::k_tc_prep, 0);
     static const char* dv = getenv("HK_DEV_TCB"); // dev what-if (tools only): bits of TcBulkArgs::dev
     a.dev = dv ? atoi(dv) : 0;
+    const char* sl = getenv("HK_TC_SLEEP"); // barrier-poll back-off (ns) of the non-issuing warps
+    a.sleep_ns = sl ? atoi(sl) : 0;
     const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
     const long long nprep = prep.count();
     launch_ex(hk::k_tc_prep, dim3(unsigned((nprep + 255) / 256)), dim3(256), 0, st, pdl, prep, nprep);
@@ -514,19 +526,27 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = fals
         }
         return;
     }
-    if (!dev_skip("prod"))
-        tc_products(c, hk::TcBulkArgs{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err},
-                    b_buf(c, i), unsigned(ncols), st, pdl);
-    if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
-    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 1)], st);
     // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
     int* cnt = c->tc_fb_count + (i & 1);
     int* nxt = c->tc_fb_count + ((i + 1) & 1);
+    hk::TcBulkArgs ta{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err};
+    const bool fuse = use_fuse(c);
+    if (fuse) {
+        ta.fuse = 1;
+        ta.Y = b_buf(c, i);
+        ta.fb_count = cnt;
+        ta.fb = c->tc_fb;
+        ta.force_fb = force_fix();
+        ta.viol = c->tc_fb_count + 3;
+    }
+    if (!dev_skip("prod")) tc_products(c, ta, b_buf(c, i), unsigned(ncols), st, pdl);
+    if (c->prof_mid) ck(cudaEventRecord(c->prof_mid, st), "prof mid");
+    if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 1)], st);
     hk::ItemTcRound ri{c->S.view(), b_buf(c, i), c->tc_P, N, L, i, jfirst, c->d_err, cnt, c->tc_fb};
     static const char* rd = getenv("HK_ROUND_DIRECT");
     ri.direct = !rd || rd[0] == '1';
     ri.force_fb = force_fix();
-    if (!dev_skip("round"))
+    if (!fuse && !dev_skip("round"))
         launch_cols(c, ri, ncols, ncols, ri.direct ? hk::align4(L + 16) : hk::tcround_words(L), st, pdl);
     if (!dev_skip("fix")) launch_fix(c, hk::FixLdlt{c->S.view(), b_buf(c, i), N, L, i, jfirst}, st, cnt, nxt, pdl);
     if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 2)], st);
@@ -692,35 +712,44 @@ void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
     ++c->launches;
 }
 
-// Tensor-core scratch for up to `items` products per step (+ the A operand of N rows).
-void ensure_tc_items(hk_ctx* c, size_t items) {
+// Tensor-core buffers: the A operand of N rows, product scratch for `p_items`
+// products (the unfused rounding pass and L^-1 steps; the fused LDLT needs
+// none) and the fix-up list for `fb_items` items per step.
+void ensure_tc_items(hk_ctx* c, size_t p_items, size_t fb_items) {
     if (c->tc_A_n < c->n) {
         if (c->tc_A) cudaFree(c->tc_A);
         c->tc_A = nullptr;
         ck(cudaMalloc(&c->tc_A, hk::tc_apre_bytes(c->n, c->L)), "cudaMalloc tc A");
         c->tc_A_n = c->n;
     }
-    const size_t need = items * hk::tc_scratch_limbs(c->L);
-    if (c->tc_P_words >= need) return;
-    if (c->tc_P) cudaFree(c->tc_P);
-    if (c->tc_fb) cudaFree(c->tc_fb);
-    if (c->tc_gcarry) cudaFree(c->tc_gcarry);
-    c->tc_P = nullptr;
-    c->tc_fb = nullptr;
-    c->tc_gcarry = nullptr;
-    ck(cudaMalloc(&c->tc_gcarry, items * (hk::kTcMaxGroups - 1) * sizeof(uint64_t)), "cudaMalloc tc carries");
     if (!c->tc_fb_count) {
         ck(cudaMalloc(&c->tc_fb_count, 4 * sizeof(int)), "cudaMalloc fb count");
         ck(cudaMemset(c->tc_fb_count, 0, 4 * sizeof(int)), "memset fb count");
     }
+    if (fb_items > c->tc_fb_cap) {
+        if (c->tc_fb) cudaFree(c->tc_fb);
+        c->tc_fb = nullptr;
+        ck(cudaMalloc(&c->tc_fb, fb_items * sizeof(long long)), "cudaMalloc fb list");
+        c->tc_fb_cap = fb_items;
+    }
+    const size_t need = std::max<size_t>(p_items, 1) * hk::tc_scratch_limbs(c->L);
+    if (c->tc_P_words >= need) return;
+    if (c->tc_P) cudaFree(c->tc_P);
+    if (c->tc_gcarry) cudaFree(c->tc_gcarry);
+    c->tc_P = nullptr;
+    c->tc_gcarry = nullptr;
+    ck(cudaMalloc(&c->tc_gcarry, std::max<size_t>(p_items, 1) * (hk::kTcMaxGroups - 1) * sizeof(uint64_t)),
+       "cudaMalloc tc carries");
     ck(cudaMalloc(&c->tc_P, need * sizeof(uint32_t)), "cudaMalloc tc scratch");
-    ck(cudaMalloc(&c->tc_fb, items * sizeof(long long)), "cudaMalloc fb list");
     c->tc_P_words = need;
 }
 
+// m == 0: the LDLT's needs; m > 0: the L^-1 steps' (N m products per step)
 void ensure_tc_scratch(hk_ctx* c, int m = 0) {
     if (!use_tc(c)) return;
-    ensure_tc_items(c, std::max((size_t)c->n * (c->n + 1) / 2, (size_t)c->n * m));
+    const size_t tri = (size_t)c->n * (c->n + 1) / 2, nm = (size_t)c->n * m;
+    const size_t p_items = m > 0 ? nm : (use_fuse(c) ? 0 : tri);
+    ensure_tc_items(c, p_items, std::max(tri, nm + c->n));
 }
 
 void enqueue_ldlt_steps(hk_ctx* c) {
@@ -987,9 +1016,11 @@ int hk_ldlt(hk_ctx* c) {
         ck(cudaEventRecord(c->ev[0], c->st), "event");
         launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
         // the cached step graphs are valid for the buffers and modes they were captured on
-        const std::vector<const void*> sig{c->S.d, c->S.m, c->R.d, c->B.d, c->mu.d, c->tc_P, c->tc_A, c->tc_fb,
+        // (the fused LDLT does not use the product scratch: L^-1 may re-size it freely)
+        const std::vector<const void*> sig{c->S.d, c->S.m, c->R.d, c->B.d, c->mu.d,
+                                           use_fuse(c) ? nullptr : (const void*)c->tc_P, c->tc_A, c->tc_fb,
                                            c->tc_fb_count, (const void*)(long long)use_tc(c),
-                                           (const void*)(long long)c->kprof};
+                                           (const void*)(long long)use_fuse(c), (const void*)(long long)c->kprof};
         if (sig != c->graph_sig) {
             for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
             c->graphs.clear();
@@ -1221,6 +1252,7 @@ int hk_set_limbs(hk_ctx* c, int limbs) {
         c->tc_fb = nullptr;
         c->tc_gcarry = nullptr;
         c->tc_P_words = 0;
+        c->tc_fb_cap = 0;
         c->tc_A_n = 0;
         c->L = limbs;
         c->n = c->m = c->k = 0;
@@ -1634,20 +1666,30 @@ bool dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st, int kslot =
         }
         return true;
     }
+    // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
+    int* cnt = s.d_fb + (i & 1);
+    int* nxt = s.d_fb + ((i + 1) & 1);
     hk::TcBulkArgs a{s.S.view(), panel, c->tc_A, c->tc_P, N, L, i, s.owned[q], 2, 0, 0, s.d_err};
     a.owned = s.d_owned;
     a.off = s.d_off;
     a.e0 = e0;
     a.first_loc = int(q);
+    const bool fuse = use_fuse(c);
+    if (fuse) {
+        a.fuse = 1;
+        a.Y = B;
+        a.fb_count = cnt;
+        a.fb = c->tc_fb;
+        a.force_fb = force_fix();
+        a.viol = c->tc_fb_count + 3;
+    }
     tc_products(c, a, B, unsigned(ncols), st);
     if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 1)], st);
-    // fallback counters alternate by step: the fix-up of step i clears the one step i+1 uses
-    int* cnt = s.d_fb + (i & 1);
-    int* nxt = s.d_fb + ((i + 1) & 1);
-    hk::ItemTcRoundD rd{s.S.view(), panel, B, s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err, cnt, c->tc_fb};
-    rd.force_fb = force_fix();
-    launch(c, rd, n,
-           hk::tcround_words(L), st);
+    if (!fuse) {
+        hk::ItemTcRoundD rd{s.S.view(), panel, B, s.d_erow, s.d_ecol, c->tc_P, L, i, e0, s.d_err, cnt, c->tc_fb};
+        rd.force_fb = force_fix();
+        launch(c, rd, n, hk::tcround_words(L), st);
+    }
     launch_fix(c, hk::FixD{s.S.view(), panel, B, s.d_erow, s.d_ecol, L, i, e0}, st, cnt, nxt);
     if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 2)], st);
     return true;
@@ -1845,7 +1887,7 @@ int dist_ldlt(hk_ctx* c) {
     if (tc) {
         long long most = 1;
         for (auto& s : c->shards) most = std::max(most, s.off.back());
-        ensure_tc_items(c, size_t(most));
+        ensure_tc_items(c, use_fuse(c) ? 0 : size_t(most), size_t(most));
     }
     ensure_step_events(c, N);
     c->bad_col = -1;
@@ -1946,6 +1988,18 @@ int hk_create_sharded(int device, int limbs, int rank, int world, const void* nc
         *out = nullptr;
     }
     return r2;
+}
+
+int hk_fused_violations(hk_ctx* c, long long* out) {
+    return guarded(c, [&] {
+        if (!out) return fail(c, HK_ERR_INVALID, "hk_fused_violations: null output");
+        int v = 0;
+        if (c->tc_fb_count) {
+            ck(cudaMemcpy(&v, c->tc_fb_count + 3, sizeof(int), cudaMemcpyDeviceToHost), "D2H violations");
+        }
+        *out = v;
+        return HK_OK;
+    });
 }
 
 int hk_set_kernel_timing(hk_ctx* c, int on) {

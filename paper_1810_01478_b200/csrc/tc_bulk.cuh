@@ -21,6 +21,7 @@
 #pragma once
 
 #include "hk_items.cuh"
+#include "tc_fused.cuh"
 #include "tc_i8.cuh"
 
 namespace hk {
@@ -32,7 +33,9 @@ constexpr int kTcGuard = 8;      // short product from limb L - 8
 constexpr int kTcThreads = 256;  // warp 0: TMA + MMA issue; warps 4-7: epilogue (TMEM lanes 32 (w % 4)..)
 constexpr int kTcKB = 4;         // MMAs (K-steps) per A block
 constexpr int kTcBlk = 4096 * kTcKB; // bytes per A block (one bulk copy)
-constexpr int kTcStages = 4;     // A ring depth
+constexpr int kTcStages = 4;     // A ring depth (3 with the fused rounding: its 32 KB staging)
+constexpr int kTcStagesFused = 3;
+constexpr int kTcStageWords = 64 * kTcRows; // fused epilogue: one chunk's 64 limbs per row
 
 HK_HD int tc_nb(int L) { return 4 * L; }
 HK_HD int tc_ncell(int L) { return tc_nb(L) + 352; }        // cells p in [-31, nb + 321)
@@ -46,11 +49,22 @@ constexpr int kTcEWin = 384;    // cells of x one A block's 4 K-steps read (wind
 // Full expansion: all nb + 352 cells built once per CTA.  Windowed (large p,
 // where the full expansion would not fit): warps 1-3 build each block's
 // 384-cell window into a ring next to the A ring, paced by the same barriers.
-HK_HD size_t tc_smem_bytes(int L, bool ewin = false) {
-    const size_t e = ewin ? (size_t)kTcStages * kTcEWin * 16 : 16 * (size_t)tc_ncell(L);
-    return (size_t)kTcStages * kTcBlk + e + 4 * (size_t)tc_sx_words(L) + 64;
+HK_HD int tc_stages(bool fuse) { return fuse ? kTcStagesFused : kTcStages; }
+HK_HD size_t tc_sx_off(int L, bool ewin, bool fuse) {
+    const int ns = tc_stages(fuse);
+    const size_t e = ewin ? (size_t)ns * kTcEWin * 16 : 16 * (size_t)tc_ncell(L);
+    return (size_t)ns * kTcBlk + e;
+}
+HK_HD size_t tc_stage_off(int L, bool ewin, bool fuse) {
+    return (tc_sx_off(L, ewin, fuse) + 4 * (size_t)tc_sx_words(L) + 127) / 128 * 128;
+}
+HK_HD size_t tc_smem_bytes(int L, bool ewin = false, bool fuse = false) {
+    return tc_stage_off(L, ewin, fuse) + (fuse ? 4 * (size_t)kTcStageWords : 0) + 64;
 }
 HK_HD bool tc_ewin(int L) { return tc_smem_bytes(L, false) > 200 * 1024; }
+// The fused rounding: LDLT steps (modes 0 / 2) whose rows are whole 8-limb
+// blocks, when two CTAs still fit an SM (227 KB of shared memory per SM)
+HK_HD bool tc_fusable(int L) { return L % 8 == 0 && tc_smem_bytes(L, true, true) + 1024 <= 113 * 1024; }
 
 // A blocks (4 K-steps each) of output chunk c; chunk c covers product bytes from
 // t' = -31 + 256 c, i.e. scratch limbs [64 c, 64 c + 64).
@@ -149,6 +163,14 @@ struct TcBulkArgs {
     long long e0 = 0;
     int first_loc = 0;
     int dev = 0; // dev what-if knobs (results wrong; tools only): 1 no window build, 2 no TMA of A, 4 no drain, 8 no P stores
+    // fused rounding (modes 0 / 2, groups == 1): S(k,j) = RNE(S(k,j) - x y_k) in the epilogue
+    int fuse = 0;
+    MpArr Y{};                  // y_k = B_i(k) (the row operand)
+    int* fb_count = nullptr;    // items left to the exact redo
+    long long* fb = nullptr;
+    int force_fb = 0;           // tests: every 7th item to the exact redo (HK_TC_FORCE_FIX)
+    int* viol = nullptr;        // tests: normalisation-check failures (must stay 0)
+    int sleep_ns = 0;           // back-off of the epilogue / window-builder barrier polls
 };
 
 #if !defined(HK_WARP_EMU)
@@ -160,7 +182,7 @@ struct TcBulkArgs {
 // tcgen05.commit) and issues the MMAs of output chunk c into TMEM accumulator
 // c & 1; warps 4-7 drain accumulator c & 1 (carry the int32 byte-column sums
 // into limbs) while chunk c + 1 accumulates into the other one (accF / accE).
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
     __shared__ uint64_t full[kTcStages], empty[kTcStages], efull[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
@@ -172,10 +194,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     if (j >= N || tile * kTcRows >= N) return;
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
     const bool ewin = a.ewin != 0;
-    uint8_t* sA = tsm;                                     // kTcStages x 16 KB A ring
-    uint8_t* sE = tsm + (size_t)kTcStages * kTcBlk;        // expanded x cells (full, or the window ring)
-    uint32_t* sX = reinterpret_cast<uint32_t*>(sE + (ewin ? (size_t)kTcStages * kTcEWin * 16
-                                                          : 16 * (size_t)tc_ncell(L))); // x bytes, 32 B zero pad
+    const bool fuse = a.fuse != 0;
+    const int ns = tc_stages(fuse);                        // A / window ring depth
+    uint8_t* sA = tsm;                                     // ns x 16 KB A ring
+    uint8_t* sE = tsm + (size_t)ns * kTcBlk;               // expanded x cells (full, or the window ring)
+    uint32_t* sX = reinterpret_cast<uint32_t*>(tsm + tc_sx_off(L, ewin, fuse)); // x bytes, 32 B zero pad
+    uint32_t* sStg = reinterpret_cast<uint32_t*>(tsm + tc_stage_off(L, ewin, fuse)); // fused: drained chunk
     const int pmin = -31;
     // cell p (byte position in X, p >= pmin) -> X[p .. p+15] from sX (zero outside [0, nb))
     auto cell = [&](int p) {
@@ -206,7 +230,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
     const int nacc = a.nacc; // TMEM accumulators (1: two CTAs per SM overlap instead)
     if (warp == 0) tc::tmem_alloc(&taddr_s, uint32_t(nacc * kTcN));
     if (tid == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
+        for (int s = 0; s < ns; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
             tc::mbar_init(&efull[s], 3); // one arrival per builder warp (1-3)
@@ -236,8 +260,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
             // producer cursor: block index qt -> (chunk pc, block pb)
             int qt = 0, pc = c_lo, pb = 0, pcn = nblk_of(c_lo);
             auto issue_tma = [&]() {
-                const int s = qt % kTcStages;
-                if (qt >= kTcStages) tc::mbar_wait(&empty[s], uint32_t((qt / kTcStages) - 1) & 1u);
+                const int s = qt % ns;
+                if (qt >= ns) tc::mbar_wait(&empty[s], uint32_t((qt / ns) - 1) & 1u);
                 tc::mbar_expect_tx(&full[s], kTcBlk);
                 tc::bulk_g2s(sA + (size_t)s * kTcBlk, Abase + (size_t)pb * kTcBlk, kTcBlk, &full[s]);
                 ++qt;
@@ -247,7 +271,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                 }
             };
             pdl_wait(); // the A operand comes from the preceding k_tc_prep
-            while (qt < Q && qt < kTcStages - 1 && !(a.dev & 2)) issue_tma();
+            while (qt < Q && qt < ns - 1 && !(a.dev & 2)) issue_tma();
             int q = 0;
             for (int c = c_lo; c < nch; ++c) {
                 const int cl = c - c_lo; // local chunk index (accumulator / phase)
@@ -259,9 +283,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                 const int ksteps = (u_hi + kTcK - 1) / kTcK;
                 const int nblk = nblk_of(c);
                 for (int b = 0; b < nblk; ++b, ++q) {
-                    const int s = q % kTcStages;
-                    if (!(a.dev & 2)) tc::mbar_wait(&full[s], uint32_t(q / kTcStages) & 1u);
-                    if (ewin && !(a.dev & 1)) tc::mbar_wait(&efull[s], uint32_t(q / kTcStages) & 1u);
+                    const int s = q % ns;
+                    if (!(a.dev & 2)) tc::mbar_wait(&full[s], uint32_t(q / ns) & 1u);
+                    if (ewin && !(a.dev & 1)) tc::mbar_wait(&efull[s], uint32_t(q / ns) & 1u);
                     tc::fence_after();
 #pragma unroll
                     for (int sub = 0; sub < kTcKB; ++sub) {
@@ -288,8 +312,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
             for (int c = c_lo; c < nch; ++c) {
                 const int tc0 = -31 + kTcN * c, nblk = nblk_of(c);
                 for (int b = 0; b < nblk; ++b, ++q) {
-                    const int s = q % kTcStages;
-                    if (q >= kTcStages) tc::mbar_wait(&empty[s], uint32_t((q / kTcStages) - 1) & 1u);
+                    const int s = q % ns;
+                    if (q >= ns) tc::mbar_wait_sleep(&empty[s], uint32_t((q / ns) - 1) & 1u, a.sleep_ns);
                     uint8_t* dst = sE + (size_t)s * kTcEWin * 16;
                     const int p0 = tc0 + b * kTcKB * kTcK;
                     for (int cc = bt; cc < kTcEWin; cc += 96) *reinterpret_cast<uint4*>(dst + 16 * cc) = cell(p0 + cc);
@@ -298,6 +322,84 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
                     if (ln == 0) tc::mbar_arrive(&efull[s]);
                 }
             }
+        }
+    } else if (fuse) {
+        // fused rounding: the thread of row k drains its product limbs chunk by chunk
+        // into its shared-memory row (the accumulator is released at once), then
+        // streams them through FusedRow into S(k,j) in place (tc_fused.cuh)
+        const int r = 32 * (warp & 3) + ln;
+        const int k = tile * kTcRows + r;
+        const bool row_ok = k >= j && k < N;
+        long long item = 0, ec = 0;
+        FusedRow fr;
+        fr.status = 0;
+        if (row_ok) {
+            Meta xm;
+            if (a.mode == 0) {
+                ec = tri_idx(k, j, N);
+                item = col_off(j - a.jfirst, N - a.jfirst) + (k - j);
+                xm = a.S.m[tri_idx(j, a.i, N)];
+            } else {
+                ec = a.off[locj] + (k - j);
+                item = ec - a.e0;
+                xm = a.X.m[j - a.i];
+            }
+            const uint64_t xt = (uint64_t(sX[8 + L - 1]) << 32) | sX[8 + L - 2];
+            const uint32_t* yl = a.Y.limbs(k, L);
+            const uint64_t yt = (uint64_t(yl[L - 1]) << 32) | yl[L - 2];
+            fr.setup(a.S.limbs(ec, L), a.S.m[ec], xt, xm, yt, a.Y.m[k], L);
+            if (a.force_fb && item % 7 == 3 && fr.status != 0) fr.status = 2;
+        }
+        uint32_t* stg = sStg + 64 * r; // 16 x 16-byte cells, XOR-swizzled by row (conflict-free)
+        const int sw = r & 15;
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+        uint64_t carry = 0;
+        for (int c = c_lo; c < nch; ++c) {
+            const int cl = c - c_lo;
+            const int ab = cl % nacc;
+            tc::mbar_wait_sleep(&accF[ab], uint32_t(cl / nacc) & 1u, a.sleep_ns);
+            tc::fence_after();
+            for (int c32 = 0; c32 < kTcN; c32 += 32) {
+                uint32_t v[32];
+                tc::tmem_ld32(lane_base + uint32_t(ab * kTcN + c32), v);
+                tc::tmem_ld_wait();
+                uint32_t o[8];
+#pragma unroll
+                for (int h = 0; h < 8; ++h) {
+                    const uint64_t s = carry + (uint64_t)v[4 * h] + ((uint64_t)v[4 * h + 1] << 8) +
+                                       ((uint64_t)v[4 * h + 2] << 16) + ((uint64_t)v[4 * h + 3] << 24);
+                    o[h] = uint32_t(s);
+                    carry = s >> 32;
+                }
+                const int q = c32 >> 4; // 16-byte cells q, q + 1: limbs 4 q .. 4 q + 7 (8 limbs per 32 columns)
+                reinterpret_cast<uint4*>(stg)[q ^ sw] = make_uint4(o[0], o[1], o[2], o[3]);
+                reinterpret_cast<uint4*>(stg)[(q + 1) ^ sw] = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (ln == 0) tc::mbar_arrive(&accE[ab]); // the MMAs of chunk c + 1 may now overwrite it
+            for (int gg = 0; gg < 8; ++gg) {
+                const int g = 8 * c + gg;
+                if (!fr.wants(g)) continue;
+                const uint4 v0 = reinterpret_cast<const uint4*>(stg)[(2 * gg) ^ sw];
+                const uint4 v1 = reinterpret_cast<const uint4*>(stg)[(2 * gg + 1) ^ sw];
+                const uint32_t pl[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                fr.group(g, pl);
+            }
+        }
+        {
+            const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            for (int g = 8 * nch; fr.wants(g); ++g) fr.group(g, zero);
+        }
+        if (row_ok) {
+            Meta mo{0, 0};
+            bool viol = false;
+            const bool ok = fr.finish(&mo, &viol);
+            if (viol && a.viol) atomicAdd(a.viol, 1);
+            if (!ok)
+                a.fb[atomicAdd(a.fb_count, 1)] = item;
+            else if (fr.status == 1)
+                a.S.m[ec] = mo;
         }
     } else {
         const int r = 32 * (warp & 3) + ln; // this thread's row / TMEM lane
@@ -314,7 +416,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_bulk(TcBulkArgs a) {
         for (int c = c_lo; c < nch; ++c) {
             const int cl = c - c_lo;
             const int ab = cl % nacc;
-            tc::mbar_wait(&accF[ab], uint32_t(cl / nacc) & 1u);
+            tc::mbar_wait_sleep(&accF[ab], uint32_t(cl / nacc) & 1u, a.sleep_ns);
             tc::fence_after();
             for (int c32 = 0; c32 < kTcN && !(a.dev & 4); c32 += 32) {
                 uint32_t v[32];

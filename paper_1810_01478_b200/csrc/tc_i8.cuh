@@ -63,6 +63,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
         : "memory");
 }
 
+// the same wait with a back-off between polls (waiters off the critical issue
+// path: every poll is a shared-memory access the tensor core competes with)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* mbar, uint32_t phase, int ns) {
+    if (ns <= 0) return mbar_wait(mbar, phase);
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(mbar)), "r"(phase)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+    }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
 }

@@ -92,3 +92,74 @@ def test_emulated_cta_ops_match_model(emu_bin, L):
         lines = [f"op {op} {L} {len(ds)}"] + [to_line(d, L) for d in ds]
         for d, r in zip(ds, run(emu_bin, lines)):
             assert from_line(r, L) == F.recip(d, p)
+
+
+def _fused_run(emu_bin, cases, L):
+    lines = [f"fused {L} {len(cases)}"] + [to_line(v, L) for t in cases for v in t]
+    return run(emu_bin, lines)
+
+
+def _ldlt_like_cases(L, rng, count):
+    """Operands shaped like the trailing update: |x y| within a few bits of |c|
+    (Schur-complement cancellation up to ~16 bits), random signs and mantissas."""
+    p = 32 * L
+    out = []
+    for _ in range(count):
+        x, y = rnd(L, rng), rnd(L, rng)
+        e = x.e + y.e + rng.randint(-16, 16)
+        c = rnd(L, rng, e=e)
+        out.append((c, x, y))
+    return out
+
+
+@pytest.mark.parametrize("L", [8, 16, 24, 40])
+def test_fused_epilogue_rounding_matches_model(emu_bin, L):
+    """The rounding fused into the tensor-core epilogue (csrc/tc_fused.cuh),
+    fed the short product exactly as k_tc_bulk forms it: every item it
+    certifies equals RNE(c - x y) (oracle/mpfloat.py); the rest go to the exact
+    redo, and on trailing-update-shaped operands that is rare."""
+    rng = random.Random(7000 + L)
+    p = 32 * L
+    for cases, max_fb in ((fms_cases(L, rng, 300), 0.6), (_ldlt_like_cases(L, rng, 300), 0.08)):
+        out = _fused_run(emu_bin, cases, L)
+        assert len(out) == len(cases)
+        fb = 0
+        for (c, x, y), r in zip(cases, out):
+            assert r != "viol", (c, x, y)
+            if r.startswith("fb"):
+                fb += 1
+                continue
+            assert from_line(r, L) == F.fms(c, x, y, p), (c, x, y)
+        assert fb <= max_fb * len(cases), fb
+
+
+def test_fused_epilogue_edges(emu_bin):
+    """Binade edges, round-up overflow, ties, tiny / huge products, zero c."""
+    L = 16
+    p = 32 * L
+    rng = random.Random(99)
+    cases = []
+    for _ in range(200):
+        x, y = rnd(L, rng), rnd(L, rng)
+        pr = F.mul(x, y, p)
+        kind = rng.randrange(7)
+        if kind == 0:  # c = -x y rounded: exact-ish doubling
+            c = F.MPF(-pr.s, pr.m, pr.e)
+        elif kind == 1:  # product far below c
+            c = rnd(L, rng, e=pr.e + rng.randint(p, 4 * p))
+        elif kind == 2:  # product far above c
+            c = rnd(L, rng, e=pr.e - rng.randint(p, 4 * p))
+        elif kind == 3:  # c a power of two, product just below half an ulp
+            c = F.MPF(rng.choice([1, -1]), 1 << (p - 1), pr.e + rng.randint(1, 8))
+        elif kind == 4:  # all-ones c plus a product that rounds it up
+            c = F.MPF(pr.s, (1 << p) - 1, pr.e + rng.randint(p - 4, p + 4))
+        elif kind == 5:
+            c = F.ZERO
+        else:  # c = x y exactly representable -> R = 0 or tiny
+            c = F.MPF(pr.s, pr.m ^ rng.getrandbits(rng.randint(1, 40)), pr.e)
+        cases.append((c, x, y))
+    out = _fused_run(emu_bin, cases, L)
+    for (c, x, y), r in zip(cases, out):
+        assert r != "viol", (c, x, y)
+        if not r.startswith("fb"):
+            assert from_line(r, L) == F.fms(c, x, y, p), (c, x, y)

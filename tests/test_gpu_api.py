@@ -119,3 +119,24 @@ def test_real_nccl_ranks_bit_identical(api, world):
     assert res[0][2] == want[1] and res[0][3] == want[2]
     for r in range(world):
         assert res[r][0] == want[0].lambda_hi and res[r][1] == want[0].lambda_lo
+
+
+@pytest.mark.parametrize("beta,n,L,k", [((1, 1), 256, 192, 8), ((1, 3), 96, 1152, 12), ((1, 2), 48, 8, 8)])
+def test_fused_rounding_bit_identical_to_rounding_pass(api, beta, n, L, k, monkeypatch):
+    """The certified rounding fused into the product kernel (tc_fused.cuh) gives
+    the same factors as the separate rounding pass, its exponent prediction
+    never fails the normalisation check, and with every 7th item forced to the
+    exact redo the bits do not change either."""
+    monkeypatch.setenv("HK_TC", "1")
+    mu, _ = api.build_hankel(beta, n, L)
+    out = {}
+    for fuse, force in (("0", "0"), ("1", "0"), ("1", "1")):
+        monkeypatch.setenv("HK_TC_FUSE", fuse)
+        monkeypatch.setenv("HK_TC_FORCE_FIX", force)
+        with api.Context(L) as ctx:
+            out[(fuse, force)] = run(ctx, mu, k)
+            assert ctx.fused_violations() == 0
+    base = out[("0", "0")]
+    for key in (("1", "0"), ("1", "1")):
+        assert out[key][1] == base[1] and out[key][2] == base[2], key
+        assert out[key][0].lambda_hi == base[0].lambda_hi

@@ -9,11 +9,16 @@
 // stdin protocol (all numbers decimal except limbs, which are hex):
 //   op <fms|mul|add|recip> <L> <count>       then count items of 3/2/2/1 operands
 //   path <L> <N> <m>                        then 2N-1 moments
+//   fused <L> <count>                       then count (c, x, y) triples: the
+//       tensor-core short product (byte columns from limb L-8, as k_tc_bulk
+//       forms it) streamed through FusedRow (csrc/tc_fused.cuh) in drain order;
+//       prints the result, or "fb" when the item goes to the exact redo
 // operand line: "<sign> <exp> <limb0> ... <limb L-1>"
 // Output: one operand line per result (op), or for `path`: D (N lines), the
 // L^{-1} rows (N*m lines, row-major), the block (m*m lines), then "err <col>".
 #define HK_WARP_EMU 1
 #include "../paper_1810_01478_b200/csrc/hk_items.cuh"
+#include "../paper_1810_01478_b200/csrc/tc_fused.cuh"
 
 #include <cstdio>
 #include <iostream>
@@ -92,6 +97,61 @@ int main() {
                 run_items(cnt, ws_words_for(L), ItemBatch{A.view(), B.view(), C.view(), O.view(), L, code});
             }
             for (long long e = 0; e < cnt; ++e) print_opd(O, e, L);
+        } else if (cmd == "fused") {
+            int L;
+            long long cnt;
+            std::cin >> L >> cnt;
+            HostArr Cc(cnt, L), X(cnt, L), Y(cnt, L);
+            for (long long e = 0; e < cnt; ++e) {
+                read_opd(Cc, e, L);
+                read_opd(X, e, L);
+                read_opd(Y, e, L);
+            }
+            const int nb = 4 * L, T0 = 4 * L - 32, nl = L + 8;
+            for (long long e = 0; e < cnt; ++e) {
+                const uint8_t* xb = reinterpret_cast<const uint8_t*>(&X.d[size_t(e) * L]);
+                const uint8_t* yb = reinterpret_cast<const uint8_t*>(&Y.d[size_t(e) * L]);
+                // short product: column sums t >= T0, carried into limbs (the epilogue's conversion)
+                std::vector<uint32_t> P(size_t(nl) + 8, 0u);
+                uint64_t carry = 0;
+                for (int q = 0; q < 4 * nl; q += 4) {
+                    uint64_t sum = carry;
+                    for (int h = 0; h < 4; ++h) {
+                        const int t = T0 + q + h;
+                        uint64_t col = 0;
+                        for (int u = 0; u < nb; ++u)
+                            if (t - u >= 0 && t - u < nb) col += uint64_t(yb[u]) * xb[t - u];
+                        sum += col << (8 * h);
+                    }
+                    P[size_t(q / 4)] = uint32_t(sum);
+                    carry = sum >> 32;
+                }
+                const uint32_t* xl = &X.d[size_t(e) * L];
+                const uint32_t* yl = &Y.d[size_t(e) * L];
+                auto top64 = [&](const uint32_t* l) { return (uint64_t(l[L - 1]) << 32) | (L > 1 ? l[L - 2] : 0u); };
+                std::vector<uint32_t> cl(Cc.d.begin() + e * L, Cc.d.begin() + (e + 1) * L);
+                FusedRow fr;
+                fr.setup(cl.data(), Cc.m[size_t(e)], top64(xl), X.m[size_t(e)], top64(yl), Y.m[size_t(e)], L);
+                int g = 0;
+                for (; g < (nl + 7) / 8; ++g) {
+                    uint32_t pl[8];
+                    for (int t = 0; t < 8; ++t) pl[t] = P[size_t(8 * g + t)];
+                    if (fr.status == 1) fr.group(g, pl);
+                }
+                const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                while (fr.wants(g)) fr.group(g++, zero);
+                Meta mo{0, 0};
+                bool viol = false;
+                const bool ok = fr.finish(&mo, &viol);
+                if (viol) std::printf("viol\n");
+                else if (!ok) std::printf("fb %d\n", fr.why);
+                else if (fr.status == 0) print_opd(Cc, e, L);
+                else {
+                    std::printf("%d %d", mo.sign, mo.exp);
+                    for (int i = 0; i < L; ++i) std::printf(" %x", cl[size_t(i)]);
+                    std::printf("\n");
+                }
+            }
         } else if (cmd == "path") {
             int L, N, m;
             std::cin >> L >> N >> m;

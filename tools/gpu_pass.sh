@@ -16,11 +16,11 @@ for w in $what; do
     ncu)
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tc_bulk -s 300 -c 1 \
         -o gpurun_out/${tag}_prof_tcb_c4 -f python tools/one_run.py c4 1 > gpurun_out/${tag}_ncu_tcb_c4.log 2>&1; echo "ncu tcb rc=$?"
-      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ItemTcRound -s 300 -c 1 \
-        -o gpurun_out/${tag}_prof_round_c4 -f python tools/one_run.py c4 1 > gpurun_out/${tag}_ncu_round_c4.log 2>&1; echo "ncu round rc=$?";;
+      ;;
     launches)
       timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 5000 \
         --log-file gpurun_out/${tag}_launches_c4.csv python tools/one_run.py c4 1 > gpurun_out/${tag}_launches_c4.log 2>&1; echo "launches rc=$?";;
+    sweep) tools/env_sweep.sh c4 "HK_TC_FUSE=0" "HK_TC_FUSE=1" "HK_TC_FUSE=1 HK_TC_SLEEP=64" "HK_TC_FUSE=1 HK_TC_SLEEP=256" "HK_TC_FUSE=0 HK_TC_SLEEP=128" > gpurun_out/${tag}_sweep.txt 2>&1; echo "sweep rc=$?";;
     ref) timeout 1500 python bench.py --impl reference --steps 1 --warmup 0 --ref-golden-precision > gpurun_out/${tag}_ref_c4.json 2> gpurun_out/${tag}_ref_c4.err; echo "ref rc=$?";;
   esac
 done
