@@ -11,7 +11,7 @@ CSRC := paper_1810_01478_b200/csrc
 HDRS := $(wildcard $(CSRC)/*.cuh) include/hankel_b200.h
 LIB := paper_1810_01478_b200/libhankel_b200.so
 
-all: $(LIB) build/emu_mp build/test_facade
+all: $(LIB) build/emu_mp build/test_facade build/record_fmt
 
 build:
 	mkdir -p build
@@ -32,6 +32,10 @@ build/emu_mp: tools/emu_mp.cpp $(HDRS) $(CSRC)/warp_emu.h | build
 build/test_facade: tests/cpp/test_facade.cpp include/hankel_b200.hpp include/hankel_b200.h $(LIB) | build
 	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -Lpaper_1810_01478_b200 -lhankel_b200 \
 		-Wl,-rpath,'$$ORIGIN/../paper_1810_01478_b200'
+
+# the RunRecord writers alone (byte parity with the reference's, tests/test_pipeline.py)
+build/record_fmt: tests/cpp/record_fmt.cpp include/hankel_b200.hpp include/hankel_b200.h | build
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $<
 
 oracle:
 	$(MAKE) -C oracle

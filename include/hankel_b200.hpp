@@ -35,6 +35,7 @@
 #include "hankel_b200.h"
 
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -765,49 +766,209 @@ inline void write_scan_csv(std::ostream& os, const std::vector<RunRecord>& recor
     for (const auto& r : records) os << to_csv_row(r) << '\n';
 }
 
-// pipeline.cpp:213-231 (+ p_bits and [hi, lo] lambda pairs)
+namespace detail {
+// A double as the reference's JSON writer (nlohmann::json::dump) prints it:
+// the Grisu2 digits (Loitsch 2010; round-trip, usually but not always the
+// shortest), positional between 1e-4 and 1e15, otherwise d.ddde+XX;
+// non-finite -> null.  Checked byte for byte against the reference's writer
+// (tests/test_pipeline.py).
+namespace grisu {
+struct Fp {
+    uint64_t f;
+    int e;
+};
+inline Fp mul(Fp x, Fp y) { // upper 64 bits of the 128-bit product, rounded
+    const uint64_t ul = x.f & 0xffffffffu, uh = x.f >> 32, vl = y.f & 0xffffffffu, vh = y.f >> 32;
+    const uint64_t p0 = ul * vl, p1 = ul * vh, p2 = uh * vl, p3 = uh * vh;
+    const uint64_t q = (p0 >> 32) + (p1 & 0xffffffffu) + (p2 & 0xffffffffu) + (1ull << 31);
+    return Fp{p3 + (p2 >> 32) + (p1 >> 32) + (q >> 32), x.e + y.e + 64};
+}
+inline Fp normalize(Fp x) {
+    while (!(x.f >> 63)) {
+        x.f <<= 1;
+        --x.e;
+    }
+    return x;
+}
+struct Pow10 {
+    uint64_t f;
+    int e, k;
+};
+// 10^k, k = -300 .. 324 step 8, significand rounded to 64 bits (tools/gen_pow10.py)
+inline const Pow10* pow10_table() {
+    static const Pow10 t[79] = {
+        {0xAB70FE17C79AC6CAull, -1060, -300}, {0xFF77B1FCBEBCDC4Full, -1034, -292},
+        {0xBE5691EF416BD60Cull, -1007, -284}, {0x8DD01FAD907FFC3Cull, -980, -276},
+        {0xD3515C2831559A83ull, -954, -268}, {0x9D71AC8FADA6C9B5ull, -927, -260},
+        {0xEA9C227723EE8BCBull, -901, -252}, {0xAECC49914078536Dull, -874, -244},
+        {0x823C12795DB6CE57ull, -847, -236}, {0xC21094364DFB5637ull, -821, -228},
+        {0x9096EA6F3848984Full, -794, -220}, {0xD77485CB25823AC7ull, -768, -212},
+        {0xA086CFCD97BF97F4ull, -741, -204}, {0xEF340A98172AACE5ull, -715, -196},
+        {0xB23867FB2A35B28Eull, -688, -188}, {0x84C8D4DFD2C63F3Bull, -661, -180},
+        {0xC5DD44271AD3CDBAull, -635, -172}, {0x936B9FCEBB25C996ull, -608, -164},
+        {0xDBAC6C247D62A584ull, -582, -156}, {0xA3AB66580D5FDAF6ull, -555, -148},
+        {0xF3E2F893DEC3F126ull, -529, -140}, {0xB5B5ADA8AAFF80B8ull, -502, -132},
+        {0x87625F056C7C4A8Bull, -475, -124}, {0xC9BCFF6034C13053ull, -449, -116},
+        {0x964E858C91BA2655ull, -422, -108}, {0xDFF9772470297EBDull, -396, -100},
+        {0xA6DFBD9FB8E5B88Full, -369, -92}, {0xF8A95FCF88747D94ull, -343, -84},
+        {0xB94470938FA89BCFull, -316, -76}, {0x8A08F0F8BF0F156Bull, -289, -68},
+        {0xCDB02555653131B6ull, -263, -60}, {0x993FE2C6D07B7FACull, -236, -52},
+        {0xE45C10C42A2B3B06ull, -210, -44}, {0xAA242499697392D3ull, -183, -36},
+        {0xFD87B5F28300CA0Eull, -157, -28}, {0xBCE5086492111AEBull, -130, -20},
+        {0x8CBCCC096F5088CCull, -103, -12}, {0xD1B71758E219652Cull, -77, -4},
+        {0x9C40000000000000ull, -50, 4}, {0xE8D4A51000000000ull, -24, 12},
+        {0xAD78EBC5AC620000ull, 3, 20}, {0x813F3978F8940984ull, 30, 28},
+        {0xC097CE7BC90715B3ull, 56, 36}, {0x8F7E32CE7BEA5C70ull, 83, 44},
+        {0xD5D238A4ABE98068ull, 109, 52}, {0x9F4F2726179A2245ull, 136, 60},
+        {0xED63A231D4C4FB27ull, 162, 68}, {0xB0DE65388CC8ADA8ull, 189, 76},
+        {0x83C7088E1AAB65DBull, 216, 84}, {0xC45D1DF942711D9Aull, 242, 92},
+        {0x924D692CA61BE758ull, 269, 100}, {0xDA01EE641A708DEAull, 295, 108},
+        {0xA26DA3999AEF774Aull, 322, 116}, {0xF209787BB47D6B85ull, 348, 124},
+        {0xB454E4A179DD1877ull, 375, 132}, {0x865B86925B9BC5C2ull, 402, 140},
+        {0xC83553C5C8965D3Dull, 428, 148}, {0x952AB45CFA97A0B3ull, 455, 156},
+        {0xDE469FBD99A05FE3ull, 481, 164}, {0xA59BC234DB398C25ull, 508, 172},
+        {0xF6C69A72A3989F5Cull, 534, 180}, {0xB7DCBF5354E9BECEull, 561, 188},
+        {0x88FCF317F22241E2ull, 588, 196}, {0xCC20CE9BD35C78A5ull, 614, 204},
+        {0x98165AF37B2153DFull, 641, 212}, {0xE2A0B5DC971F303Aull, 667, 220},
+        {0xA8D9D1535CE3B396ull, 694, 228}, {0xFB9B7CD9A4A7443Cull, 720, 236},
+        {0xBB764C4CA7A44410ull, 747, 244}, {0x8BAB8EEFB6409C1Aull, 774, 252},
+        {0xD01FEF10A657842Cull, 800, 260}, {0x9B10A4E5E9913129ull, 827, 268},
+        {0xE7109BFBA19C0C9Dull, 853, 276}, {0xAC2820D9623BF429ull, 880, 284},
+        {0x80444B5E7AA7CF85ull, 907, 292}, {0xBF21E44003ACDD2Dull, 933, 300},
+        {0x8E679C2F5E44FF8Full, 960, 308}, {0xD433179D9C8CB841ull, 986, 316},
+        {0x9E19DB92B4E31BA9ull, 1013, 324},
+    };
+    return t;
+}
+inline void round_last(std::string& buf, uint64_t dist, uint64_t delta, uint64_t rest, uint64_t ten_k) {
+    while (rest < dist && delta - rest >= ten_k && (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+        --buf.back();
+        rest += ten_k;
+    }
+}
+// digits of v > 0 and the decimal exponent: v ~= digits * 10^dexp
+inline std::string digits(double v, int& dexp) {
+    uint64_t bits;
+    std::memcpy(&bits, &v, 8);
+    const uint64_t E = bits >> 52, F = bits & ((1ull << 52) - 1);
+    const Fp w = E == 0 ? Fp{F, 1 - 1075} : Fp{F + (1ull << 52), int(E) - 1075};
+    const bool closer = F == 0 && E > 1;
+    const Fp mp = normalize(Fp{2 * w.f + 1, w.e - 1});
+    const Fp mm0 = closer ? Fp{4 * w.f - 1, w.e - 2} : Fp{2 * w.f - 1, w.e - 1};
+    const Fp mm{mm0.f << (mm0.e - mp.e), mp.e};
+    const int f = -60 - mp.e - 1;
+    const int k = (f * 78913) / (1 << 18) + (f > 0 ? 1 : 0);
+    const Pow10 c = pow10_table()[(300 + k + 7) / 8];
+    const Fp cw{c.f, c.e};
+    const Fp W = mul(normalize(w), cw), Wm = mul(mm, cw), Wp = mul(mp, cw);
+    const Fp Mm{Wm.f + 1, Wm.e}, Mp{Wp.f - 1, Wp.e};
+    dexp = -c.k;
+    uint64_t delta = Mp.f - Mm.f, dist = Mp.f - W.f;
+    const int ne = -Mp.e;
+    const uint64_t one = 1ull << ne;
+    uint32_t p1 = uint32_t(Mp.f >> ne);
+    uint64_t p2 = Mp.f & (one - 1);
+    uint32_t pow10 = 1;
+    int n = 1;
+    for (uint32_t t = 1000000000u, d = 10; d > 1; t /= 10, --d)
+        if (p1 >= t) {
+            pow10 = t;
+            n = int(d);
+            break;
+        }
+    std::string buf;
+    while (n > 0) {
+        buf += char('0' + p1 / pow10);
+        p1 %= pow10;
+        --n;
+        const uint64_t rest = (uint64_t(p1) << ne) + p2;
+        if (rest <= delta) {
+            dexp += n;
+            round_last(buf, dist, delta, rest, uint64_t(pow10) << ne);
+            return buf;
+        }
+        pow10 /= 10;
+    }
+    int m = 0;
+    for (;;) {
+        p2 *= 10;
+        buf += char('0' + (p2 >> ne));
+        p2 &= one - 1;
+        ++m;
+        delta *= 10;
+        dist *= 10;
+        if (p2 <= delta) break;
+    }
+    dexp -= m;
+    round_last(buf, dist, delta, p2, one);
+    return buf;
+}
+} // namespace grisu
+
+inline std::string json_number(double v) {
+    if (!std::isfinite(v)) return "null";
+    std::string out = std::signbit(v) ? "-" : "";
+    if (v == 0) return out + "0.0";
+    int dexp = 0;
+    const std::string d = grisu::digits(std::fabs(v), dexp);
+    const int k = int(d.size()), n = k + dexp; // decimal point after n digits
+    if (k <= n && n <= 15) {
+        out += d + std::string(size_t(n - k), '0') + ".0";
+    } else if (0 < n && n <= 15) {
+        out += d.substr(0, size_t(n)) + "." + d.substr(size_t(n));
+    } else if (-4 < n && n <= 0) {
+        out += "0." + std::string(size_t(-n), '0') + d;
+    } else {
+        out += d.substr(0, 1);
+        if (k > 1) out += "." + d.substr(1);
+        const int e = n - 1;
+        out += e < 0 ? "e-" : "e+";
+        if (std::abs(e) < 10) out += '0';
+        out += std::to_string(std::abs(e));
+    }
+    return out;
+}
+inline void json_array(std::ostream& os, const std::vector<double>& v, const std::string& ind) {
+    if (v.empty()) {
+        os << "[]";
+        return;
+    }
+    os << "[\n";
+    for (size_t i = 0; i < v.size(); ++i) os << (i ? ",\n" : "") << ind << "  " << json_number(v[i]);
+    os << "\n" << ind << "]";
+}
+} // namespace detail
+
+// pipeline.cpp:213-232, byte for byte: the reference builds an nlohmann::json
+// object (keys in sorted order) and dumps it with indent 2
 inline std::string to_json(const RunRecord& r) {
     std::ostringstream os;
-    os << std::setprecision(17);
-    auto num = [&](double v) {
-        if (std::isnan(v)) os << "null";
-        else os << v;
-    };
-    auto arr = [&](const std::vector<double>& v) {
-        os << '[';
-        for (size_t i = 0; i < v.size(); ++i) {
-            if (i) os << ", ";
-            num(v[i]);
-        }
-        os << ']';
-    };
     os << "{\n  \"N\": " << r.n << ",\n  \"beta\": \"" << r.beta.beta_num << '/' << r.beta.beta_den
-       << "\",\n  \"bits\": " << r.bits << ",\n  \"k\": " << r.k << ",\n  \"workers\": " << r.workers
-       << ",\n  \"lambda\": ";
-    arr(r.lambda);
-    os << ",\n  \"trunc_err\": ";
-    arr(r.trunc_err);
+       << "\",\n  \"bits\": " << r.bits << ",\n  \"k\": " << r.k << ",\n  \"lambda\": ";
+    detail::json_array(os, r.lambda, "  ");
     if (r.required_bits > 0) os << ",\n  \"required_bits\": " << r.required_bits;
-    os << ",\n  \"timing\": {\"wall_s\": ";
-    num(r.wall_s);
-    os << ", \"ldlt_s\": ";
-    num(r.ldlt_s);
-    os << ", \"transpose_s\": ";
-    num(r.transpose_s);
-    os << ", \"invL_s\": ";
-    num(r.invL_s);
-    os << ", \"invL_arith_s\": ";
-    num(r.invL_arith_s);
-    os << ", \"invL_comm_s\": ";
-    num(r.invL_comm_s);
-    os << ", \"invH_s\": ";
-    num(r.invH_s);
-    os << ", \"eigen_s\": ";
-    num(r.eigen_s);
-    os << "},\n  \"p_bits\": " << r.p_bits << ",\n  \"lambda_lo\": ";
-    arr(r.lambda_lo);
-    os << "\n}";
+    const std::pair<const char*, double> timing[] = {
+        {"eigen_s", r.eigen_s},           {"invH_s", r.invH_s}, {"invL_arith_s", r.invL_arith_s},
+        {"invL_comm_s", r.invL_comm_s},   {"invL_s", r.invL_s}, {"ldlt_s", r.ldlt_s},
+        {"transpose_s", r.transpose_s},   {"wall_s", r.wall_s}};
+    os << ",\n  \"timing\": {";
+    for (size_t q = 0; q < 8; ++q)
+        os << (q ? ",\n" : "\n") << "    \"" << timing[q].first << "\": " << detail::json_number(timing[q].second);
+    os << "\n  },\n  \"trunc_err\": ";
+    detail::json_array(os, r.trunc_err, "  ");
+    os << ",\n  \"workers\": " << r.workers << "\n}";
     return os.str();
+}
+
+// to_json plus this build's extras: p_bits and the low parts of the ~32-digit lambdas
+inline std::string to_json_ext(const RunRecord& r) {
+    std::string s = to_json(r);
+    std::ostringstream os;
+    os << ",\n  \"lambda_lo\": ";
+    detail::json_array(os, r.lambda_lo, "  ");
+    os << ",\n  \"p_bits\": " << r.p_bits << "\n}";
+    s.resize(s.size() - 2); // drop the closing "\n}"
+    return s + os.str();
 }
 
 } // namespace hankel::b200

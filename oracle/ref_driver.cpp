@@ -17,6 +17,14 @@
 //   ref_driver time  --beta 1/2 --n 256 --bits 2048 --k 8 --workers 8
 //       hankel::compute() itself (proj/src/pipeline.cpp:26-72) and its
 //       to_json(RunRecord) (pipeline.cpp:213-232): the CPU baseline arm.
+//
+//   ref_driver record  < records
+//       The reference's RunRecord writers on given records (byte-level parity
+//       of the product's to_csv_row / to_json): per stdin line
+//         n bnum bden bits k workers required_bits nl l_1..l_nl nt t_1..t_nt
+//         wall ldlt transpose invL invL_arith invL_comm invH eigen
+//       (doubles as C99 hex floats) prints to_csv_row (pipeline.cpp:150-160),
+//       then to_json (pipeline.cpp:213-232), then a line "@@".
 #include "hankel/errors.hpp"
 #include "hankel/inversion.hpp"
 #include "hankel/jacobi.hpp"
@@ -165,8 +173,36 @@ int run_time(const Args& a) {
 
 } // namespace
 
+int run_record() {
+    std::string line;
+    while (std::getline(std::cin, line)) {
+        if (line.empty()) continue;
+        std::istringstream is(line);
+        auto dbl = [&]() {
+            std::string t;
+            is >> t;
+            return std::strtod(t.c_str(), nullptr);
+        };
+        RunRecord r;
+        unsigned bn = 1, bd = 2;
+        is >> r.n >> bn >> bd >> r.bits >> r.k >> r.workers >> r.required_bits;
+        r.beta = WeightSpec::make(bn, bd);
+        size_t nl = 0, nt = 0;
+        is >> nl;
+        for (size_t i = 0; i < nl; ++i) r.lambda.push_back(dbl());
+        is >> nt;
+        for (size_t i = 0; i < nt; ++i) r.trunc_err.push_back(dbl());
+        for (double* f : {&r.wall_s, &r.ldlt_s, &r.transpose_s, &r.invL_s, &r.invL_arith_s, &r.invL_comm_s, &r.invH_s,
+                          &r.eigen_s})
+            *f = dbl();
+        std::cout << to_csv_row(r) << "\n" << to_json(r) << "\n@@" << std::endl;
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
     try {
+        if (argc >= 2 && std::string(argv[1]) == "record") return run_record();
         const Args a = parse(argc, argv);
         if (a.mode == "dump") return run_dump(a);
         if (a.mode == "time") return run_time(a);

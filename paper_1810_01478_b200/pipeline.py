@@ -198,17 +198,152 @@ def read_scan_csv(f) -> list[tuple[float, float]]:
     return pts
 
 
+_POW10 = None
+
+
+def _pow10_table():
+    """10^k, k = -300 .. 324 step 8, as (64-bit significand rounded to nearest, exponent, k)."""
+    global _POW10
+    if _POW10 is None:
+        from fractions import Fraction
+
+        rows = []
+        for k in range(-300, 325, 8):
+            v = Fraction(10) ** k
+            e = v.numerator.bit_length() - v.denominator.bit_length() - 64
+            while v / Fraction(2) ** e >= 2 ** 64:
+                e += 1
+            while v / Fraction(2) ** e < 2 ** 63:
+                e -= 1
+            q = v / Fraction(2) ** e
+            f = int(q) + (1 if q - int(q) >= Fraction(1, 2) else 0)
+            rows.append((f // 2, e + 1, k) if f == 2 ** 64 else (f, e, k))
+        _POW10 = rows
+    return _POW10
+
+
+def _grisu2_digits(v: float):
+    """Grisu2 (Loitsch 2010), as the reference's JSON writer runs it: digits and
+    decimal exponent of v > 0 (round-trip; usually, not always, the shortest)."""
+    import struct
+
+    M64 = (1 << 64) - 1
+
+    def mul(x, y):
+        ul, uh, vl, vh = x[0] & 0xFFFFFFFF, x[0] >> 32, y[0] & 0xFFFFFFFF, y[0] >> 32
+        p0, p1, p2, p3 = ul * vl, ul * vh, uh * vl, uh * vh
+        q = (p0 >> 32) + (p1 & 0xFFFFFFFF) + (p2 & 0xFFFFFFFF) + (1 << 31)
+        return ((p3 + (p2 >> 32) + (p1 >> 32) + (q >> 32)) & M64, x[1] + y[1] + 64)
+
+    def normalize(x):
+        f, e = x
+        while f >> 63 == 0:
+            f, e = f << 1, e - 1
+        return f, e
+
+    bits = struct.unpack("<Q", struct.pack("<d", v))[0]
+    E, F = bits >> 52, bits & ((1 << 52) - 1)
+    w = (F, 1 - 1075) if E == 0 else (F + (1 << 52), E - 1075)
+    mp = normalize((2 * w[0] + 1, w[1] - 1))
+    mm0 = (4 * w[0] - 1, w[1] - 2) if (F == 0 and E > 1) else (2 * w[0] - 1, w[1] - 1)
+    mm = (mm0[0] << (mm0[1] - mp[1]), mp[1])
+    f = -60 - mp[1] - 1
+    t = abs(f * 78913) >> 18
+    k = (t if f >= 0 else -t) + (1 if f > 0 else 0)  # C++ truncating division
+    cf, ce, ck = _pow10_table()[(300 + k + 7) // 8]
+    W, Wm, Wp = mul(normalize(w), (cf, ce)), mul(mm, (cf, ce)), mul(mp, (cf, ce))
+    Mm, Mp = Wm[0] + 1, Wp[0] - 1
+    dexp = -ck
+    delta, dist = Mp - Mm, Mp - W[0]
+    ne = -Wp[1]
+    one = 1 << ne
+    p1, p2 = Mp >> ne, Mp & (one - 1)
+    n, pow10 = 1, 1
+    for d in range(10, 1, -1):
+        if p1 >= 10 ** (d - 1):
+            n, pow10 = d, 10 ** (d - 1)
+            break
+    buf = []
+
+    def round_last(dist, delta, rest, ten_k):
+        while rest < dist and delta - rest >= ten_k and (rest + ten_k < dist or dist - rest > rest + ten_k - dist):
+            buf[-1] -= 1
+            rest += ten_k
+
+    while n > 0:
+        buf.append(p1 // pow10)
+        p1 %= pow10
+        n -= 1
+        rest = (p1 << ne) + p2
+        if rest <= delta:
+            round_last(dist, delta, rest, pow10 << ne)
+            return "".join(map(str, buf)), dexp + n
+        pow10 //= 10
+    m = 0
+    while True:
+        p2 *= 10
+        buf.append(p2 >> ne)
+        p2 &= one - 1
+        m += 1
+        delta, dist = delta * 10, dist * 10
+        if p2 <= delta:
+            break
+    round_last(dist, delta, p2, one)
+    return "".join(map(str, buf)), dexp - m
+
+
+def _json_number(v: float) -> str:
+    """A double as the reference's JSON writer (nlohmann::json::dump) prints it:
+    Grisu2 digits, positional between 1e-4 and 1e15, else d.ddde+XX; non-finite -> null."""
+    import math
+
+    if v != v or math.isinf(v):
+        return "null"
+    sign = "-" if math.copysign(1.0, v) < 0 else ""
+    if v == 0:
+        return sign + "0.0"
+    digits, dexp = _grisu2_digits(abs(v))
+    k = len(digits)
+    n = k + dexp
+    if k <= n <= 15:
+        out = digits + "0" * (n - k) + ".0"
+    elif 0 < n <= 15:
+        out = digits[:n] + "." + digits[n:]
+    elif -4 < n <= 0:
+        out = "0." + "0" * (-n) + digits
+    else:
+        e = n - 1
+        out = digits[0] + ("." + digits[1:] if k > 1 else "") + ("e-" if e < 0 else "e+") + f"{abs(e):02d}"
+    return sign + out
+
+
+def _json_array(v) -> str:
+    if not v:
+        return "[]"
+    return "[\n" + ",\n".join("    " + _json_number(x) for x in v) + "\n  ]"
+
+
 def to_json(r: RunRecord) -> str:
-    """pipeline.cpp:213-231 (plus p and the extended-precision lambda)."""
+    """pipeline.cpp:213-232 byte for byte (the reference's nlohmann::json object,
+    keys sorted, dump(2))."""
+    parts = [f'"N": {r.n}', f'"beta": "{r.beta[0]}/{r.beta[1]}"', f'"bits": {r.bits}', f'"k": {r.k}',
+             f'"lambda": {_json_array(r.lambda_)}']
+    if r.required_bits > 0:
+        parts.append(f'"required_bits": {r.required_bits}')
+    timing = (("eigen_s", r.eigen_s), ("invH_s", r.invH_s), ("invL_arith_s", r.invL_arith_s),
+              ("invL_comm_s", r.invL_comm_s), ("invL_s", r.invL_s), ("ldlt_s", r.ldlt_s),
+              ("transpose_s", r.transpose_s), ("wall_s", r.wall_s))
+    parts.append('"timing": {\n' + ",\n".join(f'    "{k}": {_json_number(v)}' for k, v in timing) + "\n  }")
+    parts.append(f'"trunc_err": {_json_array(r.trunc_err)}')
+    parts.append(f'"workers": {r.workers}')
+    return "{\n" + ",\n".join("  " + x for x in parts) + "\n}"
+
+
+def to_json_ext(r: RunRecord) -> str:
+    """to_json plus this build's extras: p and the (hi, lo) pairs of the ~32-digit lambdas."""
     import json
 
-    j = {"N": r.n, "beta": f"{r.beta[0]}/{r.beta[1]}", "bits": r.bits, "k": r.k, "workers": r.workers,
-         "lambda": r.lambda_, "trunc_err": r.trunc_err}
-    if r.required_bits > 0:
-        j["required_bits"] = r.required_bits
-    j["timing"] = {"wall_s": r.wall_s, "ldlt_s": r.ldlt_s, "transpose_s": r.transpose_s, "invL_s": r.invL_s,
-                   "invL_arith_s": r.invL_arith_s, "invL_comm_s": r.invL_comm_s, "invH_s": r.invH_s,
-                   "eigen_s": r.eigen_s}
+    j = json.loads(to_json(r))
     j["p_bits"] = r.p
     j["lambda_hi_lo"] = [[h, lo] for h, lo in zip(r.lambda_hi, r.lambda_lo)]
     return json.dumps(j, indent=2)
