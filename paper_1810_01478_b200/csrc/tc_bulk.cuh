@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             fr.setup(a.S.limbs(ec, L), a.S.m[ec], xt, xm, yt, a.Y.m[k], L);
             if (a.force_fb && item % 7 == 3 && fr.status != 0) fr.status = 2;
         }
+        fr.prefetch(8 * c_lo, 16); // the first two chunks' c limbs
         uint32_t* stg = sStg + 64 * r; // 16 x 16-byte cells, XOR-swizzled by row (conflict-free)
         const int sw = r & 15;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             tc::fence_before();
             __syncwarp();
             if (ln == 0) tc::mbar_arrive(&accE[ab]); // the MMAs of chunk c + 1 may now overwrite it
+            fr.prefetch(8 * (c + 2), 8);              // c limbs of chunk c + 2, while c and c + 1 stream
             for (int gg = 0; gg < 8; ++gg) {
                 const int g = 8 * c + gg;
                 if (!fr.wants(g)) continue;

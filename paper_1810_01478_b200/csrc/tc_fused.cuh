@@ -232,6 +232,20 @@ struct FusedRow {
         status = 1;
     }
 
+    // the c limbs groups g0 .. g0 + ng - 1 will read, into L2 (one bulk prefetch;
+    // issued a chunk ahead, so the in-order loads of the stream hit L2)
+    HK_DEV void prefetch(int g0, int ng) const {
+        if (status != 1 || czero) return;
+        int lo = 8 * g0 + (Qc - Qp - 1), hi = 8 * (g0 + ng) + (Qc - Qp - 1) + 9; // limbs [lo, hi)
+        lo = lo < 0 ? 0 : lo & ~3;
+        hi = hi > L ? L : hi;
+        if (hi <= lo) return;
+#if defined(__CUDA_ARCH__)
+        const uint32_t bytes = uint32_t((hi - lo) * 4 + 15) & ~15u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c + lo), "r"(bytes) : "memory");
+#endif
+    }
+
     // group g: product limbs pl = scratch limbs [8 g, 8 g + 8) (zeros past the product)
     HK_DEV int group_block(int g) const { return (8 * g - 1 - Qp - ow) >> 3; }
     HK_DEV bool wants(int g) const { return status == 1 && group_block(g) < nblocks(); }
