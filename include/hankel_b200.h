@@ -193,6 +193,12 @@ int hk_nccl_unique_id(void* out128);
 int hk_create_sharded(int device, int limbs, int rank, int world, const void* nccl_id128, hk_ctx** out);
 int hk_world(const hk_ctx* ctx, int* rank, int* world);
 
+/* A caller's column -> rank map for the sharded LDLT of order n (any map with
+ * owners in [0, world); ColumnAssignment of decompose_parallel, ldlt.hpp:13-21,
+ * 97-99 — the reference accepts any assignment, ldlt.cpp:355-395).  Without it
+ * the context uses assign_columns(n, world).  Results do not depend on it. */
+int hk_set_owner_map(hk_ctx* ctx, int n, const int32_t* owner);
+
 /* Balanced round-robin (boustrophedon) ownership map, assign_columns
  * (ldlt.cpp:22-35): owner[c] for c < n. */
 int hk_assign_columns(int n, int workers, int32_t* owner);

@@ -411,9 +411,12 @@ inline LdltFactors decompose_parallel(const MomentTable& table, const ColumnAssi
                                       const BroadcastPolicy& = {}, WorkerTimings* host_timings = nullptr) {
     if (assignment.n != table.order() || assignment.workers < 1 || int(assignment.owner.size()) != assignment.n)
         throw std::invalid_argument("decompose_parallel: assignment does not match the table");
-    if (assignment.owner != assign_columns(assignment.n, assignment.workers).owner)
-        throw std::invalid_argument("decompose_parallel: only the balanced round-robin assignment is supported");
-    return decompose_parallel(detail::default_device(table.limbs(), assignment.workers), table, host_timings);
+    Device& dev = detail::default_device(table.limbs(), assignment.workers);
+    if (assignment.workers > 1) { // any map (ldlt.cpp:355-395 takes any assignment); results do not depend on it
+        const std::vector<int32_t> o(assignment.owner.begin(), assignment.owner.end());
+        dev.check(hk_set_owner_map(dev.handle(), assignment.n, o.data()));
+    }
+    return decompose_parallel(dev, table, host_timings);
 }
 
 // ---------------------------------------------------------------- inverse

@@ -72,6 +72,7 @@ def lib():
             "hk_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]),
             "hk_world": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "hk_set_limbs": (C.c_int, [vp, C.c_int]),
+            "hk_set_owner_map": (C.c_int, [vp, C.c_int, i32p]),
             "hk_set_kernel_timing": (C.c_int, [vp, C.c_int]),
             "hk_kernel_times": (C.c_int, [vp, f64p]),
             "hk_fused_violations": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
@@ -342,6 +343,11 @@ class Context:
         """New precision on the same device / communicator (hk_set_limbs)."""
         _check(lib().hk_set_limbs(self.h, limbs), self.h)
         self.L = limbs
+
+    def set_owner_map(self, owner):
+        """Column -> rank map of the sharded LDLT (any ColumnAssignment, ldlt.hpp:13-21)."""
+        o = np.asarray(owner, dtype=np.int32)
+        _check(lib().hk_set_owner_map(self.h, len(o), _i32(o)), self.h)
 
     def set_kernel_timing(self, on: bool = True):
         _check(lib().hk_set_kernel_timing(self.h, 1 if on else 0), self.h)

@@ -228,7 +228,9 @@ struct hk_ctx {
     void* nccl_comm = nullptr;       // ncclComm_t (one rank per process)
     void* bcast_buf = nullptr;       // device staging of the root's result broadcast
     std::vector<Shard> shards;
-    std::vector<int> owner;          // assign_columns(n, world)
+    std::vector<int> owner;          // assign_columns(n, world), or a caller's map (hk_set_owner_map)
+    bool owner_custom = false;
+    long long owner_version = 0;     // bumped when the map changes (the step graph depends on it)
 };
 
 namespace {
@@ -1596,7 +1598,7 @@ MpArr slot3(const DevArr& a, int N, int L, int i) {
 }
 
 void shard_setup(hk_ctx* c, Shard& s, int N) {
-    if (s.setup_n == N) return; // the maps depend on (N, world) only
+    if (s.setup_n == N) return; // the maps depend on (N, world, owner map) only (setup_n reset on a change)
     s.owned.clear();
     s.loc.assign(size_t(N), -1);
     s.off.assign(1, 0);
@@ -1878,9 +1880,12 @@ void gather_to_root(hk_ctx* c) {
 int dist_ldlt(hk_ctx* c) {
     const int N = c->n, L = c->L;
     if ((int)c->owner.size() != N) {
+        if (c->owner_custom)
+            throw HkError{HK_ERR_INVALID, "decompose_parallel: the column assignment was set for another order"};
         c->owner.assign(size_t(N), 0);
         hk_assign_columns(N, c->world, c->owner.data());
         for (auto& s : c->shards) s.setup_n = -1;
+        ++c->owner_version;
     }
     for (auto& s : c->shards) shard_setup(c, s, N);
     const bool tc = use_tc(c);
@@ -1899,7 +1904,7 @@ int dist_ldlt(hk_ctx* c) {
     }
     // the step graph is valid for the buffers it was captured on
     std::vector<const void*> sig{(const void*)(long long)N, (const void*)(long long)tc, c->tc_A, c->tc_P, c->tc_fb,
-                                 (const void*)(long long)c->kprof, c->mu.d};
+                                 (const void*)(long long)c->kprof, c->mu.d, (const void*)c->owner_version};
     for (auto& s : c->shards)
         for (const void* p : {(const void*)s.S.d, (const void*)s.panel.d, (const void*)s.B.d, (const void*)s.R.d,
                               (const void*)s.d_err, (const void*)s.d_fb, (const void*)s.d_erow, (const void*)s.d_owned})
@@ -2025,6 +2030,22 @@ int hk_kernel_times(hk_ctx* c, double* out6) {
             out6[4] = c->cev_steps;
         }
         out6[5] = c->t[1] * 1e3;
+        return HK_OK;
+    });
+}
+
+int hk_set_owner_map(hk_ctx* c, int n, const int32_t* owner) {
+    return guarded(c, [&] {
+        if (!(c->world > 1 || c->virt || c->nccl_comm))
+            return fail(c, HK_ERR_INVALID, "hk_set_owner_map: not a sharded context");
+        if (n < 1 || !owner) return fail(c, HK_ERR_INVALID, "hk_set_owner_map: need n >= 1 and a map");
+        for (int j = 0; j < n; ++j)
+            if (owner[j] < 0 || owner[j] >= c->world)
+                return fail(c, HK_ERR_INVALID, "hk_set_owner_map: owner out of range at column " + std::to_string(j));
+        c->owner.assign(owner, owner + n);
+        c->owner_custom = true;
+        ++c->owner_version;
+        for (auto& sh : c->shards) sh.setup_n = -1;
         return HK_OK;
     });
 }

@@ -188,6 +188,21 @@ static void device_cases() {
             CHECK(g.L_column(3).l == f.L_column(3).l);
             CHECK(g.assignment.workers == w);
         }
+        {   // any ColumnAssignment (ldlt.cpp:355-395): contiguous blocks and plain round robin
+            hb::ColumnAssignment blk{n, 3, std::vector<int>(size_t(n))}, rr{n, 4, std::vector<int>(size_t(n))};
+            for (int c = 0; c < n; ++c) {
+                blk.owner[size_t(c)] = c * 3 / n;
+                rr.owner[size_t(c)] = c % 4;
+            }
+            for (const auto& a : {blk, rr}) {
+                const auto g = hb::decompose_parallel(table, a);
+                CHECK(g.D.l == f.D.l && g.D.e == f.D.e && g.D.s == f.D.s);
+                CHECK(g.L_column(7).l == f.L_column(7).l);
+            }
+            hb::ColumnAssignment bad = rr;
+            bad.owner[5] = 9;
+            CHECK_THROWS_AS(hb::decompose_parallel(table, bad), std::invalid_argument);
+        }
         const auto rows = hb::transpose_redistribute(f);
         hb::WorkerTimings wt;
         const auto inv = hb::invert_L_partial_parallel(rows, 8, &wt);

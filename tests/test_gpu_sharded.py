@@ -113,3 +113,20 @@ def test_nccl_world1_c2_digest(api):
             ctx.compute(mu, k)
             assert digest(from_arr(ctx.D())) == g["D_sha256"]
             assert digest(from_arr(ctx.block())) == g["block_sha256"]
+
+
+@pytest.mark.parametrize("world,kind", [(3, "blocks"), (4, "round_robin"), (2, "all_on_1")])
+def test_virtual_sharded_any_owner_map(api, single, world, kind, monkeypatch):
+    """decompose_parallel takes any ColumnAssignment (ldlt.cpp:355-395), on both
+    product paths: bit-identical to the single-GPU factors."""
+    for tc in ("0", "1"):
+        monkeypatch.setenv("HK_TC", tc)
+        for (beta, n, L, k), (mu, (r0, D0, X0, M0)) in single.items():
+            if tc == "1" and L % 4:
+                continue
+            owner = {"blocks": [c * world // n for c in range(n)], "round_robin": [c % world for c in range(n)],
+                     "all_on_1": [1] * n}[kind]
+            with api.Context(L, world=world, virtual=True) as ctx:
+                ctx.set_owner_map(owner)
+                r1, D1, X1, M1 = results(ctx, mu, k)
+            assert D1 == D0 and X1 == X0 and M1 == M0, (beta, n, world, kind, tc)
