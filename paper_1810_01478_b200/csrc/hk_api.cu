@@ -174,6 +174,7 @@ struct hk_ctx {
     int bad_col = -1;
     bool factored = false, inverted = false, assembled = false;
     int sm_count = 148;
+    size_t smem_optin = 227 * 1024;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
     long long launches = 0;
     double t[7] = {0, 0, 0, 0, 0, 0, 0};
     cudaEvent_t ev[2] = {nullptr, nullptr};
@@ -333,6 +334,17 @@ void launch_cta(hk_ctx* c, const F& f, long long n, int ws_words, cudaStream_t s
 int ws_cta_words(int L) { return hk::ctaws_words(L); }
 int ws_cta_recip_words(int L) { return hk::ctarecipws_words(L); }
 
+// R_i = RNE(1/S_ii) (+ the pivot test): the CTA-cooperative reciprocal (the
+// critical path), or one warp's when its workspace does not fit a CTA's shared
+// memory (p beyond ~114,900 bits)
+void launch_recip(hk_ctx* c, int i, cudaStream_t st, bool pdl = false) {
+    const int N = c->n, L = c->L;
+    if (size_t(ws_cta_recip_words(L)) * 4 <= c->smem_optin)
+        launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, ws_cta_recip_words(L), st, pdl);
+    else
+        launch(c, hk::ItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, ws_recip_words(L), st, pdl);
+}
+
 int fail(hk_ctx* c, int code, const std::string& msg) {
     if (c) c->err = msg;
     return code;
@@ -443,7 +455,8 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     a.ewin = 1;
     if (const char* e = getenv("HK_TC_EWIN")) a.ewin = e[0] == '1' ? 1 : 0;
     if (a.fuse) a.ewin = 1;
-    const size_t need = hk::tc_smem_bytes(L, a.ewin != 0, a.fuse != 0);
+    if (const char* e = getenv("HK_TC_STAGES")) a.stages = std::max(2, std::min(hk::kTcStages, atoi(e)));
+    const size_t need = hk::tc_smem_bytes(L, a.ewin != 0, a.fuse != 0, a.stages);
     a.nacc = need <= 113 * 1024 ? 1 : 2;
     if (const char* e = getenv("HK_TC_NACC")) a.nacc = e[0] == '1' ? 1 : 2;
     const size_t smem = a.nacc == 1 ? need : std::max(need, size_t(120 * 1024));
@@ -774,7 +787,7 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     ck(cudaStreamWaitEvent(side, c->evFork, 0), "fork wait side");
     const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
     (void)wr;
-    launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, 0, c->d_err}, 1, wcr, la);
+    launch_recip(c, 0, la);
     launch_cta(c, hk::CItemMulB{c->S.view(), c->R.view(), b_buf(c, 0), N, L, 0, c->d_err}, N - 1, wc, la);
     ck(cudaEventRecord(evP[0], la), "evP");
     // bulk: U(i) -> evU(i) -> StoreL(i-1) -> evR(i-1);  LA: [evU(i-1)] P(i+1) with
@@ -809,7 +822,7 @@ void enqueue_ldlt_steps(hk_ctx* c) {
             if (!dev_skip("coldiag"))
                 launch_cta(c, hk::CItemColUpd{c->S.view(), b_buf(c, i), N, L, i, c->d_err, 0}, 1, wc, la, pdl);
             if (!dev_skip("recip"))
-                launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i + 1, c->d_err}, 1, wcr, la, pdl);
+                launch_recip(c, i + 1, la, pdl);
             ck(cudaEventRecord(evC[i + 1], la), "evC");
             // B_{i+1}: the first entry (all the next diagonal update needs) on `la`,
             // the rest on `la2`; B buffer (i+1) % 3 was last read by StoreL(i-2)
@@ -904,6 +917,7 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         cudaDeviceProp prop{};
         ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
         c->sm_count = prop.multiProcessorCount;
+        c->smem_optin = prop.sharedMemPerBlockOptin;
         ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "cudaStreamCreate");
         int lo = 0, hi = 0;
         ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
@@ -1410,7 +1424,7 @@ int hk_profile_ldlt(hk_ctx* c, double* ms7, long long* n_trailing) {
         long long nt = 0;
         for (int i = 0; i < N; ++i) {
             timed(1, [&] {
-                launch_cta(c, hk::CItemRecip{c->S.view(), c->R.view(), N, L, i, c->d_err}, 1, ws_cta_recip_words(L));
+                launch_recip(c, i, c->st);
             });
             const int nb = N - i - 1;
             if (nb == 0) continue;
@@ -1727,7 +1741,10 @@ void dist_publish(hk_ctx* c, int col, cudaStream_t st) {
 void dist_derive(hk_ctx* c, Shard& s, int i, cudaStream_t st) {
     const int N = c->n, L = c->L;
     const MpArr p = slot3(s.panel, N, L, i);
-    launch_cta(c, hk::CItemDRecip{p, s.R.view(), L, i, s.d_err}, 1, ws_cta_recip_words(L), st);
+    if (size_t(ws_cta_recip_words(L)) * 4 <= c->smem_optin)
+        launch_cta(c, hk::CItemDRecip{p, s.R.view(), L, i, s.d_err}, 1, ws_cta_recip_words(L), st);
+    else
+        launch(c, hk::ItemDRecip{p, s.R.view(), L, i, s.d_err}, 1, ws_recip_words(L), st);
     if (N - i - 1 > 0)
         launch_cta(c, hk::CItemDMulB{p, s.R.view(), slot3(s.B, N, L, i), L, i, s.d_err}, N - i - 1, ws_cta_words(L),
                    st);

@@ -49,17 +49,16 @@ constexpr int kTcEWin = 384;    // cells of x one A block's 4 K-steps read (wind
 // Full expansion: all nb + 352 cells built once per CTA.  Windowed (large p,
 // where the full expansion would not fit): warps 1-3 build each block's
 // 384-cell window into a ring next to the A ring, paced by the same barriers.
-HK_HD int tc_stages(bool fuse) { return fuse ? kTcStagesFused : kTcStages; }
-HK_HD size_t tc_sx_off(int L, bool ewin, bool fuse) {
-    const int ns = tc_stages(fuse);
+HK_HD int tc_stages(bool fuse, int force = 0) { return force > 0 ? force : fuse ? kTcStagesFused : kTcStages; }
+HK_HD size_t tc_sx_off(int L, bool ewin, int ns) {
     const size_t e = ewin ? (size_t)ns * kTcEWin * 16 : 16 * (size_t)tc_ncell(L);
     return (size_t)ns * kTcBlk + e;
 }
-HK_HD size_t tc_stage_off(int L, bool ewin, bool fuse) {
-    return (tc_sx_off(L, ewin, fuse) + 4 * (size_t)tc_sx_words(L) + 127) / 128 * 128;
+HK_HD size_t tc_stage_off(int L, bool ewin, int ns) {
+    return (tc_sx_off(L, ewin, ns) + 4 * (size_t)tc_sx_words(L) + 127) / 128 * 128;
 }
-HK_HD size_t tc_smem_bytes(int L, bool ewin = false, bool fuse = false) {
-    return tc_stage_off(L, ewin, fuse) + (fuse ? 4 * (size_t)kTcStageWords : 0) + 64;
+HK_HD size_t tc_smem_bytes(int L, bool ewin = false, bool fuse = false, int force_stages = 0) {
+    return tc_stage_off(L, ewin, tc_stages(fuse, force_stages)) + (fuse ? 4 * (size_t)kTcStageWords : 0) + 64;
 }
 HK_HD bool tc_ewin(int L) { return tc_smem_bytes(L, false) > 200 * 1024; }
 // The fused rounding: LDLT steps (modes 0 / 2) whose rows are whole 8-limb
@@ -171,6 +170,7 @@ struct TcBulkArgs {
     int force_fb = 0;           // tests: every 7th item to the exact redo (HK_TC_FORCE_FIX)
     int* viol = nullptr;        // tests: normalisation-check failures (must stay 0)
     int sleep_ns = 0;           // back-off of the epilogue / window-builder barrier polls
+    int stages = 0;             // ring depth override (dev sweeps; 0 = default for the mode)
 };
 
 #if !defined(HK_WARP_EMU)
@@ -195,11 +195,11 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
     const bool ewin = a.ewin != 0;
     const bool fuse = a.fuse != 0;
-    const int ns = tc_stages(fuse);                        // A / window ring depth
+    const int ns = tc_stages(fuse, a.stages);              // A / window ring depth
     uint8_t* sA = tsm;                                     // ns x 16 KB A ring
     uint8_t* sE = tsm + (size_t)ns * kTcBlk;               // expanded x cells (full, or the window ring)
-    uint32_t* sX = reinterpret_cast<uint32_t*>(tsm + tc_sx_off(L, ewin, fuse)); // x bytes, 32 B zero pad
-    uint32_t* sStg = reinterpret_cast<uint32_t*>(tsm + tc_stage_off(L, ewin, fuse)); // fused: drained chunk
+    uint32_t* sX = reinterpret_cast<uint32_t*>(tsm + tc_sx_off(L, ewin, ns)); // x bytes, 32 B zero pad
+    uint32_t* sStg = reinterpret_cast<uint32_t*>(tsm + tc_stage_off(L, ewin, ns)); // fused: drained chunk
     const int pmin = -31;
     // cell p (byte position in X, p >= pmin) -> X[p .. p+15] from sX (zero outside [0, nb))
     auto cell = [&](int p) {
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             fr.prefetch(8 * (c + 2), 8);              // c limbs of chunk c + 2, while c and c + 1 stream
             for (int gg = 0; gg < 8; ++gg) {
                 const int g = 8 * c + gg;
-                if (!fr.wants(g)) continue;
+                if (!fr.wants(g) || (a.dev & 16)) continue;
                 const uint4 v0 = reinterpret_cast<const uint4*>(stg)[(2 * gg) ^ sw];
                 const uint4 v1 = reinterpret_cast<const uint4*>(stg)[(2 * gg + 1) ^ sw];
                 const uint32_t pl[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
