@@ -164,6 +164,8 @@ int hk_set_kernel_timing(hk_ctx* ctx, int on);
  * exponent prediction is certified, so this must stay 0; tests assert it. */
 int hk_fused_violations(hk_ctx* ctx, long long* out);
 int hk_kernel_times(hk_ctx* ctx, double* out6);
+/* ... and per timed step s < cap: out[2s] product ms, out[2s+1] rounding + fix-up ms; *count steps. */
+int hk_kernel_step_times(hk_ctx* ctx, double* out, int cap, int* count);
 
 /* Measured integer-MAC peak of the device: 32x32->64-bit limb MACs per second
  * of the IMAD.WIDE carry chain the MP kernels use (register-only microkernel

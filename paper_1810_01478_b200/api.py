@@ -76,6 +76,7 @@ def lib():
             "hk_set_kernel_timing": (C.c_int, [vp, C.c_int]),
             "hk_kernel_times": (C.c_int, [vp, f64p]),
             "hk_fused_violations": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
+            "hk_kernel_step_times": (C.c_int, [vp, f64p, C.c_int, C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -359,6 +360,15 @@ class Context:
         _check(lib().hk_kernel_times(self.h, t.ctypes.data_as(C.POINTER(C.c_double))), self.h)
         keys = ("products_ms", "round_ms", "steps", "comm_ms", "comm_steps", "ldlt_ms")
         return dict(zip(keys, t.tolist()))
+
+    def kernel_step_times(self):
+        """Per LDLT step (with kernel timing on): [(product ms, rounding ms), ...] of the last hk_ldlt."""
+        cap = max(self.n, 1)
+        buf = np.zeros(2 * cap)
+        cnt = C.c_int(0)
+        _check(lib().hk_kernel_step_times(self.h, buf.ctypes.data_as(C.POINTER(C.c_double)), cap, C.byref(cnt)),
+               self.h)
+        return [(buf[2 * s], buf[2 * s + 1]) for s in range(cnt.value)]
 
     def fused_violations(self) -> int:
         v = C.c_longlong()

@@ -2067,6 +2067,20 @@ int hk_set_owner_map(hk_ctx* c, int n, const int32_t* owner) {
     });
 }
 
+int hk_kernel_step_times(hk_ctx* c, double* out, int cap, int* count) {
+    return guarded(c, [&] {
+        if (!count) return fail(c, HK_ERR_INVALID, "hk_kernel_step_times: null count");
+        *count = 0;
+        if (!c->kprof) return HK_OK;
+        for (int s = 0; s < c->kev_steps && s < cap; ++s) {
+            out[2 * s] = event_ms(c->kev[size_t(3 * s)], c->kev[size_t(3 * s + 1)]);
+            out[2 * s + 1] = event_ms(c->kev[size_t(3 * s + 1)], c->kev[size_t(3 * s + 2)]);
+            *count = s + 1;
+        }
+        return HK_OK;
+    });
+}
+
 int hk_world(const hk_ctx* c, int* rank, int* world) {
     if (!c) return HK_ERR_INVALID;
     if (rank) *rank = c->rank;
