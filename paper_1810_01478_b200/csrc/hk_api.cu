@@ -228,6 +228,7 @@ struct hk_ctx {
     bool virt = false;               // all `world` ranks emulated in this one context
     void* nccl_comm = nullptr;       // ncclComm_t (one rank per process)
     void* bcast_buf = nullptr;       // device staging of the root's result broadcast
+    unsigned long long* dev_cnt = nullptr; // dev what-if counters (HK_DEV_TCB bit 64)
     std::vector<Shard> shards;
     std::vector<int> owner;          // assign_columns(n, world), or a caller's map (hk_set_owner_map)
     bool owner_custom = false;
@@ -455,6 +456,7 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     a.ewin = 1;
     if (const char* e = getenv("HK_TC_EWIN")) a.ewin = e[0] == '1' ? 1 : 0;
     if (a.fuse) a.ewin = 1;
+    if (a.fuse) a.stages = hk::tc_fused_stages(L); // 3 (2 when p is so large that 3 would not fit two CTAs)
     if (const char* e = getenv("HK_TC_STAGES")) a.stages = std::max(2, std::min(hk::kTcStages, atoi(e)));
     const size_t need = hk::tc_smem_bytes(L, a.ewin != 0, a.fuse != 0, a.stages);
     a.nacc = need <= 113 * 1024 ? 1 : 2;
@@ -464,6 +466,13 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     func_smem((const void*)hk::k_tc_prep, 0);
     static const char* dv = getenv("HK_DEV_TCB"); // dev what-if (tools only): bits of TcBulkArgs::dev
     a.dev = dv ? atoi(dv) : 0;
+    if (a.dev & 64) { // dev: issuer wait-cycle counters, printed by hk_destroy
+        if (!c->dev_cnt) {
+            ck(cudaMalloc(&c->dev_cnt, 8 * sizeof(unsigned long long)), "malloc dev counters");
+            ck(cudaMemset(c->dev_cnt, 0, 8 * sizeof(unsigned long long)), "memset dev counters");
+        }
+        a.dev_cnt = c->dev_cnt;
+    }
     const char* sl = getenv("HK_TC_SLEEP"); // barrier-poll back-off (ns) of the non-issuing warps
     a.sleep_ns = sl ? atoi(sl) : 0;
     const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
@@ -962,6 +971,15 @@ void hk_destroy(hk_ctx* c) {
     }
     if (c->d_err) cudaFree(c->d_err);
     if (c->bcast_buf) cudaFree(c->bcast_buf);
+    if (c->dev_cnt) {
+        unsigned long long h[8] = {};
+        cudaMemcpy(h, c->dev_cnt, sizeof h, cudaMemcpyDeviceToHost);
+        const double tot = h[4] ? double(h[4]) : 1.0;
+        fprintf(stderr, "k_tc_bulk issuer cycles: total %.3e over %llu CTAs; waiting empty %.1f%% full %.1f%% "
+                        "efull %.1f%% accE %.1f%%\n", double(h[4]), h[5], 100 * h[0] / tot, 100 * h[1] / tot,
+                100 * h[2] / tot, 100 * h[3] / tot);
+        cudaFree(c->dev_cnt);
+    }
     if (c->tc_P) cudaFree(c->tc_P);
     if (c->tc_fb) cudaFree(c->tc_fb);
     if (c->tc_fb_count) cudaFree(c->tc_fb_count);

@@ -63,7 +63,9 @@ HK_HD size_t tc_smem_bytes(int L, bool ewin = false, bool fuse = false, int forc
 HK_HD bool tc_ewin(int L) { return tc_smem_bytes(L, false) > 200 * 1024; }
 // The fused rounding: LDLT steps (modes 0 / 2) whose rows are whole 8-limb
 // blocks, when two CTAs still fit an SM (227 KB of shared memory per SM)
-HK_HD bool tc_fusable(int L) { return L % 8 == 0 && tc_smem_bytes(L, true, true) + 1024 <= 113 * 1024; }
+HK_HD bool tc_fits2(size_t bytes) { return bytes + 1024 <= 113 * 1024; } // two CTAs per SM
+HK_HD int tc_fused_stages(int L) { return tc_fits2(tc_smem_bytes(L, true, true, kTcStagesFused)) ? kTcStagesFused : 2; }
+HK_HD bool tc_fusable(int L) { return L % 8 == 0 && tc_fits2(tc_smem_bytes(L, true, true, 2)); }
 
 // A blocks (4 K-steps each) of output chunk c; chunk c covers product bytes from
 // t' = -31 + 256 c, i.e. scratch limbs [64 c, 64 c + 64).
@@ -171,6 +173,7 @@ struct TcBulkArgs {
     int* viol = nullptr;        // tests: normalisation-check failures (must stay 0)
     int sleep_ns = 0;           // back-off of the epilogue / window-builder barrier polls
     int stages = 0;             // ring depth override (dev sweeps; 0 = default for the mode)
+    unsigned long long* dev_cnt = nullptr; // dev (bit 64): issuer cycles waiting on empty / full / efull / accE, total
 };
 
 #if !defined(HK_WARP_EMU)
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
         const int w0 = off >> 2, sh = (off & 3) * 8;
         uint32_t W[5];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) W[q] = (w0 + q < tc_sx_words(L)) ? sX[w0 + q] : 0u;
+        for (int q = 0; q < 5; ++q) W[q] = sX[w0 + q]; // w0 + 4 < (nb + 512) / 4 for every cell p < nb + 352
         uint4 v;
         v.x = __funnelshift_r(W[0], W[1], sh);
         v.y = __funnelshift_r(W[1], W[2], sh);
@@ -259,9 +262,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             for (int c = c_lo; c < nch; ++c) Q += nblk_of(c);
             // producer cursor: block index qt -> (chunk pc, block pb)
             int qt = 0, pc = c_lo, pb = 0, pcn = nblk_of(c_lo);
+            const bool prof = (a.dev & 64) && a.dev_cnt;
+            unsigned long long w_empty = 0, w_full = 0, w_efull = 0, w_acc = 0, t_start = clock64();
             auto issue_tma = [&]() {
                 const int s = qt % ns;
+                const unsigned long long t0 = prof ? clock64() : 0;
                 if (qt >= ns) tc::mbar_wait(&empty[s], uint32_t((qt / ns) - 1) & 1u);
+                if (prof) w_empty += clock64() - t0;
                 tc::mbar_expect_tx(&full[s], kTcBlk);
                 tc::bulk_g2s(sA + (size_t)s * kTcBlk, Abase + (size_t)pb * kTcBlk, kTcBlk, &full[s]);
                 ++qt;
@@ -276,7 +283,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             for (int c = c_lo; c < nch; ++c) {
                 const int cl = c - c_lo; // local chunk index (accumulator / phase)
                 const int ab = cl % nacc;
+                const unsigned long long ta = prof ? clock64() : 0;
                 if (cl >= nacc) tc::mbar_wait(&accE[ab], uint32_t((cl - nacc) / nacc) & 1u);
+                if (prof) w_acc += clock64() - ta;
                 tc::fence_after();
                 const int tc0 = -31 + kTcN * c;
                 const int u_hi = tc0 < 0 ? nb : nb - tc0;
@@ -284,8 +293,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
                 const int nblk = nblk_of(c);
                 for (int b = 0; b < nblk; ++b, ++q) {
                     const int s = q % ns;
+                    const unsigned long long tf = prof ? clock64() : 0;
                     if (!(a.dev & 2)) tc::mbar_wait(&full[s], uint32_t(q / ns) & 1u);
+                    const unsigned long long te = prof ? clock64() : 0;
                     if (ewin && !(a.dev & 1)) tc::mbar_wait(&efull[s], uint32_t(q / ns) & 1u);
+                    if (prof) {
+                        w_full += te - tf;
+                        w_efull += clock64() - te;
+                    }
                     tc::fence_after();
 #pragma unroll
                     for (int sub = 0; sub < kTcKB; ++sub) {
@@ -302,6 +317,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
                     if (qt < Q && !(a.dev & 2)) issue_tma(); // refills the slot block q - 1 used
                 }
                 tc::commit(&accF[ab]);
+            }
+            if (prof) {
+                atomicAdd(a.dev_cnt + 0, w_empty);
+                atomicAdd(a.dev_cnt + 1, w_full);
+                atomicAdd(a.dev_cnt + 2, w_efull);
+                atomicAdd(a.dev_cnt + 3, w_acc);
+                atomicAdd(a.dev_cnt + 4, clock64() - t_start);
+                atomicAdd(a.dev_cnt + 5, 1ull);
             }
         }
         __syncwarp();

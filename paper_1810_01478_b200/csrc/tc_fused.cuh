@@ -121,8 +121,7 @@ struct FusedRow {
     int fK = 0, oc = 0;    // c window: block g + fK at group g, word offset oc in it
     int ow = 0;            // output word wg of group g sits at offset ow of its 8-word block
     int urel = 0;          // tail bits [urel, 255) decide the rounding (certificate)
-    uint32_t mneg = 0;     // ~0: r = a - b
-    bool swap = false;     // a = P, b = C
+    uint32_t mc = 0, mp = 0; // r = (C ^ mc) + (P ^ mp) + carry: one of them ~0 for a difference
     bool czero = false;
     bool decided = false, started = false;
     bool all1 = true, any1 = false;
@@ -222,9 +221,9 @@ struct FusedRow {
         urel = 302 - delta > 8 ? 302 - delta : 8; // certificate margin above the uncertainty 2^(lambda + 46)
         (void)p;
         const int coefC = czero ? 0 : sR * cm.sign, coefP = sR * sp; // |R| = coefC |c| + coefP |x y|
-        swap = coefC < 0;
-        mneg = (coefC * coefP < 0) ? 0xffffffffu : 0u;
-        cy1 = mneg & 1u;
+        mc = coefC < 0 ? 0xffffffffu : 0u; // |R| = |x y| - |c|
+        mp = coefP < 0 ? 0xffffffffu : 0u; // |R| = |c| - |x y|
+        cy1 = (mc | mp) & 1u;              // two's complement: + 1 at the stream's lowest word
         const int K0 = Qc - Qp - 1;
         fK = K0 >> 3;
         oc = K0 & 7;
@@ -288,9 +287,7 @@ struct FusedRow {
             const int w = wg + u;
             const uint32_t pw = fshr(u ? pl[u - 1] : pprev, pl[u], sig);
             const uint32_t cw = fshr(cq[u], cq[u + 1], tau);
-            const uint32_t a = swap ? pw : cw;
-            const uint32_t b = (swap ? cw : pw) ^ mneg;
-            const uint64_t s = (uint64_t)a + b + cy1;
+            const uint64_t s = (uint64_t)(cw ^ mc) + (pw ^ mp) + cy1;
             const uint32_t r = uint32_t(s);
             if (w >= -kFuseTail && w < L) cy1 = uint32_t(s >> 32);
             if (tail && w >= -kFuseTail && w < 0) {
