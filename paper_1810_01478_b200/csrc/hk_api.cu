@@ -466,13 +466,7 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     func_smem((const void*)hk::k_tc_prep, 0);
     static const char* dv = getenv("HK_DEV_TCB"); // dev what-if (tools only): bits of TcBulkArgs::dev
     a.dev = dv ? atoi(dv) : 0;
-    if (a.dev & 64) { // dev: issuer wait-cycle counters, printed by hk_destroy
-        if (!c->dev_cnt) {
-            ck(cudaMalloc(&c->dev_cnt, 8 * sizeof(unsigned long long)), "malloc dev counters");
-            ck(cudaMemset(c->dev_cnt, 0, 8 * sizeof(unsigned long long)), "memset dev counters");
-        }
-        a.dev_cnt = c->dev_cnt;
-    }
+    if (a.dev & 64) a.dev_cnt = c->dev_cnt; // dev: issuer wait-cycle counters (hk_create), printed by hk_destroy
     const char* sl = getenv("HK_TC_SLEEP"); // barrier-poll back-off (ns) of the non-issuing warps
     a.sleep_ns = sl ? atoi(sl) : 0;
     const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
@@ -940,6 +934,10 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
         ck(cudaEventCreate(&c->ev[0]), "event");
         ck(cudaEventCreate(&c->ev[1]), "event");
+        if (const char* dv = getenv("HK_DEV_TCB"); dv && (atoi(dv) & 64)) {
+            ck(cudaMalloc(&c->dev_cnt, 8 * sizeof(unsigned long long)), "malloc dev counters");
+            ck(cudaMemset(c->dev_cnt, 0, 8 * sizeof(unsigned long long)), "memset dev counters");
+        }
         return HK_OK;
     });
     if (rc != HK_OK) {
