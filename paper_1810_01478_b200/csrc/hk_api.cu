@@ -11,6 +11,7 @@
 #include "../../include/hankel_b200.h"
 #include "hk_items.cuh"
 #include "tc_bulk.cuh"
+#include "tc_pair.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -438,6 +439,13 @@ bool use_fuse(const hk_ctx* c) {
     return !e || e[0] != '0';
 }
 
+// The fused products on CTA pairs (tc_pair.cuh); HK_TC_PAIR=0 keeps one CTA per MMA
+bool use_pair(const hk_ctx* c) {
+    if (!use_fuse(c) || !hk::tcp_ok(c->L)) return false;
+    const char* e = getenv("HK_TC_PAIR");
+    return !e || e[0] != '0';
+}
+
 bool use_tc_inv(const hk_ctx* c) {
     if (!use_tc(c)) return false;
     if (getenv("HK_TC")) return true;
@@ -474,6 +482,31 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     launch_ex(hk::k_tc_prep, dim3(unsigned((nprep + 255) / 256)), dim3(256), 0, st, pdl, prep, nprep);
     ck(cudaGetLastError(), "tc prep launch");
     ++c->launches;
+    if (a.fuse && a.mode != 1 && use_pair(c)) { // CTA pairs: cluster (1, 2, 1) over row-tile pairs
+        a.stages = hk::tcp_stages(L);
+        if (const char* e = getenv("HK_TC_STAGES")) a.stages = std::max(2, std::min(hk::kTcStages, atoi(e)));
+        const size_t ps = hk::tcp_smem_bytes(L, a.stages);
+        func_smem((const void*)hk::k_tc_pair, ps);
+        const int first_row = a.jfirst;
+        const int tiles = hk::tc_ntiles(N) - first_row / hk::kTcRows;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(gx, unsigned(2 * ((tiles + 1) / 2)), 1);
+        cfg.blockDim = dim3(hk::kTcThreads);
+        cfg.dynamicSmemBytes = ps;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 1;
+        at[0].val.clusterDim.y = 2;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl ? 2 : 1;
+        ck(cudaLaunchKernelEx(&cfg, hk::k_tc_pair, a), "tc pair launch");
+        ++c->launches;
+        return;
+    }
     const int first_row = a.mode != 1 ? a.jfirst : a.i + 1;
     const dim3 grid(gx, unsigned(hk::tc_ntiles(N) - first_row / hk::kTcRows), unsigned(a.groups));
     launch_ex(hk::k_tc_bulk, grid, dim3(hk::kTcThreads), smem, st, pdl, a);

@@ -89,8 +89,9 @@ HK_HD int tc_group_first_chunk(int L, int G, int z) {
     return c;
 }
 HK_HD int tc_scratch_limbs(int L) { return L + kTcGuard; }  // limbs [L-8, 2L)
-// preformatted A operand of one step: [row tile][A block][4 K-steps x 128 rows x 32 B]
-HK_HD size_t tc_apre_bytes(int N, int L) { return (size_t)tc_ntiles(N) * tc_nblk(L) * kTcBlk; }
+// preformatted A operand of one step: [row tile][A block][4 K-steps x 128 rows x 32 B],
+// plus one all-zero tile past N (the second CTA of a pair may start there)
+HK_HD size_t tc_apre_bytes(int N, int L) { return (size_t)(tc_ntiles(N) + 1) * tc_nblk(L) * kTcBlk; }
 
 // A operand of step i in the MMA's K-major SWIZZLE_NONE layout: row k = 128 tile
 // + rr, K-step ks holds reversed bytes Yr[32 ks .. 32 ks + 31] of the row operand
@@ -122,8 +123,8 @@ struct ItemTcPrep {
         }
         reinterpret_cast<uint4*>(A)[u] = v;
     }
-    HK_HD long long count() const {
-        return (long long)(tc_ntiles(N) - (i + 1) / kTcRows) * tc_nblk(L) * kTcKB * 256;
+    HK_HD long long count() const { // tiles (i + 1) / 128 .. ntiles (the last one: the zero pad tile)
+        return (long long)(tc_ntiles(N) + 1 - (i + 1) / kTcRows) * tc_nblk(L) * kTcKB * 256;
     }
 };
 
@@ -175,6 +176,101 @@ struct TcBulkArgs {
     int stages = 0;             // ring depth override (dev sweeps; 0 = default for the mode)
     unsigned long long* dev_cnt = nullptr; // dev (bit 64): issuer cycles waiting on empty / full / efull / accE, total
 };
+
+#if !defined(HK_WARP_EMU)
+// The fused rounding (tc_fused.cuh) as the epilogue of one CTA's 128 rows:
+// the thread of row k drains its product limbs chunk by chunk into its
+// shared-memory row (the accumulator is released at once), then streams them
+// through FusedRow into S(k,j) in place.  One accumulator (TMEM columns 0-255).
+// accE_rank < 0: arrive on this CTA's accE; else on CTA accE_rank's of the cluster.
+__device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, int j, int locj, const uint32_t* sX,
+                                               uint32_t* sStg, uint32_t tmem, int c_lo, int nch, uint64_t* accF,
+                                               uint64_t* accE, int accE_rank) {
+    const int N = a.N, L = a.L;
+    const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
+    const int r = 32 * (warp & 3) + ln;
+    const int k = tile * kTcRows + r;
+    const bool row_ok = k >= j && k < N;
+    long long item = 0, ec = 0;
+    FusedRow fr;
+    fr.status = 0;
+    if (row_ok) {
+        Meta xm;
+        if (a.mode == 0) {
+            ec = tri_idx(k, j, N);
+            item = col_off(j - a.jfirst, N - a.jfirst) + (k - j);
+            xm = a.S.m[tri_idx(j, a.i, N)];
+        } else {
+            ec = a.off[locj] + (k - j);
+            item = ec - a.e0;
+            xm = a.X.m[j - a.i];
+        }
+        const uint64_t xt = (uint64_t(sX[8 + L - 1]) << 32) | sX[8 + L - 2];
+        const uint32_t* yl = a.Y.limbs(k, L);
+        const uint64_t yt = (uint64_t(yl[L - 1]) << 32) | yl[L - 2];
+        fr.setup(a.S.limbs(ec, L), a.S.m[ec], xt, xm, yt, a.Y.m[k], L);
+        if (a.force_fb && item % 7 == 3 && fr.status != 0) fr.status = 2;
+    }
+    fr.prefetch(8 * c_lo, 16); // the first two chunks' c limbs
+    uint32_t* stg = sStg + 64 * r; // 16 x 16-byte cells, XOR-swizzled by row (conflict-free)
+    const int sw = r & 15;
+    const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    uint64_t carry = 0;
+    for (int c = c_lo; c < nch; ++c) {
+        const int cl = c - c_lo;
+        const int ab = 0;
+        tc::mbar_wait_sleep(&accF[ab], uint32_t(cl) & 1u, a.sleep_ns);
+        tc::fence_after();
+        for (int c32 = 0; c32 < kTcN; c32 += 32) {
+            uint32_t v[32];
+            tc::tmem_ld32(lane_base + uint32_t(ab * kTcN + c32), v);
+            tc::tmem_ld_wait();
+            uint32_t o[8];
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                const uint64_t s = carry + (uint64_t)v[4 * h] + ((uint64_t)v[4 * h + 1] << 8) +
+                                   ((uint64_t)v[4 * h + 2] << 16) + ((uint64_t)v[4 * h + 3] << 24);
+                o[h] = uint32_t(s);
+                carry = s >> 32;
+            }
+            const int q = c32 >> 4; // 16-byte cells q, q + 1: limbs 4 q .. 4 q + 7 (8 limbs per 32 columns)
+            reinterpret_cast<uint4*>(stg)[q ^ sw] = make_uint4(o[0], o[1], o[2], o[3]);
+            reinterpret_cast<uint4*>(stg)[(q + 1) ^ sw] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (ln == 0) { // the MMAs of chunk c + 1 may now overwrite it
+            if (accE_rank < 0)
+                tc::mbar_arrive(&accE[ab]);
+            else
+                tc::mbar_arrive_remote(&accE[ab], uint32_t(accE_rank));
+        }
+        fr.prefetch(8 * (c + 2), 8);              // c limbs of chunk c + 2, while c and c + 1 stream
+        for (int gg = 0; gg < 8; ++gg) {
+            const int g = 8 * c + gg;
+            if (!fr.wants(g) || (a.dev & 16)) continue;
+            const uint4 v0 = reinterpret_cast<const uint4*>(stg)[(2 * gg) ^ sw];
+            const uint4 v1 = reinterpret_cast<const uint4*>(stg)[(2 * gg + 1) ^ sw];
+            const uint32_t pl[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            fr.group(g, pl);
+        }
+    }
+    {
+        const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        for (int g = 8 * nch; fr.wants(g); ++g) fr.group(g, zero);
+    }
+    if (row_ok) {
+        Meta mo{0, 0};
+        bool viol = false;
+        const bool ok = fr.finish(&mo, &viol);
+        if (viol && a.viol) atomicAdd(a.viol, 1);
+        if (!ok)
+            a.fb[atomicAdd(a.fb_count, 1)] = item;
+        else if (fr.status == 1)
+            a.S.m[ec] = mo;
+    }
+}
+#endif
 
 #if !defined(HK_WARP_EMU)
 // blockIdx.x: column offset (j = jfirst + x); blockIdx.y: row tile offset (tile = j / 128 + y).
@@ -347,85 +443,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             }
         }
     } else if (fuse) {
-        // fused rounding: the thread of row k drains its product limbs chunk by chunk
-        // into its shared-memory row (the accumulator is released at once), then
-        // streams them through FusedRow into S(k,j) in place (tc_fused.cuh)
-        const int r = 32 * (warp & 3) + ln;
-        const int k = tile * kTcRows + r;
-        const bool row_ok = k >= j && k < N;
-        long long item = 0, ec = 0;
-        FusedRow fr;
-        fr.status = 0;
-        if (row_ok) {
-            Meta xm;
-            if (a.mode == 0) {
-                ec = tri_idx(k, j, N);
-                item = col_off(j - a.jfirst, N - a.jfirst) + (k - j);
-                xm = a.S.m[tri_idx(j, a.i, N)];
-            } else {
-                ec = a.off[locj] + (k - j);
-                item = ec - a.e0;
-                xm = a.X.m[j - a.i];
-            }
-            const uint64_t xt = (uint64_t(sX[8 + L - 1]) << 32) | sX[8 + L - 2];
-            const uint32_t* yl = a.Y.limbs(k, L);
-            const uint64_t yt = (uint64_t(yl[L - 1]) << 32) | yl[L - 2];
-            fr.setup(a.S.limbs(ec, L), a.S.m[ec], xt, xm, yt, a.Y.m[k], L);
-            if (a.force_fb && item % 7 == 3 && fr.status != 0) fr.status = 2;
-        }
-        fr.prefetch(8 * c_lo, 16); // the first two chunks' c limbs
-        uint32_t* stg = sStg + 64 * r; // 16 x 16-byte cells, XOR-swizzled by row (conflict-free)
-        const int sw = r & 15;
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-        uint64_t carry = 0;
-        for (int c = c_lo; c < nch; ++c) {
-            const int cl = c - c_lo;
-            const int ab = cl % nacc;
-            tc::mbar_wait_sleep(&accF[ab], uint32_t(cl / nacc) & 1u, a.sleep_ns);
-            tc::fence_after();
-            for (int c32 = 0; c32 < kTcN; c32 += 32) {
-                uint32_t v[32];
-                tc::tmem_ld32(lane_base + uint32_t(ab * kTcN + c32), v);
-                tc::tmem_ld_wait();
-                uint32_t o[8];
-#pragma unroll
-                for (int h = 0; h < 8; ++h) {
-                    const uint64_t s = carry + (uint64_t)v[4 * h] + ((uint64_t)v[4 * h + 1] << 8) +
-                                       ((uint64_t)v[4 * h + 2] << 16) + ((uint64_t)v[4 * h + 3] << 24);
-                    o[h] = uint32_t(s);
-                    carry = s >> 32;
-                }
-                const int q = c32 >> 4; // 16-byte cells q, q + 1: limbs 4 q .. 4 q + 7 (8 limbs per 32 columns)
-                reinterpret_cast<uint4*>(stg)[q ^ sw] = make_uint4(o[0], o[1], o[2], o[3]);
-                reinterpret_cast<uint4*>(stg)[(q + 1) ^ sw] = make_uint4(o[4], o[5], o[6], o[7]);
-            }
-            tc::fence_before();
-            __syncwarp();
-            if (ln == 0) tc::mbar_arrive(&accE[ab]); // the MMAs of chunk c + 1 may now overwrite it
-            fr.prefetch(8 * (c + 2), 8);              // c limbs of chunk c + 2, while c and c + 1 stream
-            for (int gg = 0; gg < 8; ++gg) {
-                const int g = 8 * c + gg;
-                if (!fr.wants(g) || (a.dev & 16)) continue;
-                const uint4 v0 = reinterpret_cast<const uint4*>(stg)[(2 * gg) ^ sw];
-                const uint4 v1 = reinterpret_cast<const uint4*>(stg)[(2 * gg + 1) ^ sw];
-                const uint32_t pl[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                fr.group(g, pl);
-            }
-        }
-        {
-            const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-            for (int g = 8 * nch; fr.wants(g); ++g) fr.group(g, zero);
-        }
-        if (row_ok) {
-            Meta mo{0, 0};
-            bool viol = false;
-            const bool ok = fr.finish(&mo, &viol);
-            if (viol && a.viol) atomicAdd(a.viol, 1);
-            if (!ok)
-                a.fb[atomicAdd(a.fb_count, 1)] = item;
-            else if (fr.status == 1)
-                a.S.m[ec] = mo;
-        }
+        fused_epilogue(a, tile, j, locj, sX, sStg, tmem, c_lo, nch, accF, accE, -1);
     } else {
         const int r = 32 * (warp & 3) + ln; // this thread's row / TMEM lane
         const int k = tile * kTcRows + r;
