@@ -490,20 +490,36 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
         const int first_row = a.jfirst;
         const int tiles = hk::tc_ntiles(N) - first_row / hk::kTcRows;
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(gx, unsigned(2 * ((tiles + 1) / 2)), 1);
+        cfg.gridDim = dim3(unsigned(2 * ((tiles + 1) / 2)), gx, 1);
         cfg.blockDim = dim3(hk::kTcThreads);
         cfg.dynamicSmemBytes = ps;
         cfg.stream = st;
         cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 1;
-        at[0].val.clusterDim.y = 2;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = pdl ? 2 : 1;
-        ck(cudaLaunchKernelEx(&cfg, hk::k_tc_pair, a), "tc pair launch");
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, hk::k_tc_pair, a);
+        if (le != cudaSuccess) {
+            cudaGetLastError();
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, hk::k_tc_pair);
+            int ncl = -1;
+            cfg.numAttrs = 1;
+            const cudaError_t oe = cudaOccupancyMaxActiveClusters(&ncl, hk::k_tc_pair, &cfg);
+            throw HkError{HK_ERR_RUNTIME,
+                          std::string("tc pair launch: ") + cudaGetErrorString(le) + " (grid " +
+                              std::to_string(cfg.gridDim.x) + "x" + std::to_string(cfg.gridDim.y) + ", smem " +
+                              std::to_string(ps) + ", static " + std::to_string(fa.sharedSizeBytes) + ", regs " +
+                              std::to_string(fa.numRegs) + ", maxdyn " + std::to_string(fa.maxDynamicSharedSizeBytes) +
+                              ", reqcluster " + std::to_string(fa.requiredClusterWidth) + "x" +
+                              std::to_string(fa.requiredClusterHeight) + ", occupancy " + std::to_string(ncl) + " " +
+                              cudaGetErrorString(oe) + ")"};
+        }
         ++c->launches;
         return;
     }

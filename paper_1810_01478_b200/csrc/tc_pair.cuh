@@ -39,16 +39,16 @@ HK_HD int tcp_stages(int L) {
 HK_HD bool tcp_ok(int L) { return L % 8 == 0 && tc_fits2(tcp_smem_bytes(L, 2)); }
 
 #if !defined(HK_WARP_EMU)
-// grid (columns, 2 * pairs of row tiles), cluster (1, 2, 1); modes 0 / 2, fused
+// grid (2 * pairs of row tiles, columns), cluster (2, 1, 1) — the pair along x; modes 0 / 2, fused
 __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
     __shared__ uint64_t full[kTcStages], empty[kTcStages], efull[kTcStages], pready[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
     const uint32_t rank = tc::cluster_rank();
     const int N = a.N, L = a.L, nb = tc_nb(L);
-    const int locj = a.first_loc + int(blockIdx.x);
-    const int j = a.mode == 0 ? a.jfirst + int(blockIdx.x) : a.owned[locj];
-    const int tile0 = j / kTcRows + (int(blockIdx.y) & ~1); // the pair's first tile: both CTAs decide alike
+    const int locj = a.first_loc + int(blockIdx.y);
+    const int j = a.mode == 0 ? a.jfirst + int(blockIdx.y) : a.owned[locj];
+    const int tile0 = j / kTcRows + (int(blockIdx.x) & ~1); // the pair's first tile: both CTAs decide alike
     if (j >= N || tile0 * kTcRows >= N) return;
     const int tile = tile0 + int(rank); // rank 1's tile may lie past N: zero A rows (padded A), no items
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
