@@ -503,6 +503,20 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
         at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = pdl ? 2 : 1;
+        if (a.dev & 128) { // dev: occupancy of the pair kernel, once
+            static bool told = false;
+            if (!told) {
+                told = true;
+                int ncl = -1;
+                cudaLaunchConfig_t c2 = cfg;
+                c2.numAttrs = 1;
+                cudaOccupancyMaxActiveClusters(&ncl, hk::k_tc_pair, &c2);
+                cudaFuncAttributes fa{};
+                cudaFuncGetAttributes(&fa, hk::k_tc_pair);
+                fprintf(stderr, "k_tc_pair: %d active clusters max, smem %zu + static %zu, regs %d, stages %d\n", ncl, ps,
+                        fa.sharedSizeBytes, fa.numRegs, a.stages);
+            }
+        }
         const cudaError_t le = cudaLaunchKernelEx(&cfg, hk::k_tc_pair, a);
         if (le != cudaSuccess) {
             cudaGetLastError();
