@@ -1037,8 +1037,8 @@ void hk_destroy(hk_ctx* c) {
         cudaMemcpy(h, c->dev_cnt, sizeof h, cudaMemcpyDeviceToHost);
         const double tot = h[4] ? double(h[4]) : 1.0;
         fprintf(stderr, "k_tc_bulk issuer cycles: total %.3e over %llu CTAs; waiting empty %.1f%% full %.1f%% "
-                        "efull %.1f%% accE %.1f%%\n", double(h[4]), h[5], 100 * h[0] / tot, 100 * h[1] / tot,
-                100 * h[2] / tot, 100 * h[3] / tot);
+                        "efull %.1f%% accE %.1f%% peer %.1f%%\n", double(h[4]), h[5], 100 * h[0] / tot, 100 * h[1] / tot,
+                100 * h[2] / tot, 100 * h[3] / tot, 100 * h[6] / tot);
         cudaFree(c->dev_cnt);
     }
     if (c->tc_P) cudaFree(c->tc_P);

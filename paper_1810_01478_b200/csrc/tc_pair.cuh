@@ -98,9 +98,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
             int Q = 0;
             for (int c = 0; c < nch; ++c) Q += nblk_of(c);
             int qt = 0, pc = 0, pb = 0, pcn = nblk_of(0);
+            const bool prof = (a.dev & 64) && a.dev_cnt && rank == 0;
+            unsigned long long w_empty = 0, w_full = 0, w_efull = 0, w_acc = 0, w_peer = 0, t_start = clock64();
             auto issue_tma = [&]() {
                 const int s = qt % ns;
+                const unsigned long long t0 = prof ? clock64() : 0;
                 if (qt >= ns) tc::mbar_wait(&empty[s], uint32_t((qt / ns) - 1) & 1u);
+                if (prof) w_empty += clock64() - t0;
                 tc::mbar_expect_tx(&full[s], kTcBlk);
                 tc::bulk_g2s(sA + (size_t)s * kTcBlk, Abase + (size_t)pb * kTcBlk, kTcBlk, &full[s]);
                 ++qt;
@@ -113,7 +117,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
             while (qt < Q && qt < ns - 1) issue_tma();
             int q = 0;
             for (int c = 0; c < nch; ++c) {
+                const unsigned long long ta = prof ? clock64() : 0;
                 if (rank == 0 && c >= 1) tc::mbar_wait(&accE[0], uint32_t(c - 1) & 1u);
+                if (prof) w_acc += clock64() - ta;
                 tc::fence_after();
                 const int tc0 = -31 + kTcN * c;
                 const int u_hi = tc0 < 0 ? nb : nb - tc0;
@@ -122,10 +128,18 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
                 for (int b = 0; b < nblk; ++b, ++q) {
                     const int s = q % ns;
                     const uint32_t ph = uint32_t(q / ns) & 1u;
+                    const unsigned long long t1 = prof ? clock64() : 0;
                     tc::mbar_wait(&full[s], ph);
+                    const unsigned long long t2 = prof ? clock64() : 0;
                     tc::mbar_wait(&efull[s], ph);
                     if (rank == 0) {
+                        const unsigned long long t3 = prof ? clock64() : 0;
                         tc::mbar_wait(&pready[s], ph); // rank 1's A block and window half
+                        if (prof) {
+                            w_full += t2 - t1;
+                            w_efull += t3 - t2;
+                            w_peer += clock64() - t3;
+                        }
                         tc::fence_after();
 #pragma unroll
                         for (int sub = 0; sub < kTcKB; ++sub) {
@@ -144,6 +158,15 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
                     if (qt < Q) issue_tma();
                 }
                 if (rank == 0) tc::commit_pair(&accF[0]);
+            }
+            if (prof) {
+                atomicAdd(a.dev_cnt + 0, w_empty);
+                atomicAdd(a.dev_cnt + 1, w_full);
+                atomicAdd(a.dev_cnt + 2, w_efull);
+                atomicAdd(a.dev_cnt + 3, w_acc);
+                atomicAdd(a.dev_cnt + 4, clock64() - t_start);
+                atomicAdd(a.dev_cnt + 5, 1ull);
+                atomicAdd(a.dev_cnt + 6, w_peer);
             }
         }
         __syncwarp();

@@ -29,6 +29,7 @@ for w in $what; do
     steps) timeout 600 python tools/step_profile.py c4 > gpurun_out/${tag}_steps_c4.json 2>&1; echo "steps rc=$?";;
     pairtests) timeout 900 python -m pytest tests/test_gpu_api.py tests/test_gpu_parity.py tests/test_gpu_sharded.py -x -q -k "fused or tc or c4 or c2 or c3 or path" > gpurun_out/${tag}_gputests.log 2>&1; echo "pairtests rc=$?";;
     sweep5) tools/env_sweep.sh c4 "HK_TC_PAIR=0" "HK_TC_PAIR=1" "HK_TC_PAIR=1 HK_TC_STAGES=2" > gpurun_out/${tag}_sweep.txt 2>&1; echo "sweep rc=$?";;
+    sweep6) tools/env_sweep.sh c4 "HK_TC_PAIR=1 HK_DEV_TCB=192" "HK_TC_PAIR=0 HK_DEV_TCB=64" > gpurun_out/${tag}_sweep.txt 2>&1; echo "sweep rc=$?";;
     sweep2) tools/env_sweep.sh c4 "HK_TC_FUSE=0" "HK_TC_FUSE=1" > gpurun_out/${tag}_sweep.txt 2>&1; echo "sweep rc=$?";;
     ref) timeout 1500 python bench.py --impl reference --steps 1 --warmup 0 --ref-golden-precision > gpurun_out/${tag}_ref_c4.json 2> gpurun_out/${tag}_ref_c4.err; echo "ref rc=$?";;
   esac
