@@ -484,7 +484,7 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     ++c->launches;
     if (a.fuse && a.mode != 1 && use_pair(c)) { // CTA pairs: cluster (1, 2, 1) over row-tile pairs
         a.stages = hk::tcp_stages(L);
-        if (const char* e = getenv("HK_TC_STAGES")) a.stages = std::max(2, std::min(hk::kTcStages, atoi(e)));
+        if (const char* e = getenv("HK_TC_PAIR_STAGES")) a.stages = std::max(2, std::min(hk::kTcStagesMax, atoi(e)));
         const size_t ps = hk::tcp_smem_bytes(L, a.stages);
         func_smem((const void*)hk::k_tc_pair, ps);
         const int first_row = a.jfirst;

@@ -34,6 +34,7 @@ constexpr int kTcThreads = 256;  // warp 0: TMA + MMA issue; warps 4-7: epilogue
 constexpr int kTcKB = 4;         // MMAs (K-steps) per A block
 constexpr int kTcBlk = 4096 * kTcKB; // bytes per A block (one bulk copy)
 constexpr int kTcStages = 4;     // A ring depth (3 with the fused rounding: its 32 KB staging)
+constexpr int kTcStagesMax = 8;  // CTA pairs: one CTA per SM, a deeper ring
 constexpr int kTcStagesFused = 3;
 constexpr int kTcStageWords = 64 * kTcRows; // fused epilogue: one chunk's 64 limbs per row
 
@@ -181,11 +182,12 @@ struct TcBulkArgs {
 // The fused rounding (tc_fused.cuh) as the epilogue of one CTA's 128 rows:
 // the thread of row k drains its product limbs chunk by chunk into its
 // shared-memory row (the accumulator is released at once), then streams them
-// through FusedRow into S(k,j) in place.  One accumulator (TMEM columns 0-255).
-// accE_rank < 0: arrive on this CTA's accE; else on CTA accE_rank's of the cluster.
+// through FusedRow into S(k,j) in place.  nacc accumulators (TMEM columns
+// 256 a, chunk c in accumulator c % nacc).  accE_rank < 0: arrive on this
+// CTA's accE; else on CTA accE_rank's of the cluster.
 __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, int j, int locj, const uint32_t* sX,
                                                uint32_t* sStg, uint32_t tmem, int c_lo, int nch, uint64_t* accF,
-                                               uint64_t* accE, int accE_rank) {
+                                               uint64_t* accE, int accE_rank, int nacc = 1) {
     const int N = a.N, L = a.L;
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
     const int r = 32 * (warp & 3) + ln;
@@ -218,8 +220,8 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
     uint64_t carry = 0;
     for (int c = c_lo; c < nch; ++c) {
         const int cl = c - c_lo;
-        const int ab = 0;
-        tc::mbar_wait_sleep(&accF[ab], uint32_t(cl) & 1u, a.sleep_ns);
+        const int ab = cl % nacc;
+        tc::mbar_wait_sleep(&accF[ab], uint32_t(cl / nacc) & 1u, a.sleep_ns);
         tc::fence_after();
         for (int c32 = 0; c32 < kTcN; c32 += 32) {
             uint32_t v[32];

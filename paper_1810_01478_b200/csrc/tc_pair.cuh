@@ -30,19 +30,23 @@ constexpr int kTcEWinPair = 256; // window cells per A block and CTA (its 128 ou
 HK_HD size_t tcp_sx_off(int ns) { return (size_t)ns * kTcBlk + (size_t)ns * kTcEWinPair * 16; }
 HK_HD size_t tcp_stage_off(int L, int ns) { return (tcp_sx_off(ns) + 4 * (size_t)tc_sx_words(L) + 127) / 128 * 128; }
 HK_HD size_t tcp_smem_bytes(int L, int ns) { return tcp_stage_off(L, ns) + 4 * (size_t)kTcStageWords + 64; }
-// ring depth: 4 when two CTAs still fit an SM, else 3, else 2
+// A kernel that allocates TMEM with cta_group::2 runs one CTA per SM (the
+// driver's occupancy for it is one cluster per TPC, measured), so the CTA takes
+// all 512 TMEM columns — two accumulators: the epilogue of chunk c overlaps the
+// MMAs of chunk c + 1 — and a deep ring in up to 227 KB of shared memory
 HK_HD int tcp_stages(int L) {
-    for (int ns = 4; ns > 2; --ns)
-        if (tc_fits2(tcp_smem_bytes(L, ns))) return ns;
+    for (int ns = kTcStagesMax; ns > 2; --ns)
+        if (tcp_smem_bytes(L, ns) + 1024 <= 227 * 1024) return ns;
     return 2;
 }
-HK_HD bool tcp_ok(int L) { return L % 8 == 0 && tc_fits2(tcp_smem_bytes(L, 2)); }
+HK_HD bool tcp_ok(int L) { return L % 8 == 0 && tcp_smem_bytes(L, 2) + 1024 <= 227 * 1024; }
 
 #if !defined(HK_WARP_EMU)
 // grid (2 * pairs of row tiles, columns), cluster (2, 1, 1) — the pair along x; modes 0 / 2, fused
-__global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc_pair(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    __shared__ uint64_t full[kTcStages], empty[kTcStages], efull[kTcStages], pready[kTcStages], accF[2], accE[2];
+    __shared__ uint64_t full[kTcStagesMax], empty[kTcStagesMax], efull[kTcStagesMax], pready[kTcStagesMax], accF[2],
+        accE[2];
     __shared__ uint32_t taddr_s;
     const uint32_t rank = tc::cluster_rank();
     const int N = a.N, L = a.L, nb = tc_nb(L);
@@ -59,7 +63,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
     uint32_t* sStg = reinterpret_cast<uint32_t*>(tsm + tcp_stage_off(L, ns));
     const uint32_t* xl = a.mode == 0 ? a.S.limbs(tri_idx(j, a.i, N), L) : a.X.limbs(j - a.i, L);
     for (int w = tid; w < tc_sx_words(L); w += kTcThreads) sX[w] = (w >= 8 && w < 8 + L) ? xl[w - 8] : 0u;
-    if (warp == 0) tc::tmem_alloc_pair(&taddr_s, uint32_t(kTcN));
+    constexpr int nacc = 2;
+    if (warp == 0) tc::tmem_alloc_pair(&taddr_s, uint32_t(nacc * kTcN));
     if (tid == 0) {
         for (int s = 0; s < ns; ++s) {
             tc::mbar_init(&full[s], 1);
@@ -118,7 +123,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
             int q = 0;
             for (int c = 0; c < nch; ++c) {
                 const unsigned long long ta = prof ? clock64() : 0;
-                if (rank == 0 && c >= 1) tc::mbar_wait(&accE[0], uint32_t(c - 1) & 1u);
+                const int ab = c % nacc;
+                if (rank == 0 && c >= nacc) tc::mbar_wait(&accE[ab], uint32_t((c - nacc) / nacc) & 1u);
                 if (prof) w_acc += clock64() - ta;
                 tc::fence_after();
                 const int tc0 = -31 + kTcN * c;
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
                                 const uint64_t ad = tc::sdesc(sA + (size_t)s * kTcBlk + sub * 4096, 128, 256);
                                 const uint64_t bd =
                                     tc::sdesc(sE + (size_t)s * kTcEWinPair * 16 + 16 * (size_t)(sub * kTcK), 128, 256);
-                                tc::mma_i8_pair(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
+                                tc::mma_i8_pair(tmem + uint32_t(ab * kTcN), ad, bd, idesc, ks > 0 ? 1u : 0u);
                             }
                         }
                         tc::commit_pair(&empty[s]); // both CTAs may refill slot s
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
                     }
                     if (qt < Q) issue_tma();
                 }
-                if (rank == 0) tc::commit_pair(&accF[0]);
+                if (rank == 0) tc::commit_pair(&accF[ab]);
             }
             if (prof) {
                 atomicAdd(a.dev_cnt + 0, w_empty);
@@ -187,13 +193,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pair(TcBulkArgs a) {
             }
         }
     } else {
-        fused_epilogue(a, tile, j, locj, sX, sStg, tmem, 0, nch, accF, accE, 0);
+        fused_epilogue(a, tile, j, locj, sX, sStg, tmem, 0, nch, accF, accE, 0, nacc);
     }
     tc::fence_before();
     __syncthreads();
     tc::cluster_sync(); // no remote arrive or multicast commit may target an exited CTA
     tc::fence_after();
-    if (warp == 0) tc::tmem_dealloc_pair(tmem, uint32_t(kTcN));
+    if (warp == 0) tc::tmem_dealloc_pair(tmem, uint32_t(nacc * kTcN));
 }
 #endif
 
