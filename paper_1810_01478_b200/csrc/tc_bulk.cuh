@@ -165,7 +165,8 @@ struct TcBulkArgs {
     const long long* off = nullptr;
     long long e0 = 0;
     int first_loc = 0;
-    int dev = 0; // dev what-if knobs (results wrong; tools only): 1 no window build, 2 no TMA of A, 4 no drain, 8 no P stores
+    int dev = 0; // dev what-if knobs (results wrong; tools only): 1 no window build, 2 no TMA of A, 4 no drain, 8 no P stores,
+                 // 16 no fused processing, 64 issuer wait counters, 128 pair occupancy, 256 ignore the pivot flag
     // fused rounding (modes 0 / 2, groups == 1): S(k,j) = RNE(S(k,j) - x y_k) in the epilogue
     int fuse = 0;
     MpArr Y{};                  // y_k = B_i(k) (the row operand)
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
     __shared__ uint64_t full[kTcStages], empty[kTcStages], efull[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
-    if (a.mode != 1 && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
+    if (a.mode != 1 && !(a.dev & 256) && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
     const int N = a.N, L = a.L, nb = tc_nb(L);
     const int locj = a.first_loc + int(blockIdx.x);
     const int j = a.mode == 0 ? a.jfirst + int(blockIdx.x) : a.mode == 2 ? a.owned[locj] : a.i + 1; // first valid row
