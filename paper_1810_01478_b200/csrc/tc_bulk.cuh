@@ -211,6 +211,7 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
         const uint64_t xt = (uint64_t(sX[8 + L - 1]) << 32) | sX[8 + L - 2];
         const uint32_t* yl = a.Y.limbs(k, L);
         const uint64_t yt = (uint64_t(yl[L - 1]) << 32) | yl[L - 2];
+        fr.dev = a.dev;
         fr.setup(a.S.limbs(ec, L), a.S.m[ec], xt, xm, yt, a.Y.m[k], L);
         if (a.force_fb && item % 7 == 3 && fr.status != 0) fr.status = 2;
     }
@@ -268,7 +269,7 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
         const bool ok = fr.finish(&mo, &viol);
         if (viol && a.viol) atomicAdd(a.viol, 1);
         if (!ok)
-            a.fb[atomicAdd(a.fb_count, 1)] = item;
+            if (!(a.dev & 512)) a.fb[atomicAdd(a.fb_count, 1)] = item;
         else if (fr.status == 1)
             a.S.m[ec] = mo;
     }

@@ -128,11 +128,12 @@ struct FusedRow {
     uint32_t cy1 = 0, cy2 = 0, pprev = 0, top = 0;
     uint32_t win[16], pre[8], pend[8];
     int why = 0;           // why the exact redo (tests): 1 binade, 2 sign/binade of c - x y, 3 cancellation, 4 certificate
+    int dev = 0;           // what-if knobs (dev tools only, results wrong): 32 no stores, 1024 no loads
 
     HK_DEV int nblocks() const { return L >> 3; }
 
     HK_DEV void load8(int b, uint32_t* v) const {
-        if (czero || b < 0 || b >= nblocks()) {
+        if (czero || b < 0 || b >= nblocks() || (dev & 1024)) {
 #pragma unroll
             for (int t = 0; t < 8; ++t) v[t] = 0u;
             return;
@@ -147,6 +148,7 @@ struct FusedRow {
 #endif
     }
     HK_DEV void store8(int b, const uint32_t* v) const {
+        if (dev & 32) return;
         uint32_t* p = c + 8 * b;
 #if defined(__CUDA_ARCH__)
         asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),

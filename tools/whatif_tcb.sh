@@ -1,5 +1,5 @@
 #!/bin/bash
-# dev: what-if timings of the fused product kernel at C4 (results wrong with knobs 1/2/16; 256 keeps every step running)
-for spec in "HK_TC_PAIR=0" "HK_TC_PAIR=0 HK_DEV_TCB=256" "HK_TC_PAIR=0 HK_DEV_TCB=272" "HK_TC_PAIR=0 HK_DEV_TCB=259" "HK_TC_PAIR=0 HK_DEV_TCB=275" "HK_TC_PAIR=1 HK_DEV_TCB=272"; do
-  echo "== $spec"; env $spec timeout 600 python tools/one_run.py c4 2 2>&1 | tail -1
+# dev: what-if timings of the fused product kernel at C4 (results wrong; 256|512 keep every step running, no fix-up storm)
+for spec in "HK_DEV_TCB=768" "HK_DEV_TCB=784" "HK_DEV_TCB=800" "HK_DEV_TCB=1792" "HK_DEV_TCB=1824" "HK_DEV_TCB=771"; do
+  echo "== $spec"; env HK_TC_PAIR=0 $spec timeout 600 python tools/one_run.py c4 2 2>&1 | tail -1
 done
