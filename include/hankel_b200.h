@@ -163,6 +163,9 @@ int hk_set_kernel_timing(hk_ctx* ctx, int on);
  * failed its final normalisation check since the context was created.  The
  * exponent prediction is certified, so this must stay 0; tests assert it. */
 int hk_fused_violations(hk_ctx* ctx, long long* out);
+/* Measurement hook: items the certified roundings (tensor-core paths) left to
+ * the exact redo kernel since the context was created. */
+int hk_fix_count(hk_ctx* ctx, long long* out);
 int hk_kernel_times(hk_ctx* ctx, double* out6);
 /* ... and per timed step s < cap: out[2s] product ms, out[2s+1] rounding + fix-up ms; *count steps. */
 int hk_kernel_step_times(hk_ctx* ctx, double* out, int cap, int* count);

@@ -76,6 +76,7 @@ def lib():
             "hk_set_kernel_timing": (C.c_int, [vp, C.c_int]),
             "hk_kernel_times": (C.c_int, [vp, f64p]),
             "hk_fused_violations": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
+            "hk_fix_count": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
             "hk_kernel_step_times": (C.c_int, [vp, f64p, C.c_int, C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
@@ -369,6 +370,12 @@ class Context:
         _check(lib().hk_kernel_step_times(self.h, buf.ctypes.data_as(C.POINTER(C.c_double)), cap, C.byref(cnt)),
                self.h)
         return [(buf[2 * s], buf[2 * s + 1]) for s in range(cnt.value)]
+
+    def fix_count(self) -> int:
+        """Items left to the exact redo by the certified roundings so far (hk_fix_count)."""
+        v = C.c_longlong()
+        _check(lib().hk_fix_count(self.h, C.byref(v)), self.h)
+        return v.value
 
     def fused_violations(self) -> int:
         v = C.c_longlong()

@@ -230,6 +230,7 @@ struct hk_ctx {
     void* nccl_comm = nullptr;       // ncclComm_t (one rank per process)
     void* bcast_buf = nullptr;       // device staging of the root's result broadcast
     unsigned long long* dev_cnt = nullptr; // dev what-if counters (HK_DEV_TCB bit 64)
+    unsigned long long* fix_total = nullptr; // items the certified rounding left to the exact redo (all steps)
     std::vector<Shard> shards;
     std::vector<int> owner;          // assign_columns(n, world), or a caller's map (hk_set_owner_map)
     bool owner_custom = false;
@@ -566,7 +567,7 @@ void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset, 
     const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
     func_smem((const void*)hk::k_tc_fix<F>, 200 * 1024);
     launch_ex(hk::k_tc_fix<F>, dim3(unsigned(c->sm_count)), dim3(unsigned(32 * wpb)), size_t(wo) * 4 * wpb, st, pdl, f,
-              (const int*)count, (const long long*)c->tc_fb, wo, reset);
+              (const int*)count, (const long long*)c->tc_fb, wo, reset, c->fix_total);
     ck(cudaGetLastError(), "tc fix launch");
     ++c->launches;
 }
@@ -997,6 +998,8 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
         ck(cudaEventCreate(&c->ev[0]), "event");
         ck(cudaEventCreate(&c->ev[1]), "event");
+        ck(cudaMalloc(&c->fix_total, sizeof(unsigned long long)), "malloc fix counter");
+        ck(cudaMemset(c->fix_total, 0, sizeof(unsigned long long)), "memset fix counter");
         if (const char* dv = getenv("HK_DEV_TCB"); dv && (atoi(dv) & 64)) {
             ck(cudaMalloc(&c->dev_cnt, 8 * sizeof(unsigned long long)), "malloc dev counters");
             ck(cudaMemset(c->dev_cnt, 0, 8 * sizeof(unsigned long long)), "memset dev counters");
@@ -1032,6 +1035,7 @@ void hk_destroy(hk_ctx* c) {
     }
     if (c->d_err) cudaFree(c->d_err);
     if (c->bcast_buf) cudaFree(c->bcast_buf);
+    if (c->fix_total) cudaFree(c->fix_total);
     if (c->dev_cnt) {
         unsigned long long h[8] = {};
         cudaMemcpy(h, c->dev_cnt, sizeof h, cudaMemcpyDeviceToHost);
@@ -2099,6 +2103,16 @@ int hk_fused_violations(hk_ctx* c, long long* out) {
             ck(cudaMemcpy(&v, c->tc_fb_count + 3, sizeof(int), cudaMemcpyDeviceToHost), "D2H violations");
         }
         *out = v;
+        return HK_OK;
+    });
+}
+
+int hk_fix_count(hk_ctx* c, long long* out) {
+    return guarded(c, [&] {
+        if (!out) return fail(c, HK_ERR_INVALID, "hk_fix_count: null output");
+        unsigned long long v = 0;
+        ck(cudaMemcpy(&v, c->fix_total, sizeof v, cudaMemcpyDeviceToHost), "D2H fix count");
+        *out = (long long)v;
         return HK_OK;
     });
 }

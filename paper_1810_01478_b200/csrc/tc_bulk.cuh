@@ -789,13 +789,16 @@ __global__ void __launch_bounds__(256) k_cols(F f, int ws_words) {
 
 template <class F>
 __global__ void __launch_bounds__(256) k_tc_fix(F f, const int* fb_count, const long long* fb, int ws_words,
-                                                int* reset) {
+                                                int* reset, unsigned long long* total) {
     pdl_wait();
     extern __shared__ uint32_t fsm[];
     const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     uint32_t* ws = fsm + (size_t)wib * ws_words;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *reset = 0; // the counter the next step uses
     const int cnt = *fb_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *reset = 0;                                   // the counter the next step uses
+        if (total) atomicAdd(total, (unsigned long long)cnt); // items redone exactly (hk_fix_count)
+    }
     for (long long q = (long long)blockIdx.x * wpb + wib; q < cnt; q += (long long)gridDim.x * wpb) f(fb[q], ws);
 }
 #endif
