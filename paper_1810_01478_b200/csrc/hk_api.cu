@@ -440,11 +440,13 @@ bool use_fuse(const hk_ctx* c) {
     return !e || e[0] != '0';
 }
 
-// The fused products on CTA pairs (tc_pair.cuh); HK_TC_PAIR=0 keeps one CTA per MMA
+// The fused products on CTA pairs (tc_pair.cuh) — an experiment, off by default:
+// a cta_group::2 TMEM kernel runs one CTA per SM, and measured 2x slower at C4
+// than two single-CTA kernels per SM.  HK_TC_PAIR=1 selects it.
 bool use_pair(const hk_ctx* c) {
     if (!use_fuse(c) || !hk::tcp_ok(c->L)) return false;
     const char* e = getenv("HK_TC_PAIR");
-    return !e || e[0] != '0';
+    return e && e[0] == '1';
 }
 
 bool use_tc_inv(const hk_ctx* c) {
