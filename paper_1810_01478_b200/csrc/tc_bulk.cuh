@@ -268,10 +268,11 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
         bool viol = false;
         const bool ok = fr.finish(&mo, &viol);
         if (viol && a.viol) atomicAdd(a.viol, 1);
-        if (!ok)
+        if (!ok) {
             if (!(a.dev & 512)) a.fb[atomicAdd(a.fb_count, 1)] = item;
-        else if (fr.status == 1)
+        } else if (fr.status == 1) {
             a.S.m[ec] = mo;
+        }
     }
 }
 #endif
