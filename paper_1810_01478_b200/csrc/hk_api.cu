@@ -1003,8 +1003,8 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaMalloc(&c->fix_total, sizeof(unsigned long long)), "malloc fix counter");
         ck(cudaMemset(c->fix_total, 0, sizeof(unsigned long long)), "memset fix counter");
         if (const char* dv = getenv("HK_DEV_TCB"); dv && (atoi(dv) & 64)) {
-            ck(cudaMalloc(&c->dev_cnt, 8 * sizeof(unsigned long long)), "malloc dev counters");
-            ck(cudaMemset(c->dev_cnt, 0, 8 * sizeof(unsigned long long)), "memset dev counters");
+            ck(cudaMalloc(&c->dev_cnt, 16 * sizeof(unsigned long long)), "malloc dev counters");
+            ck(cudaMemset(c->dev_cnt, 0, 16 * sizeof(unsigned long long)), "memset dev counters");
         }
         return HK_OK;
     });
@@ -1039,12 +1039,15 @@ void hk_destroy(hk_ctx* c) {
     if (c->bcast_buf) cudaFree(c->bcast_buf);
     if (c->fix_total) cudaFree(c->fix_total);
     if (c->dev_cnt) {
-        unsigned long long h[8] = {};
+        unsigned long long h[16] = {};
         cudaMemcpy(h, c->dev_cnt, sizeof h, cudaMemcpyDeviceToHost);
         const double tot = h[4] ? double(h[4]) : 1.0;
         fprintf(stderr, "k_tc_bulk issuer cycles: total %.3e over %llu CTAs; waiting empty %.1f%% full %.1f%% "
                         "efull %.1f%% accE %.1f%% peer %.1f%%\n", double(h[4]), h[5], 100 * h[0] / tot, 100 * h[1] / tot,
                 100 * h[2] / tot, 100 * h[3] / tot, 100 * h[6] / tot);
+        const double et = h[11] ? double(h[11]) : 1.0;
+        fprintf(stderr, "fused epilogue (thread 128) cycles: total %.3e; waiting accF %.1f%% drain %.1f%% processing %.1f%%\n",
+                double(h[11]), 100 * h[8] / et, 100 * h[9] / et, 100 * h[10] / et);
         cudaFree(c->dev_cnt);
     }
     if (c->tc_P) cudaFree(c->tc_P);

@@ -220,10 +220,14 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
     const int sw = r & 15;
     const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     uint64_t carry = 0;
+    const bool prof = (a.dev & 64) && a.dev_cnt && tid == 128; // one epilogue thread's time split
+    unsigned long long e_wait = 0, e_drain = 0, e_proc = 0, e_t0 = clock64();
     for (int c = c_lo; c < nch; ++c) {
         const int cl = c - c_lo;
         const int ab = cl % nacc;
+        const unsigned long long t0 = prof ? clock64() : 0;
         tc::mbar_wait_sleep(&accF[ab], uint32_t(cl / nacc) & 1u, a.sleep_ns);
+        const unsigned long long t1 = prof ? clock64() : 0;
         tc::fence_after();
         for (int c32 = 0; c32 < kTcN; c32 += 32) {
             uint32_t v[32];
@@ -250,6 +254,7 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
                 tc::mbar_arrive_remote(&accE[ab], uint32_t(accE_rank));
         }
         fr.prefetch(8 * (c + 2), 8);              // c limbs of chunk c + 2, while c and c + 1 stream
+        const unsigned long long t2 = prof ? clock64() : 0;
         for (int gg = 0; gg < 8; ++gg) {
             const int g = 8 * c + gg;
             if (!fr.wants(g) || (a.dev & 16)) continue;
@@ -258,6 +263,18 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
             const uint32_t pl[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             fr.group(g, pl);
         }
+        if (prof) {
+            const unsigned long long t3 = clock64();
+            e_wait += t1 - t0;
+            e_drain += t2 - t1;
+            e_proc += t3 - t2;
+        }
+    }
+    if (prof) {
+        atomicAdd(a.dev_cnt + 8, e_wait);
+        atomicAdd(a.dev_cnt + 9, e_drain);
+        atomicAdd(a.dev_cnt + 10, e_proc);
+        atomicAdd(a.dev_cnt + 11, clock64() - e_t0);
     }
     {
         const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
