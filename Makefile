@@ -22,8 +22,10 @@ build/hk_api.o: $(CSRC)/hk_api.cu $(HDRS) | build
 build/host_math.o: $(CSRC)/host_math.cpp | build
 	$(CXX) -std=c++20 -O2 -fPIC -Wall -c $< -o $@
 
+# libgmp.so.10 (the image's GMP runtime, as the reference uses) for the half-integer Gamma moments
+GMP_LIB ?= /usr/lib/x86_64-linux-gnu/libgmp.so.10
 $(LIB): build/hk_api.o build/host_math.o
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl -Xlinker $(GMP_LIB)
 
 build/emu_mp: tools/emu_mp.cpp $(HDRS) $(CSRC)/warp_emu.h | build
 	$(CXX) -std=c++20 -O2 -pthread -Wall -Wno-unknown-pragmas -o $@ $<

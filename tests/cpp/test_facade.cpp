@@ -62,7 +62,14 @@ static void host_cases() {
     const auto tab = hb::build_hankel(one, 6, 4);
     CHECK(tab.exact() && tab.order() == 6 && tab.entry(2, 3) == tab.mu(5));
     CHECK(!hb::build_hankel(half, 64, 2).exact()); // 2 (253)! does not fit 64 bits
-    CHECK_THROWS_AS(hb::build_hankel(hb::WeightSpec::make(2, 3), 4, 4), std::invalid_argument); // odd 2/beta
+    {   // odd 2/beta: half-integer Gamma values, correctly rounded (test_moments.cpp:23-28 sqrt(pi) digits)
+        const auto t2 = hb::build_hankel(hb::WeightSpec::make(2, 1), 4, 4); // beta = 2: mu_k = Gamma((k+1)/2) / 2
+        CHECK(!t2.exact());
+        CHECK(std::fabs(t2.mu(0).to_double() - 0.88622692545275801365) < 1e-16); // sqrt(pi) / 2
+        CHECK(t2.mu(1).to_double() == 0.5);                                        // Gamma(1) / 2
+        CHECK(std::fabs(t2.mu(2).to_double() - 0.44311346272637900682) < 1e-16); // sqrt(pi) / 4
+        CHECK_THROWS_AS(hb::WeightSpec::make(3, 1), std::invalid_argument);     // 2/beta not an integer
+    }
     CHECK(hb::moment_bits(one, 3) == 5);                                 // mu_4 = 24
 
     // MpFloat <-> binary64

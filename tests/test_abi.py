@@ -48,8 +48,6 @@ def test_host_moments_match_reference_moments():
             s, m, e = mu.entry(j)
             assert F.MPF(s, m, e) == F.from_int(R.moment_integer(beta, j), 32 * L), (beta, L, j)
     with pytest.raises(ValueError):
-        api.build_hankel((2, 1), 4, 4)  # beta = 2: half-integer gamma path not implemented
-    with pytest.raises(ValueError):
         api.build_hankel((3, 1), 4, 4)  # 2/beta not an integer (moments.cpp:74-75)
 
 
@@ -72,3 +70,25 @@ def test_device_entry_points_fail_loudly_without_gpu():
 
     with pytest.raises(RuntimeError):
         api.Context(4)
+
+
+def test_half_integer_gamma_moments_correctly_rounded():
+    """Odd 2/beta (beta = 2, 2/3, 2/5): mu_k = (q/2) Gamma((k+1) q / 2) at half-integer
+    arguments (moments.cpp:90-99; sqrt(pi) via Machin + isqrt, Ziv-checked) must be
+    the correctly rounded p-bit values (mpmath at p + 200 bits)."""
+    import mpmath
+
+    from paper_1810_01478_b200 import api
+
+    for beta, L, n in (((2, 1), 4, 30), ((2, 1), 16, 40), ((2, 3), 8, 30), ((2, 5), 3, 20), ((2, 1), 96, 64)):
+        mu, exact = api.build_hankel(beta, n, L)
+        assert not exact
+        q, p = 2 * beta[1] // beta[0], 32 * L
+        mpmath.mp.prec = p + 200
+        for k in range(2 * n - 1):
+            v = mpmath.mpf(q) / 2 * mpmath.gamma(mpmath.mpf((k + 1) * q) / 2)
+            m, e = mpmath.frexp(v)
+            M, E = int(mpmath.nint(m * mpmath.mpf(2) ** p)), int(e)
+            if M == 1 << p:
+                M, E = M >> 1, E + 1
+            assert mu.entry(k) == (1, M, E), (beta, L, k)
