@@ -193,7 +193,14 @@ int hk_peak_i8mma(int device, double* u8_macs_per_s);
  * context on one device (broadcast = device-to-device copy): the sharded
  * kernels and maps, testable on a single GPU; rank must then be 0.
  * hk_compute returns rank 0's status and lambdas on every rank (one small
- * broadcast), so the callers' precision-search loops agree across ranks. */
+ * broadcast), so the callers' precision-search loops agree across ranks.
+ * On a sharded context hk_invert_L_partial and hk_assemble_block are
+ * collective too (every rank calls them): rows are owned in 128-row blocks
+ * (block b on rank b % world), column i of L and row i of L^{-1} are broadcast
+ * at step i (inversion.cpp:106-230, the per-row publish), and the block's
+ * terms are reduced per rank up to 128-row subtrees of the fixed pairwise tree
+ * that rank 0 finishes — results bit-identical to one GPU; rank 0 holds
+ * L^{-1} and the block (hk_get_Linv / hk_get_block). */
 int hk_nccl_unique_id(void* out128);
 int hk_create_sharded(int device, int limbs, int rank, int world, const void* nccl_id128, hk_ctx** out);
 int hk_world(const hk_ctx* ctx, int* rank, int* world);

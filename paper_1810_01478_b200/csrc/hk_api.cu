@@ -174,6 +174,7 @@ struct hk_ctx {
     std::string err;
     int bad_col = -1;
     bool factored = false, inverted = false, assembled = false;
+    bool dist_factored = false; // this rank took part in a sharded factorisation (all ranks)
     int sm_count = 148;
     size_t smem_optin = 227 * 1024;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
     long long launches = 0;
@@ -221,6 +222,12 @@ struct hk_ctx {
         long long* d_off = nullptr;
         int* d_fb = nullptr;         // uncertified-item counters of this shard, by step parity
         int setup_n = -1;            // order the maps / buffers were built for
+        // sharded L^-1 / block (row blocks b % world == rank): X (all rows arrive, only
+        // owned ones are computed here), block buffers, owned row tiles
+        DevArr X, Y, T, T2;
+        std::vector<int> otiles;
+        int* d_otiles = nullptr;
+        int rows_n = -1;
     };
     cudaGraphExec_t dist_graph = nullptr; // sharded LDLT step graph (look-ahead, NCCL captured)
     long long dist_graph_launches = 0;
@@ -457,7 +464,8 @@ bool use_tc_inv(const hk_ctx* c) {
 
 // A operand preformat + the tcgen05 product kernel (one CTA per SM: it owns all
 // 512 TMEM columns).  `rows` is the row-operand source (ItemTcPrep).
-void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaStream_t st, bool pdl = false) {
+void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaStream_t st, bool pdl = false,
+                 int gy = -1, int prep_panel = 0) {
     const int N = c->n, L = c->L;
     // Windowed x expansion (93-103 KB of shared memory for any p) and one TMEM
     // accumulator: two CTAs per SM, one CTA's prologue and epilogue overlap the
@@ -480,7 +488,8 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     if (a.dev & 64) a.dev_cnt = c->dev_cnt; // dev: issuer wait-cycle counters (hk_create), printed by hk_destroy
     const char* sl = getenv("HK_TC_SLEEP"); // barrier-poll back-off (ns) of the non-issuing warps
     a.sleep_ns = sl ? atoi(sl) : 0;
-    const hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
+    hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
+    prep.panel = prep_panel;
     const long long nprep = prep.count();
     launch_ex(hk::k_tc_prep, dim3(unsigned((nprep + 255) / 256)), dim3(256), 0, st, pdl, prep, nprep);
     ck(cudaGetLastError(), "tc prep launch");
@@ -541,7 +550,7 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
         return;
     }
     const int first_row = a.mode != 1 ? a.jfirst : a.i + 1;
-    const dim3 grid(gx, unsigned(hk::tc_ntiles(N) - first_row / hk::kTcRows), unsigned(a.groups));
+    const dim3 grid(gx, unsigned(gy >= 0 ? gy : hk::tc_ntiles(N) - first_row / hk::kTcRows), unsigned(a.groups));
     launch_ex(hk::k_tc_bulk, grid, dim3(hk::kTcThreads), smem, st, pdl, a);
     ck(cudaGetLastError(), "tc bulk launch");
     ++c->launches;
@@ -636,36 +645,60 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = fals
     if (kslot >= 0) graph_event(c->kev[size_t(3 * kslot + 2)], st);
 }
 
+// Where an L^-1 step reads and writes (one GPU: S and X; a sharded rank: the
+// panel of column i, its X, its rows and row tiles)
+struct InvTarget {
+    hk::MpArr Lsrc;             // L(:, i): S (tri_idx) or the panel (j - i)
+    int panel = 0;
+    hk::MpArr X;
+    int rw = 1, rr = 0;         // row blocks of this rank (hk::row_mine)
+    const int* otiles = nullptr; // device list of this rank's row tiles with rows > i (tc path)
+    int ntiles = -1;
+};
+
 // L^-1 step i on the tensor cores (same product kernel, mode 1).
-void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false) {
+void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false, const InvTarget* tg = nullptr) {
     const int N = c->n, L = c->L, m = c->m;
     const int b = i < m ? i : m;
     if (i + 1 >= N) return;
+    InvTarget one;
+    if (!tg) {
+        one.Lsrc = c->S.view();
+        one.X = c->X.view();
+        tg = &one;
+    }
     // narrow step: split each product's output chunks over G CTAs (carries joined in the rounding pass)
-    const int tiles = hk::tc_ntiles(N) - (i + 1) / hk::kTcRows;
+    const int tiles = tg->ntiles >= 0 ? tg->ntiles : hk::tc_ntiles(N) - (i + 1) / hk::kTcRows;
     // two CTAs per SM (windowed expansion, one accumulator): keep the split to a
     // single wave — rounding the group count up made a second, mostly empty wave
     int G = b > 0 ? 2 * c->sm_count / (b * tiles) : 1;
     G = std::min(G, std::min(int(hk::kTcMaxGroups), hk::tc_nchunks(L) / 2));
     if (G < 1) G = 1;
-    if (b > 0) {
-        hk::TcBulkArgs a{c->S.view(), c->X.view(), c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err};
+    if (b > 0 && tiles > 0) {
+        hk::TcBulkArgs a{hk::MpArr{}, tg->X, c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err};
         a.groups = G;
         a.gcarry = c->tc_gcarry;
-        tc_products(c, a, c->S.view(), unsigned(b), st, pdl);
+        a.otiles = tg->otiles;
+        tc_products(c, a, tg->Lsrc, unsigned(b), st, pdl, tg->ntiles, tg->panel);
     }
     int* cnt = c->tc_fb_count + (i & 1);
     int* nxt = c->tc_fb_count + ((i + 1) & 1);
     const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
-    hk::ItemTcRoundInv ri{c->S.view(), c->X.view(), c->tc_P, N, L, m, i, b, cnt, c->tc_fb};
+    hk::ItemTcRoundInv ri{tg->Lsrc, tg->X, c->tc_P, N, L, m, i, b, cnt, c->tc_fb};
     ri.G = G;
     ri.gcarry = c->tc_gcarry;
     ri.force_fb = force_fix();
+    ri.panel = tg->panel;
+    ri.rw = tg->rw;
+    ri.rr = tg->rr;
     launch(c, ri, items, hk::tcround_words(L), st, pdl);
-    if (b > 0)
-        launch_fix(c, hk::FixInv{c->S.view(), c->X.view(), N, L, m, i, b}, st, cnt, nxt, pdl);
-    else
+    if (b > 0) {
+        hk::FixInv fx{tg->Lsrc, tg->X, N, L, m, i, b};
+        fx.panel = tg->panel;
+        launch_fix(c, fx, st, cnt, nxt, pdl);
+    } else {
         ck(cudaMemsetAsync(nxt, 0, sizeof(int), st), "memset fb");
+    }
 }
 
 // ---- L^{-1} as a dataflow (small p, IMAD path): one CTA per entry X(j,c),
@@ -953,6 +986,13 @@ int check_pivots(hk_ctx* c) {
 }
 
 int dist_ldlt(hk_ctx* c); // multi-GPU factorisation (below)
+int dist_invert(hk_ctx* c, int m);
+int dist_block(hk_ctx* c, int k);
+// HK_DIST_INV=0: a sharded context runs L^-1 and the block on rank 0 alone (the r01 schedule)
+bool sharded_inv_off() {
+    const char* e = getenv("HK_DIST_INV");
+    return e && e[0] == '0';
+}
 int share_root_result(hk_ctx* c, int* rc, int s, double* hi, double* lo, double* te); // (below)
 
 void drop_graphs(hk_ctx* c) {
@@ -1022,7 +1062,8 @@ void hk_destroy(hk_ctx* c) {
     drop_graphs(c);
     for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg}) a->release();
     for (auto& s : c->shards) {
-        for (DevArr* a : {&s.S, &s.panel, &s.R, &s.B}) a->release();
+        for (DevArr* a : {&s.S, &s.panel, &s.R, &s.B, &s.X, &s.Y, &s.T, &s.T2}) a->release();
+        if (s.d_otiles) cudaFree(s.d_otiles);
         if (s.d_erow) cudaFree(s.d_erow);
         if (s.d_ecol) cudaFree(s.d_ecol);
         if (s.d_err) cudaFree(s.d_err);
@@ -1180,9 +1221,12 @@ int hk_get_L_column(hk_ctx* c, int col, uint32_t* limbs, int32_t* exps, int32_t*
 
 int hk_invert_L_partial(hk_ctx* c, int m) {
     return guarded(c, [&] {
-        if (!c->factored) return fail(c, HK_ERR_INVALID, "invert_L_partial: not factored");
+        const bool sharded = c->world > 1 || c->virt || c->nccl_comm;
+        if (!c->factored && !(sharded && c->dist_factored))
+            return fail(c, HK_ERR_INVALID, "invert_L_partial: not factored");
         const int N = c->n, L = c->L;
         if (m < 1 || m > N) return fail(c, HK_ERR_INVALID, "invert_L_partial: need 1 <= m <= n");
+        if (sharded && !sharded_inv_off()) return dist_invert(c, m);
         c->m = m;
         c->X.ensure((long long)N * m, L);
         const bool tc = use_tc_inv(c);
@@ -1253,6 +1297,7 @@ int hk_assemble_block(hk_ctx* c, int k) {
     return guarded(c, [&] {
         if (!c->inverted) return fail(c, HK_ERR_INVALID, "assemble_truncated_inverse: not inverted");
         if (k < 1 || k > c->m) return fail(c, HK_ERR_INVALID, "assemble_truncated_inverse: need 1 <= k <= m");
+        if ((c->world > 1 || c->virt || c->nccl_comm) && !sharded_inv_off()) return dist_block(c, k);
         const int N = c->n, L = c->L, m = c->m;
         int size = 1;
         while (size < N) size *= 2;
@@ -1322,10 +1367,13 @@ int hk_compute(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, con
     const int s = kk < 3 ? kk : 3;   // pipeline.cpp:64
     int rc = hk_load_moments(c, n, limbs, exps, signs);
     if (rc == HK_OK) rc = hk_ldlt(c);
-    // the columns are gathered on rank 0, which runs the rest of the path
+    // L^-1 and the block are sharded too (every rank takes part); rank 0 then
+    // holds the block and runs the eigensolve.  HK_DIST_INV=0: rank 0 alone
+    // from the gathered columns.
     const bool root = c->rank == 0;
-    if (rc == HK_OK && root) rc = hk_invert_L_partial(c, kk);
-    if (rc == HK_OK && root) rc = hk_assemble_block(c, kk);
+    const bool all = (c->world > 1 || c->virt || c->nccl_comm) && !sharded_inv_off();
+    if (rc == HK_OK && (root || all)) rc = hk_invert_L_partial(c, kk);
+    if (rc == HK_OK && (root || all)) rc = hk_assemble_block(c, kk);
     if (rc == HK_OK && root) rc = hk_smallest_eigs(c, s, lambda_hi, lambda_lo, trunc_err);
     // every rank returns rank 0's record (status, lambdas), so a caller's
     // auto_precision / scan loop takes the same branch on every rank
@@ -1346,8 +1394,9 @@ int hk_set_limbs(hk_ctx* c, int limbs) {
         drop_graphs(c);
         for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg}) a->release();
         for (auto& sh : c->shards) {
-            for (DevArr* a : {&sh.S, &sh.panel, &sh.R, &sh.B}) a->release();
+            for (DevArr* a : {&sh.S, &sh.panel, &sh.R, &sh.B, &sh.X, &sh.Y, &sh.T, &sh.T2}) a->release();
             sh.setup_n = -1;
+            sh.rows_n = -1;
         }
         for (void* p : {(void*)c->tc_P, (void*)c->tc_A, (void*)c->tc_fb, (void*)c->tc_gcarry})
             if (p) cudaFree(p);
@@ -1982,6 +2031,229 @@ void gather_to_root(hk_ctx* c) {
     }
 }
 
+// ---- sharded L^{-1} and H^{-1} block ------------------
+// Rows are owned in 128-row blocks, block b by rank b % world (the row tiles of
+// the tensor-core product kernel).  Step i of the reference's row elimination
+// (inversion.cpp:93-102; parallel form 106-230 with a per-row publish, 145-195):
+//   * the column owner broadcasts column i of L (its panel slot; the LDLT's
+//     pivot-column broadcast again) and the owner of row i broadcasts X(i, :)
+//     (final after step i - 1);
+//   * every rank updates its own rows j > i: X(j,c) = RNE(X(j,c) - L(j,i) X(i,c)),
+//     X(j,i) = -L(j,i) (i < m) — each entry's chain in the reference's order, so
+//     bit-identical to one GPU for any world size.
+// Every row is broadcast at its step, so after the last one each rank holds all
+// of X.  The block M(j,c) = sum_l X(l,j) X(l,c) / D_l: each rank forms the terms
+// of its rows (the others' are exact zeros) and reduces them up to 128-row
+// subtrees of the fixed pairwise tree; rank 0 takes each subtree from its owner
+// and finishes the same tree — the single-GPU sum, bit for bit.
+
+void shard_rows_setup(hk_ctx* c, Shard& s) {
+    const int N = c->n;
+    if (s.rows_n == N) return;
+    s.otiles.clear();
+    for (int t = 0; t * hk::kRowBlock < N; ++t)
+        if (t % c->world == s.rank) s.otiles.push_back(t);
+    if (s.d_otiles) cudaFree(s.d_otiles);
+    s.d_otiles = nullptr;
+    ck(cudaMalloc(&s.d_otiles, (s.otiles.size() + 1) * sizeof(int)), "malloc otiles");
+    if (!s.otiles.empty())
+        ck(cudaMemcpy(s.d_otiles, s.otiles.data(), s.otiles.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D otiles");
+    s.rows_n = N;
+}
+
+int row_owner(const hk_ctx* c, int j) { return (j / hk::kRowBlock) % c->world; }
+
+// X(i, 0 .. cnt) of the row owner -> every rank
+void dist_publish_xrow(hk_ctx* c, int i, int cnt, cudaStream_t st) {
+    if (cnt <= 0) return;
+    const int L = c->L, m = c->m, root = row_owner(c, i);
+    const long long off = (long long)i * m;
+    if (c->virt) {
+        const Shard& src = c->shards[size_t(root)];
+        for (auto& s : c->shards) {
+            if (s.rank == root) continue;
+            ck(cudaMemcpyAsync(s.X.d + off * L, src.X.d + off * L, size_t(cnt) * L * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, st), "xrow copy");
+            ck(cudaMemcpyAsync(s.X.m + off, src.X.m + off, size_t(cnt) * sizeof(Meta), cudaMemcpyDeviceToDevice, st),
+               "xrow meta copy");
+        }
+        return;
+    }
+    Shard& s = c->shards[0];
+    NcclApi* A = nccl_api();
+    ncclComm_t comm = (ncclComm_t)c->nccl_comm;
+    nk(A->GroupStart(), "group start");
+    nk(A->Broadcast(s.X.d + off * L, s.X.d + off * L, size_t(cnt) * L, ncclUint32, root, comm, st), "bcast xrow");
+    nk(A->Broadcast(s.X.m + off, s.X.m + off, size_t(cnt) * 2, ncclInt32, root, comm, st), "bcast xrow meta");
+    nk(A->GroupEnd(), "group end");
+}
+
+// column i of L -> every rank's panel slot i % 3 (the owner copies it out of its columns first)
+void dist_publish_lcol(hk_ctx* c, int i, cudaStream_t st) {
+    const int N = c->n, L = c->L;
+    for (auto& s : c->shards)
+        if (c->owner[size_t(i)] == s.rank)
+            launch(c, hk::ItemCopy{slot3(s.panel, N, L, i), s.S.view(), 0, s.off[size_t(s.loc[size_t(i)])], L}, N - i,
+                   64, st);
+    dist_publish(c, i, st);
+}
+
+void enqueue_dist_inv(hk_ctx* c, bool tc, cudaStream_t st) {
+    const int N = c->n, L = c->L, m = c->m;
+    for (auto& s : c->shards) {
+        hk::ItemInvInit ini{hk::MpArr{}, s.X.view(), N, L, m};
+        ini.zero = 1;
+        launch(c, ini, (long long)N * m, 64, st);
+    }
+    if (c->tc_fb_count) ck(cudaMemsetAsync(c->tc_fb_count, 0, 2 * sizeof(int), st), "memset fb counters");
+    for (int i = 0; i + 1 < N; ++i) {
+        dist_publish_lcol(c, i, st);
+        dist_publish_xrow(c, i, std::min(i, m), st);
+        const int b = i < m ? i : m;
+        for (auto& s : c->shards) {
+            InvTarget tg;
+            tg.Lsrc = slot3(s.panel, N, L, i);
+            tg.panel = 1;
+            tg.X = s.X.view();
+            tg.rw = c->world;
+            tg.rr = s.rank;
+            if (tc) {
+                // this rank's row tiles holding rows > i
+                size_t q = 0;
+                while (q < s.otiles.size() && (s.otiles[q] + 1) * hk::kRowBlock <= i + 1) ++q;
+                tg.otiles = s.d_otiles + q;
+                tg.ntiles = int(s.otiles.size() - q);
+                enqueue_inv_tc(c, i, st, false, &tg);
+            } else {
+                hk::ItemInvStep f{tg.Lsrc, tg.X, N, L, m, i};
+                f.panel = 1;
+                f.rw = c->world;
+                f.rr = s.rank;
+                launch(c, f, (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0), ws_op_words(L), st);
+            }
+        }
+    }
+    if (N >= 2) dist_publish_xrow(c, N - 1, std::min(N - 1, m), st); // the last row: now every rank holds all of X
+}
+
+int dist_invert(hk_ctx* c, int m) {
+    const int N = c->n, L = c->L;
+    c->m = m;
+    for (auto& s : c->shards) {
+        s.X.ensure((long long)N * m, L);
+        shard_rows_setup(c, s);
+    }
+    const bool tc = use_tc_inv(c);
+    if (tc) ensure_tc_items(c, (size_t)N * m, (size_t)N * m + N);
+    ck(cudaEventRecord(c->ev[0], c->st), "event");
+    enqueue_dist_inv(c, tc, c->st);
+    if (c->rank == 0) { // rank 0's copy of X is the result (hk_get_Linv, the block)
+        c->X.ensure((long long)N * m, L);
+        const Shard& s0 = c->shards[0];
+        ck(cudaMemcpyAsync(c->X.d, s0.X.d, size_t(N) * m * L * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st), "X");
+        ck(cudaMemcpyAsync(c->X.m, s0.X.m, size_t(N) * m * sizeof(Meta), cudaMemcpyDeviceToDevice, c->st), "X meta");
+    }
+    ck(cudaEventRecord(c->ev[1], c->st), "event");
+    ck(cudaEventSynchronize(c->ev[1]), "sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
+    c->t[2] = ms * 1e-3;
+    c->inverted = true;
+    c->assembled = false;
+    return HK_OK;
+}
+
+int dist_block(hk_ctx* c, int k) {
+    const int N = c->n, L = c->L, m = c->m;
+    int size = 1;
+    while (size < N) size *= 2;
+    const int npair = k * (k + 1) / 2;
+    const int B = std::min(hk::kRowBlock, size), nb = size / B; // subtrees of B leaves, block t on rank t % world
+    const int wo = ws_op_words(L);
+    ck(cudaEventRecord(c->ev[0], c->st), "event");
+    for (auto& s : c->shards) {
+        s.Y.ensure((long long)N * m, L);
+        s.T.ensure((long long)npair * size, L);
+        s.T2.ensure((long long)npair * std::max(size / 2, 1), L);
+        launch(c, hk::ItemBlockY{s.X.view(), s.R.view(), s.Y.view(), N, L, m}, (long long)N * m, wo);
+        hk::ItemBlockTerms tf{s.X.view(), s.Y.view(), s.T.view(), N, L, m, k, size};
+        tf.rw = c->world;
+        tf.rr = s.rank;
+        launch(c, tf, (long long)npair * size, wo);
+        DevArr* cur = &s.T;
+        DevArr* nxt = &s.T2;
+        for (int half = size / 2; half >= nb; half /= 2) {
+            launch(c, hk::ItemTreeLevel{cur->view(), nxt->view(), L, half}, (long long)npair * half, wo);
+            std::swap(cur, nxt);
+        }
+        if (cur != &s.T) std::swap(s.T, s.T2); // the subtree sums: s.T[q * nb + t]
+    }
+    // rank 0: subtree t from rank t % world, into its own T (then the remaining levels)
+    const long long cnt = (long long)npair * nb;
+    if (c->virt) {
+        Shard& s0 = c->shards[0];
+        for (int t = 0; t < nb; ++t) {
+            const Shard& o = c->shards[size_t(t % c->world)];
+            if (o.rank == 0) continue;
+            for (int q = 0; q < npair; ++q) {
+                const long long e = (long long)q * nb + t;
+                ck(cudaMemcpyAsync(s0.T.d + e * L, o.T.d + e * L, size_t(L) * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                   c->st), "subtree");
+                ck(cudaMemcpyAsync(s0.T.m + e, o.T.m + e, sizeof(Meta), cudaMemcpyDeviceToDevice, c->st), "subtree m");
+            }
+        }
+    } else if (c->world > 1) {
+        // every rank sends its subtree array; rank 0 receives them into T2 [world][npair * nb] and picks
+        Shard& s = c->shards[0];
+        if (c->rank == 0) s.T2.ensure((long long)c->world * cnt, L);
+        NcclApi* A = nccl_api();
+        ncclComm_t comm = (ncclComm_t)c->nccl_comm;
+        nk(A->GroupStart(), "group start");
+        if (c->rank == 0) {
+            for (int r = 1; r < c->world; ++r) {
+                nk(A->Recv(s.T2.d + r * cnt * L, size_t(cnt) * L, ncclUint32, r, comm, c->st), "recv subtrees");
+                nk(A->Recv(s.T2.m + r * cnt, size_t(cnt) * 2, ncclInt32, r, comm, c->st), "recv subtrees m");
+            }
+        } else {
+            nk(A->Send(s.T.d, size_t(cnt) * L, ncclUint32, 0, comm, c->st), "send subtrees");
+            nk(A->Send(s.T.m, size_t(cnt) * 2, ncclInt32, 0, comm, c->st), "send subtrees m");
+        }
+        nk(A->GroupEnd(), "group end");
+        if (c->rank == 0)
+            for (int t = 0; t < nb; ++t) {
+                const int r = t % c->world;
+                if (r == 0) continue;
+                for (int q = 0; q < npair; ++q) {
+                    const long long e = (long long)q * nb + t;
+                    ck(cudaMemcpyAsync(s.T.d + e * L, s.T2.d + (r * cnt + e) * L, size_t(L) * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToDevice, c->st), "pick");
+                    ck(cudaMemcpyAsync(s.T.m + e, s.T2.m + r * cnt + e, sizeof(Meta), cudaMemcpyDeviceToDevice, c->st),
+                       "pick m");
+                }
+            }
+    }
+    if (c->rank == 0) {
+        Shard& s0 = c->shards[0];
+        DevArr* cur = &s0.T;
+        DevArr* nxt = &s0.T2;
+        nxt->ensure((long long)npair * std::max(nb / 2, 1), L);
+        for (int half = nb / 2; half >= 1; half /= 2) {
+            launch(c, hk::ItemTreeLevel{cur->view(), nxt->view(), L, half}, (long long)npair * half, wo);
+            std::swap(cur, nxt);
+        }
+        c->M.ensure((long long)k * k, L);
+        launch(c, hk::ItemBlockOut{cur->view(), c->M.view(), L, k}, npair, 64);
+    }
+    ck(cudaEventRecord(c->ev[1], c->st), "event");
+    ck(cudaEventSynchronize(c->ev[1]), "sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
+    c->t[3] = ms * 1e-3;
+    c->k = k;
+    c->assembled = c->rank == 0;
+    return HK_OK;
+}
+
 int dist_ldlt(hk_ctx* c) {
     const int N = c->n, L = c->L;
     if ((int)c->owner.size() != N) {
@@ -2049,6 +2321,7 @@ int dist_ldlt(hk_ctx* c) {
     ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
     c->t[1] = ms * 1e-3;
     c->factored = c->rank == 0;
+    c->dist_factored = true;
     c->inverted = c->assembled = false;
     return HK_OK;
 }

@@ -27,6 +27,12 @@ struct MpArr {
 HK_HD long long col_off(int j, int N) { return (long long)j * N - (long long)j * (j - 1) / 2; }
 HK_HD long long tri_idx(int k, int j, int N) { return col_off(j, N) + (k - j); }
 
+// Sharded L^{-1} (multi-GPU): rows are owned in 128-row blocks, block b by rank
+// b % rw; the pivot column i of L arrives as a panel (rows i..N-1 at [j - i]).
+constexpr int kRowBlock = 128;
+HK_HD bool row_mine(int j, int rw, int rr) { return rw <= 1 || (j / kRowBlock) % rw == rr; }
+HK_HD long long lcol_idx(int j, int i, int N, int panel) { return panel ? (long long)(j - i) : tri_idx(j, i, N); }
+
 // w -> (j, k), 0 <= j <= k < n, column-major lower triangle of order n.
 HK_DEV void tri_decode(long long w, int n, int& j, int& k) {
     const double b = 2.0 * n + 1.0;
@@ -193,10 +199,11 @@ struct ItemStoreL {
 struct ItemInvInit {
     MpArr S, X;
     int N, L, m;
+    int zero = 0; // sharded: all zero (column c of X is set at step c before any use)
     HK_DEV void operator()(long long w, uint32_t*) const {
         const int r = int(w / m), c = int(w % m);
         const long long dst = (long long)r * m + c;
-        if (c < r) {
+        if (c < r && !zero) {
             const long long e = tri_idx(r, c, N);
             copy_entry(X.limbs(dst, L), X.m + dst, S.limbs(e, L), S.m + e, L);
         } else {
@@ -212,12 +219,14 @@ struct ItemInvInit {
 struct ItemInvStep {
     MpArr S, X;
     int N, L, m, i;
+    int panel = 0, rw = 1, rr = 0; // sharded: L(:, i) from the panel S, this rank's rows only
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         const int b = i < m ? i : m;
         const long long nfma = (long long)(N - i - 1) * b;
         if (w < nfma) {
             const int j = i + 1 + int(w / b), c = int(w % b);
-            const long long el = tri_idx(j, i, N);
+            if (!row_mine(j, rw, rr)) return;
+            const long long el = lcol_idx(j, i, N, panel);
             const long long xc = (long long)j * m + c, xi = (long long)i * m + c;
             uint32_t* o = X.limbs(xc, L);
             const Meta r = warp_fms(o, X.m[xc], S.limbs(el, L), S.m[el], X.limbs(xi, L), X.m[xi], o, L,
@@ -226,7 +235,8 @@ struct ItemInvStep {
             wsync();
         } else {
             const int j = i + 1 + int(w - nfma);
-            const long long el = tri_idx(j, i, N);
+            if (!row_mine(j, rw, rr)) return;
+            const long long el = lcol_idx(j, i, N, panel);
             const long long xd = (long long)j * m + i;
             copy_entry(X.limbs(xd, L), X.m + xd, S.limbs(el, L), S.m + el, L);
             if (lane() == 0) X.m[xd].sign = -X.m[xd].sign;
@@ -272,12 +282,13 @@ HK_DEV void pair_decode(int q, int k, int& j, int& c) {
 struct ItemBlockTerms {
     MpArr X, Y, T;
     int N, L, m, k, size;
+    int rw = 1, rr = 0; // sharded: this rank's rows only (the others' terms are exact zeros)
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         const int q = int(w / size), l = int(w % size);
         int j, c;
         pair_decode(q, k, j, c);
         uint32_t* o = T.limbs(w, L);
-        if (l >= c && l < N) {
+        if (l >= c && l < N && row_mine(l, rw, rr)) {
             const long long yi = (long long)l * m + c;
             if (l == j) {
                 copy_entry(o, T.m + w, Y.limbs(yi, L), Y.m + yi, L);

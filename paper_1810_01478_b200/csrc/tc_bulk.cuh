@@ -99,9 +99,10 @@ HK_HD size_t tc_apre_bytes(int N, int L) { return (size_t)(tc_ntiles(N) + 1) * t
 // (LDLT: y_k = B_i(k); L^-1: L(k, i) = S(k, i)), zero for k <= i, k >= N or past
 // nb.  Tiles from tile0 = (i + 1) / 128 on.  16 B per thread, coalesced writes.
 struct ItemTcPrep {
-    MpArr R;   // LDLT: B_i (row k at k);  L^-1: S (row k at tri_idx(k, i))
+    MpArr R;   // LDLT: B_i (row k at k);  L^-1: S (row k at tri_idx(k, i)), or the panel (row k at k - i)
     uint8_t* A;
     int N, L, i, mode;
+    int panel = 0;
     HK_DEV void operator()(long long u) const {
         const int nb = tc_nb(L);
         const long long per_tile = (long long)tc_nblk(L) * kTcKB * 256;
@@ -115,7 +116,7 @@ struct ItemTcPrep {
         const int u0 = ks * kTcK + 16 * h;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (k > i && k < N && u0 < nb) {
-            const uint32_t* row = mode != 1 ? R.limbs(k, L) : R.limbs(tri_idx(k, i, N), L);
+            const uint32_t* row = mode != 1 ? R.limbs(k, L) : R.limbs(lcol_idx(k, i, N, panel), L);
             const uint4 g = *reinterpret_cast<const uint4*>(row + (L - 4 - u0 / 4));
             v.x = __byte_perm(g.w, 0u, 0x0123);
             v.y = __byte_perm(g.z, 0u, 0x0123);
@@ -176,6 +177,7 @@ struct TcBulkArgs {
     int* viol = nullptr;        // tests: normalisation-check failures (must stay 0)
     int sleep_ns = 0;           // back-off of the epilogue / window-builder barrier polls
     int stages = 0;             // ring depth override (dev sweeps; 0 = default for the mode)
+    const int* otiles = nullptr; // mode 1, sharded L^-1: this rank's row tiles (blockIdx.y -> otiles[y])
     unsigned long long* dev_cnt = nullptr; // dev (bit 64): issuer cycles waiting on empty / full / efull / accE, total
 };
 
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
     const int N = a.N, L = a.L, nb = tc_nb(L);
     const int locj = a.first_loc + int(blockIdx.x);
     const int j = a.mode == 0 ? a.jfirst + int(blockIdx.x) : a.mode == 2 ? a.owned[locj] : a.i + 1; // first valid row
-    const int tile = j / kTcRows + int(blockIdx.y);
+    const int tile = a.otiles ? a.otiles[blockIdx.y] : j / kTcRows + int(blockIdx.y);
     if (j >= N || tile * kTcRows >= N) return;
     const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
     const bool ewin = a.ewin != 0;
@@ -653,11 +655,13 @@ struct ItemTcRoundInv {
     int force_fb = 0; // tests: every 7th certified item is sent to the exact fix-up anyway (HK_TC_FORCE_FIX)
     int G = 1;                       // chunk groups of the product kernel
     const uint64_t* gcarry = nullptr; // their carries, added here
+    int panel = 0, rw = 1, rr = 0;   // sharded: L(:, i) from the panel S, this rank's rows only
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         const long long nfma = (long long)(N - i - 1) * b;
         if (w >= nfma) {
             const int j = i + 1 + int(w - nfma);
-            const long long el = tri_idx(j, i, N);
+            if (!row_mine(j, rw, rr)) return;
+            const long long el = lcol_idx(j, i, N, panel);
             const long long xd = (long long)j * m + i;
             copy_entry(X.limbs(xd, L), X.m + xd, S.limbs(el, L), S.m + el, L);
             if (lane() == 0) X.m[xd].sign = -X.m[xd].sign;
@@ -665,7 +669,8 @@ struct ItemTcRoundInv {
             return;
         }
         const int j = i + 1 + int(w / b), c = int(w % b);
-        const long long xc = (long long)j * m + c, xi = (long long)i * m + c, el = tri_idx(j, i, N);
+        if (!row_mine(j, rw, rr)) return;
+        const long long xc = (long long)j * m + c, xi = (long long)i * m + c, el = lcol_idx(j, i, N, panel);
         const Meta cm = X.m[xc], xm = S.m[el], ym = X.m[xi];
         const int sp = -(xm.sign * ym.sign);
         if (sp == 0) return;
@@ -765,9 +770,10 @@ struct FixLdlt {
 struct FixInv {
     MpArr S, X;
     int N, L, m, i, b;
+    int panel = 0;
     HK_DEV void operator()(long long w, uint32_t* ws) const {
         const int j = i + 1 + int(w / b), c = int(w % b);
-        const long long xc = (long long)j * m + c, xi = (long long)i * m + c, el = tri_idx(j, i, N);
+        const long long xc = (long long)j * m + c, xi = (long long)i * m + c, el = lcol_idx(j, i, N, panel);
         uint32_t* o = X.limbs(xc, L);
         const Meta r = warp_fms(o, X.m[xc], S.limbs(el, L), S.m[el], X.limbs(xi, L), X.m[xi], o, L, opws_carve(ws, L));
         if (lane() == 0) X.m[xc] = r;

@@ -130,3 +130,23 @@ def test_virtual_sharded_any_owner_map(api, single, world, kind, monkeypatch):
                 ctx.set_owner_map(owner)
                 r1, D1, X1, M1 = results(ctx, mu, k)
             assert D1 == D0 and X1 == X0 and M1 == M0, (beta, n, world, kind, tc)
+
+
+@pytest.mark.parametrize("beta,n,L,k,tc", [((1, 2), 400, 8, 8, "0"), ((1, 1), 300, 32, 12, "1"),
+                                           ((1, 3), 280, 24, 16, "0")])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("dist_inv", ["1", "0"])
+def test_virtual_sharded_inverse_and_block_rows(api, beta, n, L, k, tc, world, dist_inv, monkeypatch):
+    """L^-1 and the H^-1 block sharded by 128-row blocks (K5/K6: column and row
+    broadcasts per step, per-rank subtrees of the pairwise tree finished on rank
+    0) — with several row blocks per rank — give the single-GPU bits; so does
+    the rank-0 schedule (HK_DIST_INV=0)."""
+    monkeypatch.setenv("HK_TC", tc)
+    monkeypatch.setenv("HK_DIST_INV", dist_inv)
+    mu, _ = api.build_hankel(beta, n, L)
+    with api.Context(L) as one:
+        r0, D0, X0, M0 = results(one, mu, k)
+    with api.Context(L, world=world, virtual=True) as ctx:
+        r1, D1, X1, M1 = results(ctx, mu, k)
+    assert D1 == D0 and X1 == X0 and M1 == M0, (beta, n, world, tc, dist_inv)
+    assert r1.lambda_hi == r0.lambda_hi and r1.lambda_lo == r0.lambda_lo
