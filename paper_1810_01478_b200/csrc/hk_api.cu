@@ -671,7 +671,7 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false, const I
     const int tiles = tg->ntiles >= 0 ? tg->ntiles : hk::tc_ntiles(N) - (i + 1) / hk::kTcRows;
     // two CTAs per SM (windowed expansion, one accumulator): keep the split to a
     // single wave — rounding the group count up made a second, mostly empty wave
-    int G = b > 0 ? 2 * c->sm_count / (b * tiles) : 1;
+    int G = b > 0 && tiles > 0 ? 2 * c->sm_count / (b * tiles) : 1;
     G = std::min(G, std::min(int(hk::kTcMaxGroups), hk::tc_nchunks(L) / 2));
     if (G < 1) G = 1;
     if (b > 0 && tiles > 0) {
