@@ -132,8 +132,8 @@ def test_virtual_sharded_any_owner_map(api, single, world, kind, monkeypatch):
             assert D1 == D0 and X1 == X0 and M1 == M0, (beta, n, world, kind, tc)
 
 
-@pytest.mark.parametrize("beta,n,L,k,tc", [((1, 2), 400, 8, 8, "0"), ((1, 1), 300, 32, 12, "1"),
-                                           ((1, 3), 280, 24, 16, "0")])
+@pytest.mark.parametrize("beta,n,L,k,tc", [((1, 1), 300, 224, 8, "0"), ((1, 1), 300, 224, 12, "1"),
+                                           ((1, 1), 290, 256, 16, "0")])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("dist_inv", ["1", "0"])
 def test_virtual_sharded_inverse_and_block_rows(api, beta, n, L, k, tc, world, dist_inv, monkeypatch):
