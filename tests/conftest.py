@@ -11,6 +11,9 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
+    # torch first: its NCCL (libnccl.so.2) is then the one the library's dlopen
+    # resolves to; the other order binds torch to an older NCCL and fails its import
+    import torch  # noqa: F401
 
 
 def _ensure_built(target):
