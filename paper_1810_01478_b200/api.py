@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhankel_b200.so")
+LIB_PATH = os.environ.get("HK_LIB_PATH") or os.path.join(_HERE, "libhankel_b200.so")  # override: dev A/B builds
 
 HK_OK, HK_ERR_RUNTIME, HK_ERR_PRECISION, HK_ERR_INVALID = 0, 1, 2, 3
 OP_FMS, OP_MUL, OP_ADD, OP_RECIP = 0, 1, 2, 3
