@@ -47,19 +47,12 @@ HK_HD int tc_ntiles(int N) { return (N + kTcRows - 1) / kTcRows; }
 HK_HD int tc_nchunks(int L) { return (tc_nb(L) + 32 + kTcN - 1) / kTcN; }
 constexpr int kTcMaxGroups = 8; // chunk groups per product (L^-1)
 constexpr int kTcEWin = 384;    // cells of x one A block's 4 K-steps read (windowed expansion)
-// Windowed expansion as a circular cell buffer: consecutive blocks of a chunk
-// read windows 128 cells apart, so each block builds only its 128 new cells
-// (the whole 384 at a chunk's first block).  Ring of 384 ns cells (room for ns
-// live windows across chunk starts) + a 384-cell mirror of its head, so every
-// window is contiguous for the MMA descriptor.
-HK_HD int tc_win_ring(int ns) { return kTcEWin * ns; }
-HK_HD int tc_win_cells(int ns) { return kTcEWin * (ns + 1); }
 // Full expansion: all nb + 352 cells built once per CTA.  Windowed (large p,
 // where the full expansion would not fit): warps 1-3 build each block's
 // 384-cell window into a ring next to the A ring, paced by the same barriers.
 HK_HD int tc_stages(bool fuse, int force = 0) { return force > 0 ? force : fuse ? kTcStagesFused : kTcStages; }
 HK_HD size_t tc_sx_off(int L, bool ewin, int ns) {
-    const size_t e = ewin ? (size_t)tc_win_cells(ns) * 16 : 16 * (size_t)tc_ncell(L);
+    const size_t e = ewin ? (size_t)ns * kTcEWin * 16 : 16 * (size_t)tc_ncell(L);
     return (size_t)ns * kTcBlk + e;
 }
 HK_HD size_t tc_stage_off(int L, bool ewin, int ns) {
@@ -407,8 +400,6 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             pdl_wait(); // the A operand comes from the preceding k_tc_prep
             while (qt < Q && qt < ns - 1 && !(a.dev & 2)) issue_tma();
             int q = 0;
-            int wpos = 0; // ring position of the current chunk's first window
-            const int wring = tc_win_ring(ns);
             for (int c = c_lo; c < nch; ++c) {
                 const int cl = c - c_lo; // local chunk index (accumulator / phase)
                 const int ab = cl % nacc;
@@ -437,8 +428,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
                         if (ks < ksteps) {
                             const uint64_t ad = tc::sdesc(sA + (size_t)s * kTcBlk + sub * 4096, 128, 256);
                             const uint64_t bd =
-                                ewin ? tc::sdesc(sE + 16 * (size_t)((wpos + kTcKB * kTcK * b) % wring + sub * kTcK),
-                                                 128, 256)
+                                ewin ? tc::sdesc(sE + (size_t)s * kTcEWin * 16 + 16 * (size_t)(sub * kTcK), 128, 256)
                                      : tc::sdesc(sE + 16 * (size_t)(tc0 + ks * kTcK - pmin), 128, 256);
                             tc::mma_i8(tmem + uint32_t(ab * kTcN), ad, bd, idesc, ks > 0 ? 1u : 0u);
                         }
@@ -447,7 +437,6 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
                     if (qt < Q && !(a.dev & 2)) issue_tma(); // refills the slot block q - 1 used
                 }
                 tc::commit(&accF[ab]);
-                wpos = (wpos + kTcKB * kTcK * nblk + (kTcEWin - kTcKB * kTcK)) % wring;
             }
             if (prof) {
                 atomicAdd(a.dev_cnt + 0, w_empty);
@@ -463,27 +452,18 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
         if (ewin && !(a.dev & 1)) { // warps 1-3: the x window of every block, in issue order
             const int bt = tid - 32;
             int q = 0;
-            int wpos = 0;
-            const int wring = tc_win_ring(ns);
-            constexpr int step = kTcKB * kTcK; // 128 cells between consecutive windows
             for (int c = c_lo; c < nch; ++c) {
                 const int tc0 = -31 + kTcN * c, nblk = nblk_of(c);
                 for (int b = 0; b < nblk; ++b, ++q) {
                     const int s = q % ns;
                     if (q >= ns) tc::mbar_wait_sleep(&empty[s], uint32_t((q / ns) - 1) & 1u, a.sleep_ns);
-                    const int p0 = tc0 + b * step;
-                    const int w0 = (wpos + b * step) % wring;
-                    for (int cc = (b == 0 ? 0 : kTcEWin - step) + bt; cc < kTcEWin; cc += 96) {
-                        const uint4 v = cell(p0 + cc);
-                        const int r = (w0 + cc) % wring;
-                        *reinterpret_cast<uint4*>(sE + 16 * (size_t)r) = v;
-                        if (r < kTcEWin) *reinterpret_cast<uint4*>(sE + 16 * (size_t)(wring + r)) = v; // the mirror
-                    }
+                    uint8_t* dst = sE + (size_t)s * kTcEWin * 16;
+                    const int p0 = tc0 + b * kTcKB * kTcK;
+                    for (int cc = bt; cc < kTcEWin; cc += 96) *reinterpret_cast<uint4*>(dst + 16 * cc) = cell(p0 + cc);
                     tc::fence_async_smem();
                     __syncwarp();
                     if (ln == 0) tc::mbar_arrive(&efull[s]);
                 }
-                wpos = (wpos + step * nblk + (kTcEWin - step)) % wring;
             }
         }
     } else if (fuse) {
