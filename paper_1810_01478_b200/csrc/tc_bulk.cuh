@@ -199,6 +199,10 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
     long long item = 0, ec = 0;
     FusedRow fr;
     fr.status = 0;
+    fr.wlane = ln;
+    fr.wbase = reinterpret_cast<uint32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(
+                                                                         a.S.limbs(tri_idx(tile * kTcRows, j, N), L)),
+                                                      0));
     if (row_ok) {
         Meta xm;
         if (a.mode == 0) {

@@ -128,7 +128,10 @@ struct FusedRow {
     uint32_t cy1 = 0, cy2 = 0, pprev = 0, top = 0;
     uint32_t win[16], pre[8], pend[8];
     int why = 0;           // why the exact redo (tests): 1 binade, 2 sign/binade of c - x y, 3 cancellation, 4 certificate
-    int dev = 0;           // what-if knobs (dev tools only, results wrong): 32 no stores, 1024 no loads
+    int dev = 0;           // what-if knobs (dev tools only, results wrong): 32 no stores, 1024 no loads,
+                           // 2048 loads / stores to coalesced dummy addresses (wbase + 8 lane)
+    uint32_t* wbase = nullptr;
+    int wlane = 0;
 
     HK_DEV int nblocks() const { return L >> 3; }
 
@@ -138,7 +141,7 @@ struct FusedRow {
             for (int t = 0; t < 8; ++t) v[t] = 0u;
             return;
         }
-        const uint32_t* p = c + 8 * b;
+        const uint32_t* p = (dev & 2048) ? wbase + 8 * wlane + 256 * (b & 3) : c + 8 * b;
 #if defined(__CUDA_ARCH__)
         asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -149,7 +152,7 @@ struct FusedRow {
     }
     HK_DEV void store8(int b, const uint32_t* v) const {
         if (dev & 32) return;
-        uint32_t* p = c + 8 * b;
+        uint32_t* p = (dev & 2048) ? wbase + 8 * wlane + 256 * (b & 3) : c + 8 * b;
 #if defined(__CUDA_ARCH__)
         asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
                      "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
