@@ -126,7 +126,7 @@ struct FusedRow {
     bool decided = false, started = false;
     bool all1 = true, any1 = false;
     uint32_t cy1 = 0, cy2 = 0, pprev = 0, top = 0;
-    uint32_t win[16], pre[8], pre2[8], pend[8]; // c window, blocks bg+2 and bg+3 in flight, output tail
+    uint32_t win[16], pre[8], pend[8];
     int why = 0;           // why the exact redo (tests): 1 binade, 2 sign/binade of c - x y, 3 cancellation, 4 certificate
     int dev = 0;           // what-if knobs (dev tools only, results wrong): 32 no stores, 1024 no loads,
                            // 2048 loads / stores to coalesced dummy addresses (wbase + 8 lane)
@@ -266,17 +266,13 @@ struct FusedRow {
             load8(bg, win);
             load8(bg + 1, win + 8);
             load8(bg + 2, pre);
-            load8(bg + 3, pre2);
         } else {
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 win[t] = win[t + 8];
                 win[t + 8] = pre[t];
-                pre[t] = pre2[t];
             }
-            // two groups ahead, before this group's stores (they may overlap that
-            // block: safe for Q_c >= -17, the prediction requires >= -8)
-            load8(bg + 3, pre2);
+            load8(bg + 2, pre); // before this group's stores (they may overlap that block)
         }
         // c limbs a_g + u, u = 0..8 (a_g = 8 bg + oc): select network on oc
         uint32_t cq[9];
