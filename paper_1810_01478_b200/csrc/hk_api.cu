@@ -447,6 +447,12 @@ bool use_fuse(const hk_ctx* c) {
     return !e || e[0] != '0';
 }
 
+// which fused stream: HK_TC_FUSE_WARP=1 the warp-cooperative one (tc_fused.cuh warp_row_*)
+int fuse_mode() {
+    const char* e = getenv("HK_TC_FUSE_WARP");
+    return e && e[0] == '1' ? 2 : 1;
+}
+
 // The fused products on CTA pairs (tc_pair.cuh) — an experiment, off by default:
 // a cta_group::2 TMEM kernel runs one CTA per SM, and measured 2x slower at C4
 // than two single-CTA kernels per SM.  HK_TC_PAIR=1 selects it.
@@ -625,7 +631,7 @@ void enqueue_bulk(hk_ctx* c, int i, int jfirst, cudaStream_t st, bool pdl = fals
     hk::TcBulkArgs ta{c->S.view(), hk::MpArr{}, c->tc_A, c->tc_P, N, L, i, jfirst, 0, 0, 0, c->d_err};
     const bool fuse = use_fuse(c);
     if (fuse) {
-        ta.fuse = 1;
+        ta.fuse = fuse_mode();
         ta.Y = b_buf(c, i);
         ta.fb_count = cnt;
         ta.fb = c->tc_fb;
@@ -1829,7 +1835,7 @@ bool dist_bulk(hk_ctx* c, Shard& s, int i, bool tc, cudaStream_t st, int kslot =
     a.first_loc = int(q);
     const bool fuse = use_fuse(c);
     if (fuse) {
-        a.fuse = 1;
+        a.fuse = fuse_mode();
         a.Y = B;
         a.fb_count = cnt;
         a.fb = c->tc_fb;

@@ -169,7 +169,7 @@ struct TcBulkArgs {
     int dev = 0; // dev what-if knobs (results wrong; tools only): 1 no window build, 2 no TMA of A, 4 no drain, 8 no P stores,
                  // 16 no fused processing, 64 issuer wait counters, 128 pair occupancy, 256 ignore the pivot flag
     // fused rounding (modes 0 / 2, groups == 1): S(k,j) = RNE(S(k,j) - x y_k) in the epilogue
-    int fuse = 0;
+    int fuse = 0;               // 1: thread-per-row stream, 2: warp-cooperative stream
     MpArr Y{};                  // y_k = B_i(k) (the row operand)
     int* fb_count = nullptr;    // items left to the exact redo
     long long* fb = nullptr;
@@ -290,6 +290,121 @@ __device__ __forceinline__ void fused_epilogue(const TcBulkArgs& a, int tile, in
         Meta mo{0, 0};
         bool viol = false;
         const bool ok = fr.finish(&mo, &viol);
+        if (viol && a.viol) atomicAdd(a.viol, 1);
+        if (!ok) {
+            if (!(a.dev & 512)) a.fb[atomicAdd(a.fb_count, 1)] = item;
+        } else if (fr.status == 1) {
+            a.S.m[ec] = mo;
+        }
+    }
+}
+#endif
+
+#if !defined(HK_WARP_EMU)
+// The fused rounding with the warp-cooperative stream (tc_fused.cuh
+// warp_row_*): drain as fused_epilogue, then each epilogue warp streams its 32
+// rows one at a time with coalesced c accesses (the next row's loads issued
+// while the current one is computed).
+__device__ __forceinline__ void fused_epilogue_warp(const TcBulkArgs& a, int tile, int j, int locj,
+                                                    const uint32_t* sX, uint32_t* sStg, uint32_t tmem, int c_lo,
+                                                    int nch, uint64_t* accF, uint64_t* accE, int accE_rank,
+                                                    int nacc = 1) {
+    const int N = a.N, L = a.L;
+    const int tid = threadIdx.x, warp = tid >> 5, ln = tid & 31;
+    const int r = 32 * (warp & 3) + ln, rbase = 32 * (warp & 3);
+    const int k = tile * kTcRows + r;
+    const bool row_ok = k >= j && k < N;
+    // row r (this warp's rows rbase + 0..31) -> entry of S
+    auto entry_of = [&](int rr) -> long long {
+        const int kk = tile * kTcRows + rbase + rr;
+        return a.mode == 0 ? tri_idx(kk, j, N) : a.off[locj] + (kk - j);
+    };
+    long long item = 0, ec = 0;
+    FusedRow fr;
+    fr.status = 0;
+    if (row_ok) {
+        ec = entry_of(ln);
+        item = a.mode == 0 ? col_off(j - a.jfirst, N - a.jfirst) + (k - j) : ec - a.e0;
+        const Meta xm = a.mode == 0 ? a.S.m[tri_idx(j, a.i, N)] : a.X.m[j - a.i];
+        const uint64_t xt = (uint64_t(sX[8 + L - 1]) << 32) | sX[8 + L - 2];
+        const uint32_t* yl = a.Y.limbs(k, L);
+        const uint64_t yt = (uint64_t(yl[L - 1]) << 32) | yl[L - 2];
+        fr.setup(a.S.limbs(ec, L), a.S.m[ec], xt, xm, yt, a.Y.m[k], L);
+        if (a.force_fb && item % 7 == 3 && fr.status != 0) fr.status = 2;
+    }
+    WarpRowState own = warp_row_init(fr);
+    fr.prefetch(8 * c_lo, 16); // the first two chunks' c limbs into L2
+    uint32_t* stg = sStg + 64 * r;
+    const int sw = r & 15;
+    const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    uint64_t carry = 0;
+    auto row_ptr = [&](int rr) { return a.S.limbs(entry_of(rr), L); };
+    // one chunk of all 32 rows; staged: product limbs from the staging rows (else zeros)
+    auto stream = [&](int c, bool staged) {
+        bool any = false;
+        WarpRowState bn = warp_row_bcast(own, 0);
+        uint32_t qn0, qn1;
+        warp_row_load(bn, row_ptr(0), L, c, qn0, qn1);
+        for (int rr = 0; rr < 32; ++rr) {
+            WarpRowState b = bn;
+            const uint32_t q0 = qn0, q1 = qn1;
+            if (rr + 1 < 32) {
+                bn = warp_row_bcast(own, rr + 1);
+                warp_row_load(bn, row_ptr(rr + 1), L, c, qn0, qn1);
+            }
+            if (b.status() != 1 || 64 * c - 1 - int(b.prm & 0xffffu) >= L) continue;
+            any = true;
+            uint32_t p0 = 0u, p1 = 0u;
+            if (staged) { // limbs 2 ln, 2 ln + 1 of staging row rbase + rr (16-byte cells, XOR-swizzled)
+                const uint32_t* srow = sStg + 64 * (rbase + rr);
+                const uint2 v = reinterpret_cast<const uint2*>(srow)[2 * ((ln >> 1) ^ ((rbase + rr) & 15)) + (ln & 1)];
+                p0 = v.x;
+                p1 = v.y;
+            }
+            warp_row_chunk(b, row_ptr(rr), L, c, p0, p1, q0, q1);
+            if (ln == rr) own = b;
+        }
+        return any;
+    };
+    for (int c = c_lo; c < nch; ++c) {
+        const int cl = c - c_lo;
+        const int ab = cl % nacc;
+        tc::mbar_wait_sleep(&accF[ab], uint32_t(cl / nacc) & 1u, a.sleep_ns);
+        tc::fence_after();
+        for (int c32 = 0; c32 < kTcN; c32 += 32) {
+            uint32_t v[32];
+            tc::tmem_ld32(lane_base + uint32_t(ab * kTcN + c32), v);
+            tc::tmem_ld_wait();
+            uint32_t o[8];
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                const uint64_t s = carry + (uint64_t)v[4 * h] + ((uint64_t)v[4 * h + 1] << 8) +
+                                   ((uint64_t)v[4 * h + 2] << 16) + ((uint64_t)v[4 * h + 3] << 24);
+                o[h] = uint32_t(s);
+                carry = s >> 32;
+            }
+            const int q = c32 >> 4;
+            reinterpret_cast<uint4*>(stg)[q ^ sw] = make_uint4(o[0], o[1], o[2], o[3]);
+            reinterpret_cast<uint4*>(stg)[(q + 1) ^ sw] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+        tc::fence_before();
+        __syncwarp(); // the warp reads its rows' staged limbs next
+        if (ln == 0) {
+            if (accE_rank < 0)
+                tc::mbar_arrive(&accE[ab]);
+            else
+                tc::mbar_arrive_remote(&accE[ab], uint32_t(accE_rank));
+        }
+        fr.prefetch(8 * (c + 2), 8);
+        if (!(a.dev & 16)) stream(c, true);
+        __syncwarp(); // staging rows rewritten by the next drain
+    }
+    for (int c = nch; !(a.dev & 16) && stream(c, false); ++c) {
+    }
+    if (row_ok) {
+        Meta mo{0, 0};
+        bool viol = false;
+        const bool ok = warp_row_finish(own, fr, a.S.limbs(ec, L), L, &mo, &viol);
         if (viol && a.viol) atomicAdd(a.viol, 1);
         if (!ok) {
             if (!(a.dev & 512)) a.fb[atomicAdd(a.fb_count, 1)] = item;
@@ -471,7 +586,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
             }
         }
     } else if (fuse) {
-        fused_epilogue(a, tile, j, locj, sX, sStg, tmem, c_lo, nch, accF, accE, -1);
+        if (a.fuse == 2)
+            fused_epilogue_warp(a, tile, j, locj, sX, sStg, tmem, c_lo, nch, accF, accE, -1);
+        else
+            fused_epilogue(a, tile, j, locj, sX, sStg, tmem, c_lo, nch, accF, accE, -1);
     } else {
         const int r = 32 * (warp & 3) + ln; // this thread's row / TMEM lane
         const int k = tile * kTcRows + r;

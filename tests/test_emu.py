@@ -94,8 +94,8 @@ def test_emulated_cta_ops_match_model(emu_bin, L):
             assert from_line(r, L) == F.recip(d, p)
 
 
-def _fused_run(emu_bin, cases, L):
-    lines = [f"fused {L} {len(cases)}"] + [to_line(v, L) for t in cases for v in t]
+def _fused_run(emu_bin, cases, L, op="fused"):
+    lines = [f"{op} {L} {len(cases)}"] + [to_line(v, L) for t in cases for v in t]
     return run(emu_bin, lines)
 
 
@@ -112,8 +112,9 @@ def _ldlt_like_cases(L, rng, count):
     return out
 
 
+@pytest.mark.parametrize("op", ["fused", "fusedw"])
 @pytest.mark.parametrize("L", [8, 16, 24, 40])
-def test_fused_epilogue_rounding_matches_model(emu_bin, L):
+def test_fused_epilogue_rounding_matches_model(emu_bin, L, op):
     """The rounding fused into the tensor-core epilogue (csrc/tc_fused.cuh),
     fed the short product exactly as k_tc_bulk forms it: every item it
     certifies equals RNE(c - x y) (oracle/mpfloat.py); the rest go to the exact
@@ -121,7 +122,7 @@ def test_fused_epilogue_rounding_matches_model(emu_bin, L):
     rng = random.Random(7000 + L)
     p = 32 * L
     for cases, max_fb in ((fms_cases(L, rng, 300), 0.6), (_ldlt_like_cases(L, rng, 300), 0.08)):
-        out = _fused_run(emu_bin, cases, L)
+        out = _fused_run(emu_bin, cases, L, op)
         assert len(out) == len(cases)
         fb = 0
         for (c, x, y), r in zip(cases, out):
@@ -133,7 +134,8 @@ def test_fused_epilogue_rounding_matches_model(emu_bin, L):
         assert fb <= max_fb * len(cases), fb
 
 
-def test_fused_epilogue_edges(emu_bin):
+@pytest.mark.parametrize("op", ["fused", "fusedw"])
+def test_fused_epilogue_edges(emu_bin, op):
     """Binade edges, round-up overflow, ties, tiny / huge products, zero c."""
     L = 16
     p = 32 * L
@@ -158,7 +160,7 @@ def test_fused_epilogue_edges(emu_bin):
         else:  # c = x y exactly representable -> R = 0 or tiny
             c = F.MPF(pr.s, pr.m ^ rng.getrandbits(rng.randint(1, 40)), pr.e)
         cases.append((c, x, y))
-    out = _fused_run(emu_bin, cases, L)
+    out = _fused_run(emu_bin, cases, L, op)
     for (c, x, y), r in zip(cases, out):
         assert r != "viol", (c, x, y)
         if not r.startswith("fb"):

@@ -152,6 +152,99 @@ int main() {
                     std::printf("\n");
                 }
             }
+        } else if (cmd == "fusedw") { // the warp-cooperative stream (csrc/tc_fused.cuh warp_row_*), 32 items per warp
+            int L;
+            long long cnt;
+            std::cin >> L >> cnt;
+            HostArr Cc(cnt, L), X(cnt, L), Y(cnt, L);
+            for (long long e = 0; e < cnt; ++e) {
+                read_opd(Cc, e, L);
+                read_opd(X, e, L);
+                read_opd(Y, e, L);
+            }
+            const int nb = 4 * L, T0 = 4 * L - 32, nl = L + 8, nch = (nl + 63) / 64;
+            std::vector<std::string> out(static_cast<size_t>(cnt));
+            for (long long w0 = 0; w0 < cnt; w0 += 32) {
+                // per row: the short product as k_tc_bulk forms it, in chunks of 64 limbs
+                std::vector<std::vector<uint32_t>> P(32, std::vector<uint32_t>(size_t(64) * (nch + 64), 0u));
+                std::vector<std::vector<uint32_t>> crow(32, std::vector<uint32_t>(size_t(L), 0u));
+                for (int r = 0; r < 32 && w0 + r < cnt; ++r) {
+                    const long long e = w0 + r;
+                    const uint8_t* xb = reinterpret_cast<const uint8_t*>(&X.d[size_t(e) * L]);
+                    const uint8_t* yb = reinterpret_cast<const uint8_t*>(&Y.d[size_t(e) * L]);
+                    uint64_t carry = 0;
+                    for (int q = 0; q < 4 * nl; q += 4) {
+                        uint64_t sum = carry;
+                        for (int h = 0; h < 4; ++h) {
+                            const int t = T0 + q + h;
+                            uint64_t col = 0;
+                            for (int u = 0; u < nb; ++u)
+                                if (t - u >= 0 && t - u < nb) col += uint64_t(yb[u]) * xb[t - u];
+                            sum += col << (8 * h);
+                        }
+                        P[size_t(r)][size_t(q / 4)] = uint32_t(sum);
+                        carry = sum >> 32;
+                    }
+                    std::copy(Cc.d.begin() + e * L, Cc.d.begin() + (e + 1) * L, crow[size_t(r)].begin());
+                }
+                std::vector<int> stat(32, 0), why(32, 0);
+                std::vector<Meta> mo(32, Meta{0, 0});
+                std::vector<char> okv(32, 1), viol(32, 0); // not vector<bool>: lanes write concurrently
+                hk_emu::run_warp([&] {
+                    const int ln = hk::lane();
+                    const long long e = w0 + ln;
+                    FusedRow fr;
+                    if (e < cnt) {
+                        auto top64 = [&](const uint32_t* l) { return (uint64_t(l[L - 1]) << 32) | (L > 1 ? l[L - 2] : 0u); };
+                        fr.setup(crow[size_t(ln)].data(), Cc.m[size_t(e)], top64(&X.d[size_t(e) * L]), X.m[size_t(e)],
+                                 top64(&Y.d[size_t(e) * L]), Y.m[size_t(e)], L);
+                    }
+                    WarpRowState own = warp_row_init(fr);
+                    for (int c = 0;; ++c) {
+                        bool any = false;
+                        for (int rr = 0; rr < 32; ++rr) {
+                            WarpRowState b = warp_row_bcast(own, rr);
+                            if (b.status() != 1) continue;
+                            const int Qp = int(b.prm & 0xffffu);
+                            if (64 * c - 1 - Qp >= L) continue; // row complete
+                            any = true;
+                            const uint32_t p0 = P[size_t(rr)][size_t(64 * c + 2 * ln)];
+                            const uint32_t p1 = P[size_t(rr)][size_t(64 * c + 2 * ln + 1)];
+                            uint32_t q0, q1;
+                            warp_row_load(b, crow[size_t(rr)].data(), L, c, q0, q1);
+                            warp_row_chunk(b, crow[size_t(rr)].data(), L, c, p0, p1, q0, q1);
+                            if (ln == rr) own = b;
+                        }
+                        if (!any && c >= nch) break;
+                    }
+                    Meta m{0, 0};
+                    bool v = false;
+                    const bool ok = warp_row_finish(own, fr, crow[size_t(ln)].data(), L, &m, &v);
+                    stat[size_t(ln)] = fr.status;
+                    okv[size_t(ln)] = ok;
+                    viol[size_t(ln)] = v;
+                    mo[size_t(ln)] = m;
+                    why[size_t(ln)] = fr.why;
+                });
+                for (int r = 0; r < 32 && w0 + r < cnt; ++r) {
+                    const long long e = w0 + r;
+                    char buf[64];
+                    if (viol[size_t(r)]) out[size_t(e)] = "viol";
+                    else if (!okv[size_t(r)]) {
+                        std::snprintf(buf, sizeof buf, "fb %d", why[size_t(r)]);
+                        out[size_t(e)] = buf;
+                    } else {
+                        const Meta m = stat[size_t(r)] == 0 ? Cc.m[size_t(e)] : mo[size_t(r)];
+                        std::string ln = std::to_string(m.sign) + " " + std::to_string(m.exp);
+                        for (int i = 0; i < L; ++i) {
+                            std::snprintf(buf, sizeof buf, " %x", crow[size_t(r)][size_t(i)]);
+                            ln += buf;
+                        }
+                        out[size_t(e)] = ln;
+                    }
+                }
+            }
+            for (auto& o : out) std::printf("%s\n", o.c_str());
         } else if (cmd == "path") {
             int L, N, m;
             std::cin >> L >> N >> m;
