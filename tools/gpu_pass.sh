@@ -18,8 +18,8 @@ for w in $what; do
         -o gpurun_out/${tag}_prof_tcb_c4 -f python tools/one_run.py c4 1 > gpurun_out/${tag}_ncu_tcb_c4.log 2>&1; echo "ncu tcb rc=$?"
       ;;
     launches)
-      timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 5000 \
-        --log-file gpurun_out/${tag}_launches_c4.csv python tools/one_run.py c4 1 > gpurun_out/${tag}_launches_c4.log 2>&1; echo "launches rc=$?";;
+      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 6000 \
+        --log-file gpurun_out/${tag}_launches_c4.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/${tag}_launches_c4.log 2>&1; echo "launches rc=$?";;
     sweep) tools/env_sweep.sh c4 "HK_TC_FUSE=0" "HK_TC_FUSE=1" "HK_TC_FUSE=1 HK_TC_SLEEP=64" "HK_TC_FUSE=1 HK_TC_SLEEP=256" "HK_TC_FUSE=0 HK_TC_SLEEP=128" > gpurun_out/${tag}_sweep.txt 2>&1; echo "sweep rc=$?";;
     c5pin) timeout 1500 python tools/c5_pin.py > gpurun_out/${tag}_c5pin.json 2> gpurun_out/${tag}_c5pin.err; echo "c5pin rc=$?";;
     fusedtests) timeout 900 python -m pytest tests/test_gpu_api.py tests/test_gpu_parity.py -x -q -k "fused or tc or c4 or c2" > gpurun_out/${tag}_gputests.log 2>&1; echo "fusedtests rc=$?";;
