@@ -465,7 +465,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the NCCL column-sharded path even on 1 GPU")
-    ap.add_argument("--ref-budget-s", type=float, default=480.0,
+    ap.add_argument("--ref-budget-s", type=float, default=300.0,
                     help="reference arm: wall-clock budget for its full runs (at least one runs)")
     ap.add_argument("--ref-golden-precision", action="store_true",
                     help="reference arm: also time one full run at the golden runs' K (K_ref)")
