@@ -349,6 +349,26 @@ def bench_ours(args, cfg):
         e2e_ms += e0.elapsed_time(e1)
     e2e_ms = max_over_ranks(e2e_ms / args.steps, world, local)
     h2d = mu.limbs.nbytes + mu.exps.nbytes + mu.signs.nbytes
+
+    # ---- the same call with the moments generated on the device (hk_compute_generated,
+    # SURVEY 8 f4): scalars in, lambdas out — reported beside e2e, not instead of it
+    gen_ms = None
+    if (2 * cfg["beta"][1] // cfg["beta"][0]) % 2 == 0:
+        ctx.compute_generated(cfg["beta"], n, k)
+        barrier()
+        gen_ms, gsteps = 0.0, min(args.steps, 2)
+        for _ in range(gsteps):
+            flush.zero_()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            rec_g = ctx.compute_generated(cfg["beta"], n, k)
+            e1.record(ext)
+            e1.synchronize()
+            gen_ms += e0.elapsed_time(e1)
+        gen_ms = max_over_ranks(gen_ms / gsteps, world, local)
+        gen_moments_ms = ctx.timings()[5] * 1e3
+        assert rank != 0 or rec_g.lambda_hi == rec.lambda_hi, "device-generated moments changed lambda"
     d2h = kk * kk * (4 * L + 8) + 9 * 8 if rank == 0 else 11 * 8
 
     # ---- roofline of the dominant kernel: its graph-resident event times over the timed steps
@@ -393,7 +413,10 @@ def bench_ours(args, cfg):
             "share_of_ldlt": ms_k / ldlt_ms if ldlt_ms > 0 else None,
             "kernel_ms_per_step": kt,
         })
-        if kt.get("round_ms", 0.0) > 0:
+        if 0 < kt.get("round_ms", 0.0) < 0.02 * ms_k:  # fused rounding: only the rare exact redos are left
+            roofline["exact_redo"] = {"kernel": "k_tc_fix (items the fused certificate left to the exact FMA)",
+                                      "ms": kt["round_ms"]}
+        elif kt.get("round_ms", 0.0) > 0:
             round_bytes = sum((n - i - 2) * (n - i - 1) // 2 for i in range(n)) * (12 * L + 32)
             gbps = round_bytes / (kt["round_ms"] * 1e-3) / 1e9
             roofline["rounding_pass"] = {"kernel": "k_cols<ItemTcRound> + k_tc_fix", "ms": kt["round_ms"],
@@ -416,6 +439,11 @@ def bench_ours(args, cfg):
         "e2e": {"value": fmas(n) / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "includes": "host moment generation (hk_moments into pinned memory) + hk_compute"},
+        "e2e_device_moments": None if gen_ms is None else {
+            "value": fmas(n) / (gen_ms * 1e-3), "unit": UNIT, "ms_per_step": gen_ms, "h2d_bytes_per_step": 0,
+            "moments_ms": gen_moments_ms,
+            "includes": "hk_compute_generated: moments built on the device (k_moments_fact), path, D2H of the "
+                        "block + lambdas; same lambdas as e2e"},
         "roofline": roofline,
         "gpu_launches": launches,
         "clocks": sampler.summary(),

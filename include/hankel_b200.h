@@ -66,11 +66,22 @@ int hk_limbs(const hk_ctx* ctx);
 int hk_set_limbs(hk_ctx* ctx, int limbs);
 
 /* Host-side exact moments mu_0..mu_{count-1} of w(x)=exp(-x^beta) as p-bit
- * floats (moments.cpp:80-111: gamma_exact + moment, the factorial path; the
- * half-integer sqrt(pi) path is not implemented -> HK_ERR_INVALID).
+ * floats (moments.cpp:80-111: gamma_exact + moment; the factorial branch and —
+ * for odd 2/beta — the half-integer sqrt(pi) branch, correctly rounded).
  * *exact = 1 iff every moment was representable without rounding. No GPU. */
 int hk_moments(unsigned beta_num, unsigned beta_den, int count, int limbs, uint32_t* out_limbs,
                int32_t* out_exps, int32_t* out_signs, int* exact);
+
+/* The 2n-1 moments of order n generated ON THE DEVICE into the context's moment
+ * array (csrc/moments_dev.cuh): one CTA keeps the running factorial as an exact
+ * integer in shared memory and writes RNE_p of every moment — gamma_exact's
+ * factorial branch + moment + the integer -> working-precision conversion of
+ * build_hankel (moments.cpp:83-89, 102-111, 113-129).  Bit-identical to
+ * hk_moments + hk_load_moments; no host bigint, no H2D.  Even 2/beta only (odd
+ * 2/beta needs sqrt(pi): host path, HK_ERR_INVALID here).  *exact as hk_moments.
+ * hk_get_moments copies the context's 2n-1 moments back (tests). */
+int hk_generate_moments(hk_ctx* ctx, unsigned beta_num, unsigned beta_den, int n, int* exact);
+int hk_get_moments(hk_ctx* ctx, uint32_t* limbs, int32_t* exps, int32_t* signs);
 
 /* Upload the 2n-1 moments (H2D).  Replaces MomentTable / build_hankel
  * (moments.hpp:36-58) as the input of the factorisation. */
@@ -120,9 +131,14 @@ int hk_block_eigenvalues(int k, int limbs, const uint32_t* limbs_in, const int32
 int hk_compute(hk_ctx* ctx, int n, const uint32_t* limbs, const int32_t* exps, const int32_t* signs, int k,
                double* lambda_hi, double* lambda_lo, double* trunc_err, int* s_out);
 
+/* The same path with the moments generated on the device (hk_generate_moments):
+ * the inputs are the scalars of ComputeOptions (pipeline.hpp:13-26) only. */
+int hk_compute_generated(hk_ctx* ctx, unsigned beta_num, unsigned beta_den, int n, int k, double* lambda_hi,
+                         double* lambda_lo, double* trunc_err, int* s_out, int* moments_exact);
+
 /* Stage times of the last calls, RunRecord taxonomy (pipeline.hpp:38-45), in
  * seconds: [0] wall (hk_compute), [1] ldlt, [2] invL, [3] invH, [4] eigen,
- * [5] h2d, [6] d2h.  Device stages are CUDA-event times on the ctx stream. */
+ * [5] h2d (or the on-device moment generation), [6] d2h.  Device stages are CUDA-event times on the ctx stream. */
 int hk_timings(const hk_ctx* ctx, double* out7);
 
 /* Kernel launches issued by the last hk_ldlt / invert / assemble calls. */

@@ -596,6 +596,9 @@ struct ComputeOptions { // pipeline.hpp:16-23; workers = GPUs (see compute)
     // ncclUniqueId; without an id, workers > 1 emulates the split on one GPU
     int rank = 0;
     const void* nccl_id128 = nullptr;
+    // moments generated on the device (hk_generate_moments; even 2/beta) instead
+    // of host build_hankel + upload — the same bits either way
+    bool device_moments = true;
 };
 
 struct RunRecord { // pipeline.hpp:28-48 (+ p_bits and the ~32-digit lambda_lo)
@@ -664,14 +667,24 @@ inline RunRecord compute(const ComputeOptions& opts) {
     if (opts.workers < 1) throw std::invalid_argument("compute: need workers >= 1");
     if (opts.k < 1) throw std::invalid_argument("compute: need k >= 1");
     const int p = precision_bits(opts.beta, opts.n, opts.bits);
-    const MomentTable table = build_hankel(opts.beta, opts.n, p / 32);
-    if (!table.exact() && opts.beta.doubled_inverse() % 2 == 0)
-        throw precision_error("compute: moments not exact at p bits");
-    Device& dev = detail::compute_device(opts, p / 32);
+    const bool even_q = opts.beta.doubled_inverse() % 2 == 0;
     double hi[3], lo[3], te[3];
     int s = 0;
-    const MpVector& mu = table.moments();
-    dev.check(hk_compute(dev.handle(), opts.n, mu.pl(), mu.pe(), mu.ps(), opts.k, hi, lo, te, &s));
+    Device* devp = nullptr;
+    if (opts.device_moments && even_q) { // moments.cpp:113-133 on the device
+        devp = &detail::compute_device(opts, p / 32);
+        int exact = 0;
+        devp->check(hk_compute_generated(devp->handle(), opts.beta.beta_num, opts.beta.beta_den, opts.n, opts.k, hi,
+                                         lo, te, &s, &exact));
+        if (!exact) throw precision_error("compute: moments not exact at p bits");
+    } else {
+        const MomentTable table = build_hankel(opts.beta, opts.n, p / 32);
+        if (!table.exact() && even_q) throw precision_error("compute: moments not exact at p bits");
+        devp = &detail::compute_device(opts, p / 32);
+        const MpVector& mu = table.moments();
+        devp->check(hk_compute(devp->handle(), opts.n, mu.pl(), mu.pe(), mu.ps(), opts.k, hi, lo, te, &s));
+    }
+    Device& dev = *devp;
     const std::vector<double> t = dev.timings();
     RunRecord r;
     r.n = opts.n;

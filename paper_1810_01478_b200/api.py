@@ -51,6 +51,10 @@ def lib():
             "hk_limbs": (C.c_int, [vp]),
             "hk_moments": (C.c_int, [C.c_uint, C.c_uint, C.c_int, C.c_int, u32p, i32p, i32p, C.POINTER(C.c_int)]),
             "hk_load_moments": (C.c_int, [vp, C.c_int, u32p, i32p, i32p]),
+            "hk_generate_moments": (C.c_int, [vp, C.c_uint, C.c_uint, C.c_int, C.POINTER(C.c_int)]),
+            "hk_get_moments": (C.c_int, [vp, u32p, i32p, i32p]),
+            "hk_compute_generated": (C.c_int, [vp, C.c_uint, C.c_uint, C.c_int, C.c_int, f64p, f64p, f64p,
+                                               C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "hk_ldlt": (C.c_int, [vp]),
             "hk_get_D": (C.c_int, [vp, u32p, i32p, i32p]),
             "hk_get_L_column": (C.c_int, [vp, C.c_int, u32p, i32p, i32p]),
@@ -317,6 +321,37 @@ class Context:
             self.bad_column = lib().hk_bad_column(self.h)
         _check(rc, self.h)
         self.n, self.m, self.k = n, min(k, n), min(k, n)
+        t = self.timings()
+        ns = s.value
+        return RunRecord(n=n, k=min(k, n), lambda_hi=hi[:ns].tolist(), lambda_lo=lo[:ns].tolist(),
+                         trunc_err=te[:ns].tolist(), wall_s=t[0], ldlt_s=t[1], invL_s=t[2], invH_s=t[3],
+                         eigen_s=t[4], h2d_s=t[5], d2h_s=t[6])
+
+    def generate_moments(self, beta: tuple[int, int], n: int) -> bool:
+        """build_hankel on the device (even 2/beta): the context's moments of order n; returns `exact`."""
+        exact = C.c_int(0)
+        _check(lib().hk_generate_moments(self.h, beta[0], beta[1], n, C.byref(exact)), self.h)
+        self.n = n
+        return bool(exact.value)
+
+    def moments(self) -> MPArray:
+        """The context's 2n-1 moments copied back (tests)."""
+        out = MPArray.empty(2 * self.n - 1, self.L)
+        _check(lib().hk_get_moments(self.h, *out.ptrs()), self.h)
+        return out
+
+    def compute_generated(self, beta: tuple[int, int], n: int, k: int) -> RunRecord:
+        """hankel::compute (pipeline.cpp:26-72) with the moments generated on the device."""
+        hi, lo, te = (np.zeros(3) for _ in range(3))
+        s, ex = C.c_int(0), C.c_int(0)
+        f64 = C.POINTER(C.c_double)
+        rc = lib().hk_compute_generated(self.h, beta[0], beta[1], n, k, hi.ctypes.data_as(f64),
+                                        lo.ctypes.data_as(f64), te.ctypes.data_as(f64), C.byref(s), C.byref(ex))
+        if rc == HK_ERR_PRECISION:
+            self.bad_column = lib().hk_bad_column(self.h)
+        _check(rc, self.h)
+        self.n, self.m, self.k = n, min(k, n), min(k, n)
+        self.moments_exact = bool(ex.value)
         t = self.timings()
         ns = s.value
         return RunRecord(n=n, k=min(k, n), lambda_hi=hi[:ns].tolist(), lambda_lo=lo[:ns].tolist(),

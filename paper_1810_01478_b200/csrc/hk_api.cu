@@ -10,6 +10,7 @@
 // item sees it and returns, and the host maps it to HK_ERR_PRECISION.
 #include "../../include/hankel_b200.h"
 #include "hk_items.cuh"
+#include "moments_dev.cuh"
 #include "tc_bulk.cuh"
 #include "tc_pair.cuh"
 
@@ -19,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -1043,7 +1045,7 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaEventCreateWithFlags(&c->evJoin2, cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->evJoin3, cudaEventDisableTiming), "event");
         ck(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking), "cudaStreamCreate side");
-        ck(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc err");
+        ck(cudaMalloc(&c->d_err, 2 * sizeof(int)), "cudaMalloc err"); // [0] failing column, [1] inexact-moment flag
         ck(cudaEventCreate(&c->ev[0]), "event");
         ck(cudaEventCreate(&c->ev[1]), "event");
         ck(cudaMalloc(&c->fix_total, sizeof(unsigned long long)), "malloc fix counter");
@@ -1147,6 +1149,56 @@ int hk_load_moments(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps
         c->t[5] = now_s() - t0;
         c->n = n;
         c->factored = c->inverted = c->assembled = false;
+        return HK_OK;
+    });
+}
+
+// The 2n-1 moments generated on the device (csrc/moments_dev.cuh) straight
+// into the context's moment array; even q = 2/beta only (the factorial branch).
+int hk_generate_moments(hk_ctx* c, unsigned beta_num, unsigned beta_den, int n, int* exact) {
+    return guarded(c, [&] {
+        if (n < 1) return fail(c, HK_ERR_INVALID, "matrix order must be >= 1");
+        if (beta_num == 0 || beta_den == 0 || (2ul * beta_den) % beta_num != 0)
+            return fail(c, HK_ERR_INVALID, "unsupported beta: 2/beta must be a positive integer");
+        const unsigned long q = 2ul * beta_den / beta_num;
+        if (q % 2 != 0)
+            return fail(c, HK_ERR_INVALID,
+                        "hk_generate_moments: odd 2/beta (half-integer Gamma) is host-only: hk_moments + hk_load_moments");
+        const double t0 = now_s();
+        const int count = 2 * n - 1, L = c->L;
+        // limbs of the largest value (q/2) (count q/2 - 1)!, with slack
+        const double amax = double(count) * double(q / 2);
+        const double bits = std::lgamma(amax + 1.0) / std::log(2.0) + std::log2(double(q / 2)) + 96.0;
+        const long long need = (long long)(bits / 32.0) + 4;
+        int threads = int(std::min<long long>(hk::kMomMaxThreads, (need + 31) / 32 * 32));
+        int per = int((need + threads - 1) / threads);
+        per |= 1; // odd stride between the threads' segments: no bank conflicts
+        const size_t smem = ((q / 2 == 1 ? 1 : 2) * size_t(per) * threads + threads + 32) * sizeof(uint32_t);
+        if (smem > c->smem_optin || q / 2 > 0xfffffffful)
+            return fail(c, HK_ERR_INVALID, "hk_generate_moments: moments too large for the on-device generator");
+        c->mu.ensure(count, L);
+        int* d_inexact = c->d_err + 1; // second word of the error block
+        ck(cudaMemsetAsync(d_inexact, 0, sizeof(int), c->st), "memset");
+        func_smem((const void*)&hk::k_moments_fact, smem);
+        hk::MomentsArgs a{c->mu.d, c->mu.m, count, L, unsigned(q), per, d_inexact};
+        hk::k_moments_fact<<<1, threads, smem, c->st>>>(a);
+        ck(cudaGetLastError(), "k_moments_fact");
+        ++c->launches;
+        int inexact = 0;
+        ck(cudaMemcpyAsync(&inexact, d_inexact, sizeof(int), cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaStreamSynchronize(c->st), "sync");
+        if (exact) *exact = inexact ? 0 : 1;
+        c->t[5] = now_s() - t0;
+        c->n = n;
+        c->factored = c->inverted = c->assembled = false;
+        return HK_OK;
+    });
+}
+
+int hk_get_moments(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
+    return guarded(c, [&] {
+        if (c->n < 1 || !c->mu.d) return fail(c, HK_ERR_INVALID, "hk_get_moments: no moments on the device");
+        d2h_range(c, c->mu, 0, 2LL * c->n - 1, limbs, exps, signs);
         return HK_OK;
     });
 }
@@ -1363,15 +1415,12 @@ int hk_smallest_eigs(hk_ctx* c, int s, double* lambda_hi, double* lambda_lo, dou
     });
 }
 
-int hk_compute(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, const int32_t* signs, int k,
-               double* lambda_hi, double* lambda_lo, double* trunc_err, int* s_out) {
-    if (!c) return HK_ERR_INVALID;
-    if (n < 1) return fail(c, HK_ERR_INVALID, "compute: need N >= 1");
-    if (k < 1) return fail(c, HK_ERR_INVALID, "compute: need k >= 1");
-    const double t0 = now_s();
+namespace {
+// the path after the moments are on the device (pipeline.cpp:41-66)
+int compute_tail(hk_ctx* c, int n, int rc, int k, double* lambda_hi, double* lambda_lo, double* trunc_err,
+                 int* s_out, double t0) {
     const int kk = k < n ? k : n;    // pipeline.cpp:36
     const int s = kk < 3 ? kk : 3;   // pipeline.cpp:64
-    int rc = hk_load_moments(c, n, limbs, exps, signs);
     if (rc == HK_OK) rc = hk_ldlt(c);
     // L^-1 and the block are sharded too (every rank takes part); rank 0 then
     // holds the block and runs the eigensolve.  HK_DIST_INV=0: rank 0 alone
@@ -1390,6 +1439,27 @@ int hk_compute(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, con
     if (s_out) *s_out = rc == HK_OK ? s : 0;
     c->t[0] = now_s() - t0;
     return rc;
+}
+} // namespace
+
+int hk_compute(hk_ctx* c, int n, const uint32_t* limbs, const int32_t* exps, const int32_t* signs, int k,
+               double* lambda_hi, double* lambda_lo, double* trunc_err, int* s_out) {
+    if (!c) return HK_ERR_INVALID;
+    if (n < 1) return fail(c, HK_ERR_INVALID, "compute: need N >= 1");
+    if (k < 1) return fail(c, HK_ERR_INVALID, "compute: need k >= 1");
+    const double t0 = now_s();
+    const int rc = hk_load_moments(c, n, limbs, exps, signs);
+    return compute_tail(c, n, rc, k, lambda_hi, lambda_lo, trunc_err, s_out, t0);
+}
+
+int hk_compute_generated(hk_ctx* c, unsigned beta_num, unsigned beta_den, int n, int k, double* lambda_hi,
+                         double* lambda_lo, double* trunc_err, int* s_out, int* moments_exact) {
+    if (!c) return HK_ERR_INVALID;
+    if (n < 1) return fail(c, HK_ERR_INVALID, "compute: need N >= 1");
+    if (k < 1) return fail(c, HK_ERR_INVALID, "compute: need k >= 1");
+    const double t0 = now_s();
+    const int rc = hk_generate_moments(c, beta_num, beta_den, n, moments_exact);
+    return compute_tail(c, n, rc, k, lambda_hi, lambda_lo, trunc_err, s_out, t0);
 }
 
 int hk_set_limbs(hk_ctx* c, int limbs) {

@@ -32,6 +32,7 @@ class ComputeOptions:
     k: int = 8
     workers: int = 1
     device: int = 0
+    device_moments: bool = True  # even 2/beta: hk_generate_moments instead of host build_hankel + upload
 
 
 @dataclass
@@ -101,11 +102,18 @@ def compute(opts: ComputeOptions) -> RunRecord:
         raise ValueError("compute: need k >= 1")
     p = precision_bits(opts.beta, opts.n, opts.bits)
     L = p // 32
-    mu, exact = api.build_hankel(opts.beta, opts.n, L)
-    if not exact and (2 * opts.beta[1] // opts.beta[0]) % 2 == 0:
-        raise api.PrecisionError("compute: moments not exact at p bits")
-    with api.Context(L, device=opts.device) as ctx:
-        r = ctx.compute(mu, opts.k)
+    even_q = (2 * opts.beta[1] // opts.beta[0]) % 2 == 0
+    if opts.device_moments and even_q:  # moments.cpp:113-133 on the device
+        with api.Context(L, device=opts.device) as ctx:
+            r = ctx.compute_generated(opts.beta, opts.n, opts.k)
+            if not ctx.moments_exact:
+                raise api.PrecisionError("compute: moments not exact at p bits")
+    else:
+        mu, exact = api.build_hankel(opts.beta, opts.n, L)
+        if not exact and even_q:
+            raise api.PrecisionError("compute: moments not exact at p bits")
+        with api.Context(L, device=opts.device) as ctx:
+            r = ctx.compute(mu, opts.k)
     return RunRecord(n=opts.n, beta=tuple(opts.beta), bits=opts.bits, k=r.k, workers=opts.workers,
                      lambda_=[h + l for h, l in zip(r.lambda_hi, r.lambda_lo)], trunc_err=list(r.trunc_err),
                      wall_s=r.wall_s, ldlt_s=r.ldlt_s, invL_s=r.invL_s, invL_arith_s=r.invL_s, invH_s=r.invH_s,

@@ -140,3 +140,51 @@ def test_fused_rounding_bit_identical_to_rounding_pass(api, beta, n, L, k, monke
     for key in (("1", "0"), ("1", "1")):
         assert out[key][1] == base[1] and out[key][2] == base[2], key
         assert out[key][0].lambda_hi == base[0].lambda_hi
+
+
+def _same(a, b):
+    import numpy as np
+
+    return (np.array_equal(a.limbs, b.limbs) and np.array_equal(a.exps, b.exps) and np.array_equal(a.signs, b.signs))
+
+
+# moments generated on the device (csrc/moments_dev.cuh) against the
+# host generator (itself checked against the reference's integers, test_abi.py):
+# every BASELINE weight, exact (p > bits) and rounded (p < bits, RNE incl. sticky
+# and carry), one thread per limb and several limbs per thread
+@pytest.mark.parametrize("beta,n,L", [
+    ((1, 2), 64, 96),      # C1
+    ((1, 1), 256, 192),    # C2
+    ((1, 3), 512, 1152),   # C3
+    ((1, 2), 1024, 1536),  # C4
+    ((1, 2), 2048, 3584),  # C5 (several limbs per thread)
+    ((1, 1), 1, 4), ((1, 2), 2, 1), ((1, 4), 9, 3),
+    ((1, 2), 300, 8),      # rounded: 256 bits of a ~9000-bit integer
+    ((1, 1), 700, 31),     # rounded
+    ((1, 3), 150, 40),     # rounded, 3 factor pairs per moment
+    ((1, 1), 33000, 1),    # factors past 65535 (multiplied one at a time), a ~1 Mbit integer in shared memory
+])
+def test_device_moments_bit_identical_to_host(api, beta, n, L):
+    want, ex_h = api.build_hankel(beta, n, L)
+    with api.Context(L) as ctx:
+        ex_d = ctx.generate_moments(beta, n)
+        got = ctx.moments()
+    assert ex_d == ex_h
+    assert _same(got, want)
+
+
+def test_device_moments_compute_matches_host_path(api):
+    beta, n, L, k = (1, 2), 48, 48, 8
+    mu, exact = api.build_hankel(beta, n, L)
+    with api.Context(L) as ctx:
+        r0, D0, M0 = run(ctx, mu, k)
+        r1 = ctx.compute_generated(beta, n, k)
+        D1, M1 = from_arr(ctx.D()), from_arr(ctx.block())
+        assert exact and ctx.moments_exact
+    assert D1 == D0 and M1 == M0 and r1.lambda_hi == r0.lambda_hi and r1.lambda_lo == r0.lambda_lo
+
+
+def test_device_moments_odd_q_is_host_only(api):
+    with api.Context(8) as ctx:
+        with pytest.raises(ValueError):
+            ctx.generate_moments((2, 1), 8)  # beta = 2: half-integer Gamma needs sqrt(pi)
