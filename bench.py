@@ -378,6 +378,21 @@ def bench_ours(args, cfg):
     ms_k = kt.get("products_ms", 0.0)
     ldlt_ms = kt.get("ldlt_ms", 0.0)
     roofline = None
+    if ms_k == 0 and not tc_path and ldlt_ms > 0:
+        # small p: the whole LDLT is the one dataflow kernel k_ldlt_flow (no per-step launches)
+        peak = api.peak_imad(local) / 1e12
+        achieved = alg_macs / (ldlt_ms * 1e-3) / 1e12
+        roofline = {"bound": "imad", "unit": "Tlimb-MAC/s",
+                    "kernel": "k_ldlt_flow: the LDLT as one dataflow kernel (a CTA per entry applies all its "
+                              "updates in order, ldlt.cpp:91-135); latency-bound: its critical path is N x "
+                              "(fms -> reciprocal -> mul)",
+                    "peak_how": "hk_peak_imad: register-only IMAD.WIDE carry-chain microkernel, best of 5 "
+                                "(MEASURED_PEAKS.json has no integer peak)",
+                    "achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
+                    "per_launch": f"1 launch per step, {ldlt_ms:.4f} ms, {alg_macs:.3e} algorithmic limb-MACs",
+                    "algorithmic_units": "L^2 limb-MACs per MP-FMA (SURVEY 8d)",
+                    "how_timed": "CUDA events around the kernel on the context's stream (hk_timings ldlt_s)",
+                    "share_of_ldlt": 1.0, "kernel_ms_per_step": kt}
     if ms_k > 0:
         # the look-ahead column (ldlt.cpp:122-129 for j = i+1) runs on the chain, not in these launches
         bulk_macs = sum((n - i - 2) * (n - i - 1) // 2 for i in range(n)) * L * L

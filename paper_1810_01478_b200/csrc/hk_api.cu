@@ -171,7 +171,7 @@ struct hk_ctx {
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
     std::vector<cudaEvent_t> evP, evR, evU, evD, evO, evC, evB1; // per-step dependencies (graph capture)
     cudaEvent_t evJoin2 = nullptr, evJoin3 = nullptr;
-    DevArr mu, S, R, B, X, Y, T, T2, M, Dg;
+    DevArr mu, S, R, B, X, Y, T, T2, M, Dg, Vf; // Vf: unscaled columns of the dataflow LDLT
     int* d_err = nullptr;
     std::string err;
     int bad_col = -1;
@@ -210,6 +210,8 @@ struct hk_ctx {
     long long* tc_fb = nullptr;
     int* flow_ready = nullptr;    // dataflow L^-1: per-entry flags + entry counter
     long long flow_cap = 0;
+    int* lflow = nullptr;         // dataflow LDLT: control words, per-entry flags, per-column counts
+    long long lflow_cap = 0;      // entries it was sized for
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
     struct Shard {
         int rank = 0;
@@ -837,6 +839,247 @@ void enqueue_inv_flow(hk_ctx* c, cudaStream_t st) {
     ++c->launches;
 }
 
+// ---- LDLT as a dataflow (small p, IMAD path): the blocked rank-b update taken
+// to its limit, b = j.  One CTA per entry (k, j) of the lower triangle applies
+// ALL of that entry's rank-1 updates in the reference's order (ldlt.cpp:122-129,
+// ascending step i) while the entry sits in shared memory:
+//     acc = mu_{k+j};  for i = 0 .. j-1:  acc = RNE(acc - V(j,i) L(k,i))
+// V(j,i) = the entry (j,i) before scaling, L(k,i) = B_i(k) = RNE(V(k,i) R_i).  Then
+//     k == j:  D_j = acc (pivot test, ldlt.cpp:111), R_j = RNE(1/D_j)
+//     k >  j:  V(k,j) = acc,  L(k,j) = RNE(acc R_j) into S in place (ldlt.cpp:113-120)
+// Every operation and its order per entry are those of the N-step schedule, so
+// the factors are bit-identical; the accumulator is read and written once per
+// entry instead of once per step (N(N+1)/2 instead of N^3/6 passes over S), and
+// the N dependent step launches (each a look-ahead chain of 5 kernels) become
+// one kernel whose critical path per column is fms -> recip -> mul with a flag
+// hand-off between them.  Entries are taken from a global counter in
+// column-major order and wait only for entries of earlier columns (or their own
+// column's diagonal, taken earlier), i.e. for entries already held by running
+// CTAs: no deadlock whatever the residency.  A per-column completion count
+// (cols_done: every column below it is final) saves the per-entry flag polls
+// for all but the frontier columns.
+struct LdltFlowArgs {
+    MpArr S, V, R, mu;
+    int N, L;
+    int* ready;    // [N(N+1)/2 * fstride]: entry final (diagonal: R_j published)
+    int* col_cnt;  // [N]: finished entries of each column
+    int* ctl;      // [0] cols_done, [1] abort (1 pivot <= 0, 2 watchdog), [2..3] entry counter
+    int* err;      // failing column (ldlt.cpp:83-87)
+    int fstride, sleep_ns;
+};
+
+// false: the run was aborted (a pivot failed elsewhere) or the watchdog fired
+__device__ __forceinline__ bool flow_wait(const int* flag, int* abort_flag, int sleep_ns, int want = 2) {
+    long long spins = 0;
+    while (ld_acquire_gpu(flag) < want) {
+        if (*(volatile const int*)abort_flag != 0) return false;
+        if (++spins > (1LL << 26)) { // > 6 s on one flag: never in a healthy run
+            atomicCAS(abort_flag, 0, 2);
+            return false; // (the caller reports it through err = -2)
+        }
+        __nanosleep(sleep_ns);
+    }
+    return true;
+}
+
+// out-of-line copies of the three CTA ops: inlined together they cost the kernel
+// 128 registers and spills, and with them its residency
+__device__ __noinline__ Meta flow_fms(uint32_t* acc, Meta am, const uint32_t* xs, Meta xm, const uint32_t* ys, Meta ym,
+                                      int L, uint32_t* ws) {
+    return hk::cta_fms(acc, am, xs, xm, ys, ym, acc, L, hk::ctaws_carve(ws, L));
+}
+__device__ __noinline__ Meta flow_mulr(const uint32_t* acc, Meta am, const uint32_t* xs, Meta xm, uint32_t* out, int L,
+                                       uint32_t* ws) {
+    return hk::cta_mulr(acc, am, xs, xm, out, L, hk::ctaws_carve(ws, L));
+}
+__device__ __noinline__ Meta flow_recip(const uint32_t* acc, Meta am, uint32_t* out, int L, uint32_t* ws) {
+    return hk::cta_recip(acc, am, out, L, ws);
+}
+
+__global__ void __launch_bounds__(256) k_ldlt_flow(LdltFlowArgs a) {
+    extern __shared__ __align__(16) uint32_t lfs_[];
+    __shared__ unsigned long long e_s;
+    __shared__ int stop_s, done_s;
+    const int L = a.L, N = a.N, tid = int(threadIdx.x), nt = int(blockDim.x);
+    uint32_t* acc = lfs_;
+    uint32_t* xs = acc + hk::align4(L);
+    uint32_t* ys = xs + hk::align4(L);
+    uint32_t* zs = ys + hk::align4(L);
+    uint32_t* ws = zs + hk::align4(L);
+    const long long E = (long long)N * (N + 1) / 2;
+    int* cols_done = a.ctl;
+    int* abort_flag = a.ctl + 1;
+    unsigned long long* next = reinterpret_cast<unsigned long long*>(a.ctl + 2);
+    int known = 0; // columns < known are final (block-uniform)
+    // publish entry (k, j) as final (flag 2): flag, column count, and the prefix of finished columns
+    auto publish = [&](long long e, int j) {
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            st_release_gpu(a.ready + e * a.fstride, 2);
+            if (atomicAdd(a.col_cnt + j, 1) == N - j - 1) {
+                __threadfence();
+                int c = j;
+                while (c < N && atomicCAS(cols_done, c, c + 1) == c) {
+                    ++c;
+                    __threadfence();
+                    if (c >= N || *(volatile int*)(a.col_cnt + c) != N - c) break;
+                }
+            }
+        }
+    };
+    for (;;) {
+        if (tid == 0) {
+            e_s = atomicAdd(next, 1ull);
+            stop_s = 0;
+        }
+        __syncthreads();
+        const long long e = (long long)e_s;
+        if (e >= E) return;
+        int j, k;
+        hk::tri_decode(e, N, j, k);
+        for (int q = tid; q < L; q += nt) acc[q] = a.mu.limbs(k + j, L)[q];
+        Meta am = a.mu.m[k + j];
+        __syncthreads();
+        for (int i = 0; i < j; ++i) {
+            const long long exi = hk::tri_idx(j, i, N), eyi = hk::tri_idx(k, i, N);
+            // The diagonal's last update D_j -= V(j,j-1) L(j,j-1) sits on the critical
+            // path (R_{j-1} -> L(j,j-1) -> D_j -> R_j): this CTA forms L(j,j-1) =
+            // RNE(V(j,j-1) R_{j-1}) itself (the same value entry (j,j-1) stores) instead
+            // of waiting for that entry's publication: one flag hand-off less per column.
+            const bool own_l = k == j && i == j - 1;
+            if (i >= known) {
+                if (tid == 0) {
+                    const int cd = ld_acquire_gpu(cols_done);
+                    done_s = cd;
+                    // x = V(j,i) needs flag >= 1; y = L(k,i) needs 2 (k == j: the same entry)
+                    if (cd <= i && !flow_wait(a.ready + exi * a.fstride, abort_flag, a.sleep_ns, k == j && !own_l ? 2 : 1))
+                        stop_s = 1;
+                }
+                if (tid == 32 && k != j && !flow_wait(a.ready + eyi * a.fstride, abort_flag, a.sleep_ns)) stop_s = 1;
+                if (tid == 32 && own_l && !flow_wait(a.ready + hk::tri_idx(i, i, N) * a.fstride, abort_flag, a.sleep_ns))
+                    stop_s = 1;
+                __syncthreads();
+                if (stop_s) {
+                    if (tid == 0 && *(volatile int*)abort_flag == 2) atomicCAS(a.err, -1, -2);
+                    return;
+                }
+                known = done_s;
+            }
+            const uint32_t* ysrc = own_l ? a.R.limbs(i, L) : a.S.limbs(eyi, L);
+            for (int q = tid; q < L; q += nt) {
+                xs[q] = __ldcg(a.V.limbs(exi, L) + q);
+                ys[q] = __ldcg(ysrc + q);
+            }
+            const int2 xm2 = __ldcg(reinterpret_cast<const int2*>(a.V.m + exi));
+            int2 ym2 = __ldcg(reinterpret_cast<const int2*>(own_l ? a.R.m + i : a.S.m + eyi));
+            __syncthreads();
+            const uint32_t* yop = ys;
+            if (own_l) {
+                const Meta lm = flow_mulr(xs, Meta{xm2.x, xm2.y}, ys, Meta{ym2.x, ym2.y}, zs, L, ws);
+                ym2 = make_int2(lm.exp, lm.sign);
+                yop = zs;
+                __syncthreads();
+            }
+            am = flow_fms(acc, am, xs, Meta{xm2.x, xm2.y}, yop, Meta{ym2.x, ym2.y}, L, ws);
+            __syncthreads();
+        }
+        if (k == j) {
+            if (am.sign <= 0) { // ldlt.cpp:111: pivot must be positive
+                if (tid == 0) {
+                    atomicCAS(a.err, -1, j);
+                    __threadfence();
+                    atomicCAS(abort_flag, 0, 1);
+                }
+                return;
+            }
+            const Meta rm = flow_recip(acc, am, a.R.limbs(j, L), L, ws);
+            if (tid == 0) a.R.m[j] = rm;
+            for (int q = tid; q < L; q += nt) a.S.limbs(e, L)[q] = acc[q];
+            if (tid == 0) a.S.m[e] = am;
+            publish(e, j);
+        } else {
+            for (int q = tid; q < L; q += nt) a.V.limbs(e, L)[q] = acc[q];
+            if (tid == 0) a.V.m[e] = am;
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                st_release_gpu(a.ready + e * a.fstride, 1); // V(k,j) is final (x operand of row k's entries)
+                if (!flow_wait(a.ready + hk::tri_idx(j, j, N) * a.fstride, abort_flag, a.sleep_ns)) stop_s = 1;
+            }
+            __syncthreads();
+            if (stop_s) {
+                if (tid == 0 && *(volatile int*)abort_flag == 2) atomicCAS(a.err, -1, -2);
+                return;
+            }
+            for (int q = tid; q < L; q += nt) xs[q] = __ldcg(a.R.limbs(j, L) + q);
+            const int2 rm2 = __ldcg(reinterpret_cast<const int2*>(a.R.m + j));
+            __syncthreads();
+            const Meta bm = flow_mulr(acc, am, xs, Meta{rm2.x, rm2.y}, a.S.limbs(e, L), L, ws);
+            if (tid == 0) a.S.m[e] = bm;
+            publish(e, j);
+        }
+    }
+}
+
+constexpr int kLdltFlowStride = 8; // one 32-byte sector per flag
+constexpr long long kLdltFlowMaxWork = 1LL << 21; // n^2 L bound of the default selection
+
+int ldlt_flow_ws_words(int L) { return std::max(hk::ctaws_words(L), hk::ctarecipws_words(L)); }
+
+int ldlt_flow_threads() {
+    static const char* e = getenv("HK_LDLT_FLOW_THREADS");
+    const int t = e ? atoi(e) : 128;
+    return std::max(64, std::min(256, t / 32 * 32));
+}
+
+// The dataflow LDLT is for the IMAD path (p below the tensor-core threshold):
+// past a few thousand entries of a few thousand MACs each the N-step schedule's
+// paired warp FMAs have the better throughput.  HK_LDLT_FLOW=0/1 forces it.
+bool use_ldlt_flow(const hk_ctx* c) {
+    if (c->world > 1 || c->virt || c->nccl_comm) return false;
+    const size_t smem = (4 * size_t(hk::align4(c->L)) + ldlt_flow_ws_words(c->L)) * sizeof(uint32_t);
+    if (smem > c->smem_optin) return false;
+    if (const char* e = getenv("HK_LDLT_FLOW")) return e[0] == '1';
+    if (use_tc(c)) return false;
+    return (long long)c->n * c->n * c->L <= kLdltFlowMaxWork;
+}
+
+// [8 control ints][flags][column counts]; n <= ntri
+size_t ldlt_flow_ints(long long ntri, int n) { return 8 + size_t(ntri) * kLdltFlowStride + size_t(n); }
+
+void ensure_ldlt_flow(hk_ctx* c, long long ntri) {
+    c->Vf.ensure(ntri, c->L);
+    if (c->lflow_cap >= ntri) return;
+    if (c->lflow) cudaFree(c->lflow);
+    c->lflow = nullptr;
+    c->lflow_cap = 0;
+    ck(cudaMalloc(&c->lflow, ldlt_flow_ints(ntri, c->n) * sizeof(int)), "cudaMalloc ldlt flow");
+    c->lflow_cap = ntri;
+}
+
+void enqueue_ldlt_flow(hk_ctx* c, cudaStream_t st) {
+    const int N = c->n, L = c->L;
+    const long long ntri = (long long)N * (N + 1) / 2;
+    int* ctl = c->lflow;
+    int* ready = ctl + 8;
+    int* col_cnt = ready + ntri * kLdltFlowStride;
+    ck(cudaMemsetAsync(c->lflow, 0, ldlt_flow_ints(ntri, N) * sizeof(int), st), "memset ldlt flow");
+    const char* sl = getenv("HK_FLOW_SLEEP");
+    const int sleep_ns = sl ? atoi(sl) : 100;
+    const size_t smem = (4 * size_t(hk::align4(L)) + ldlt_flow_ws_words(L)) * sizeof(uint32_t);
+    func_smem((const void*)k_ldlt_flow, smem);
+    const int threads = ldlt_flow_threads();
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ldlt_flow, threads, smem), "occupancy");
+    const unsigned grid = unsigned(std::max(1LL, std::min(ntri, (long long)std::max(1, per_sm) * c->sm_count)));
+    LdltFlowArgs a{c->S.view(), c->Vf.view(), c->R.view(), c->mu.view(), N, L, ready, col_cnt, ctl, c->d_err,
+                   kLdltFlowStride, sleep_ns};
+    k_ldlt_flow<<<grid, threads, smem, st>>>(a);
+    ck(cudaGetLastError(), "ldlt flow launch");
+    ++c->launches;
+}
+
 // Tensor-core buffers: the A operand of N rows, product scratch for `p_items`
 // products (the unfused rounding pass and L^-1 steps; the fused LDLT needs
 // none) and the fix-up list for `fb_items` items per step.
@@ -983,6 +1226,10 @@ int check_pivots(hk_ctx* c) {
     int e = -1;
     ck(cudaMemcpyAsync(&e, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->st), "D2H err");
     ck(cudaStreamSynchronize(c->st), "sync");
+    if (e == -2) { // k_ldlt_flow's watchdog: a flag never arrived
+        c->factored = false;
+        return fail(c, HK_ERR_RUNTIME, "hk_ldlt: the dataflow kernel's watchdog fired (a dependency flag never arrived)");
+    }
     if (e >= 0) {
         c->bad_col = e;
         c->factored = false;
@@ -1068,7 +1315,7 @@ void hk_destroy(hk_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     drop_graphs(c);
-    for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg}) a->release();
+    for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg, &c->Vf}) a->release();
     for (auto& s : c->shards) {
         for (DevArr* a : {&s.S, &s.panel, &s.R, &s.B, &s.X, &s.Y, &s.T, &s.T2}) a->release();
         if (s.d_otiles) cudaFree(s.d_otiles);
@@ -1105,6 +1352,7 @@ void hk_destroy(hk_ctx* c) {
     if (c->tc_A) cudaFree(c->tc_A);
     if (c->tc_gcarry) cudaFree(c->tc_gcarry);
     if (c->flow_ready) cudaFree(c->flow_ready);
+    if (c->lflow) cudaFree(c->lflow);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);
@@ -1211,10 +1459,28 @@ int hk_ldlt(hk_ctx* c) {
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
+        c->bad_col = -1;
+        if (use_ldlt_flow(c)) {
+            // small p: the whole factorisation as one dataflow kernel (k_ldlt_flow)
+            ensure_ldlt_flow(c, ntri);
+            ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
+            ck(cudaEventRecord(c->ev[0], c->st), "event");
+            enqueue_ldlt_flow(c, c->st);
+            c->kev_steps = 0;
+            ck(cudaEventRecord(c->ev[1], c->st), "event");
+            ck(cudaEventSynchronize(c->ev[1]), "sync");
+            float fms = 0;
+            ck(cudaEventElapsedTime(&fms, c->ev[0], c->ev[1]), "elapsed");
+            c->t[1] = fms * 1e-3;
+            const int frc = check_pivots(c);
+            if (frc != HK_OK) return frc;
+            c->factored = true;
+            c->inverted = c->assembled = false;
+            return HK_OK;
+        }
         c->B.ensure(3LL * N, L);
         ensure_tc_scratch(c);
         ensure_step_events(c, N);
-        c->bad_col = -1;
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         ck(cudaEventRecord(c->ev[0], c->st), "event");
         launch(c, hk::ItemInitS{c->S.view(), c->mu.view(), N, L}, ntri, 64);
@@ -1468,7 +1734,7 @@ int hk_set_limbs(hk_ctx* c, int limbs) {
         if (limbs == c->L) return HK_OK;
         ck(cudaStreamSynchronize(c->st), "sync");
         drop_graphs(c);
-        for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg}) a->release();
+        for (DevArr* a : {&c->mu, &c->S, &c->R, &c->B, &c->X, &c->Y, &c->T, &c->T2, &c->M, &c->Dg, &c->Vf}) a->release();
         for (auto& sh : c->shards) {
             for (DevArr* a : {&sh.S, &sh.panel, &sh.R, &sh.B, &sh.X, &sh.Y, &sh.T, &sh.T2}) a->release();
             sh.setup_n = -1;

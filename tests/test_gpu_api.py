@@ -25,9 +25,37 @@ def run(ctx, mu, k):
     return rec, from_arr(ctx.D()), from_arr(ctx.block())
 
 
+def test_dataflow_ldlt_same_bits_as_step_graph(api, monkeypatch):
+    """Small p: the one-kernel dataflow LDLT (k_ldlt_flow, the default below the tensor-core
+    threshold) against the N-step look-ahead graph: every pivot, every column of L, the block
+    and lambda bit for bit; it reports no per-step kernel times."""
+    for beta, n, L, k, threads in [((1, 2), 64, 96, 8, None), ((1, 1), 97, 40, 8, "64"), ((1, 3), 33, 100, 12, "256"),
+                                   ((1, 1), 120, 96, 16, None)]:
+        if threads:
+            monkeypatch.setenv("HK_LDLT_FLOW_THREADS", threads)
+        else:
+            monkeypatch.delenv("HK_LDLT_FLOW_THREADS", raising=False)
+        mu, exact = api.build_hankel(beta, n, L)
+        assert exact
+        got = {}
+        for flow in ("0", "1"):
+            monkeypatch.setenv("HK_LDLT_FLOW", flow)
+            with api.Context(L) as ctx:
+                ctx.set_kernel_timing(True)
+                rec, D, M = run(ctx, mu, k)
+                cols = [from_arr(ctx.L_column(j)) for j in range(n - 1)]
+                steps = ctx.kernel_times()["steps"]
+                rec2, D2, M2 = run(ctx, mu, k)  # replay on the same context
+                assert D2 == D and M2 == M
+            got[flow] = (rec.lambda_hi, rec.lambda_lo, D, M, cols)
+            assert steps == (0 if flow == "1" else n - 2)
+        assert got["0"] == got["1"]
+
+
 @pytest.mark.parametrize("beta,n,L,k,tc", [((1, 2), 48, 8, 8, "0"), ((1, 1), 40, 192, 8, "1")])
 def test_kernel_timing_nodes_do_not_change_results(api, beta, n, L, k, tc, monkeypatch):
     monkeypatch.setenv("HK_TC", tc)
+    monkeypatch.setenv("HK_LDLT_FLOW", "0")  # the timing nodes belong to the N-step graph
     mu, _ = api.build_hankel(beta, n, L)
     with api.Context(L) as ctx:
         r0, D0, M0 = run(ctx, mu, k)

@@ -83,8 +83,10 @@ def run_path(api, beta, n, L, k):
 @pytest.mark.parametrize("beta,n,L,k", [((1, 2), 1, 2, 1), ((1, 2), 2, 4, 2), ((1, 2), 8, 4, 4), ((1, 1), 24, 6, 8),
                                         ((1, 3), 20, 24, 12), ((1, 2), 64, 96, 8)])
 @pytest.mark.parametrize("inv_flow", ["1", "0"])  # small-p L^-1: dataflow kernel / N-step schedule
-def test_path_bit_exact_vs_model(api, beta, n, L, k, inv_flow, monkeypatch):
+@pytest.mark.parametrize("ldlt_flow", ["1", "0"])  # small-p LDLT: dataflow kernel / N-step look-ahead graph
+def test_path_bit_exact_vs_model(api, beta, n, L, k, inv_flow, ldlt_flow, monkeypatch):
     monkeypatch.setenv("HK_INV_FLOW", inv_flow)
+    monkeypatch.setenv("HK_LDLT_FLOW", ldlt_flow)
     p = 32 * L
     mu = [R.moment_integer(beta, j) for j in range(2 * n - 1)]
     D, Lf, Rr = F.ldlt(mu, n, p)
@@ -92,9 +94,8 @@ def test_path_bit_exact_vs_model(api, beta, n, L, k, inv_flow, monkeypatch):
     M = F.block(X, Rr, n, k, p)
     with run_path(api, beta, n, L, k) as ctx:
         assert from_arr(ctx.D()) == D
-        if n > 1:
-            assert from_arr(ctx.L_column(0)) == Lf[0]
-            assert from_arr(ctx.L_column(n - 2)) == Lf[n - 2]
+        for j in range(n - 1):
+            assert from_arr(ctx.L_column(j)) == Lf[j]
         gx = from_arr(ctx.Linv())
         assert all(gx[r * k + c] == X[r][c] for r in range(n) for c in range(min(r, k)))
         assert all(gx[r * k + c] == F.ZERO for r in range(n) for c in range(min(r, k), k))
@@ -252,7 +253,7 @@ def test_block_eigenvalue_grows_with_k(api):
             prev = mu_max
 
 
-def test_precision_exhaustion_raises_with_column(api):
+def test_precision_exhaustion_raises_with_column(api, monkeypatch):
     """beta = 1 at p = 32 bits: a pivot goes non-positive -> precision_error with the
     first bad column (ldlt.cpp:83-87); the model agrees on the column."""
     n, L = 16, 1
@@ -261,13 +262,17 @@ def test_precision_exhaustion_raises_with_column(api):
     with pytest.raises(ArithmeticError) as ei:
         F.ldlt(mu_int, n, 32)
     want = int(str(ei.value).rsplit(" ", 1)[1])
-    with api.Context(L) as ctx:
-        ctx.load_moments(mu)
-        with pytest.raises(api.PrecisionError):
+    for flow in ("1", "0"):  # the dataflow kernel (aborts every waiting CTA) and the N-step graph
+        monkeypatch.setenv("HK_LDLT_FLOW", flow)
+        with api.Context(L) as ctx:
+            ctx.load_moments(mu)
+            with pytest.raises(api.PrecisionError):
+                ctx.decompose()
+            assert ctx.bad_column == want
+            with pytest.raises(ValueError):
+                ctx.D()  # not factored
+            ctx.load_moments(api.build_hankel((1, 2), 2, L)[0])  # the context survives the failure
             ctx.decompose()
-        assert ctx.bad_column == want
-        with pytest.raises(ValueError):
-            ctx.D()  # not factored
 
 
 def test_invalid_arguments(api):
