@@ -540,10 +540,75 @@ HK_DEV uint32_t reg_limb(uint32_t lo, uint32_t hi, int t) {
     return t < 32 ? vl : vh;
 }
 
+// ---- The first Newton levels in scalar code.  A register level costs ~2200
+// cycles whatever its size (two products' staging, shuffles and ballot carry
+// passes: measured with tools/recip_probe.cu), and the schedule crawls through
+// 3, 4, 5, 8 limbs before the sizes start to matter.  Up to 8 fraction limbs the
+// same level formulas are therefore evaluated by every lane redundantly on
+// compile-time-sized arrays (fully unrolled, all in registers): 2 -> 3 -> 4 ->
+// 6 -> 8 limbs, each level with the two limbs of slack the schedule keeps
+// (nk <= 2 nf - 2; the binary64 seed's 2 -> 3).  The result only seeds the later
+// levels: the final Ziv test / exact midpoint test still decides the rounding.
+template <int NA, int NB>
+HK_DEV void scalar_mul(const uint32_t (&A)[NA], const uint32_t (&B)[NB], uint32_t (&P)[NA + NB]) {
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+    for (int t = 0; t < NA + NB - 1; ++t) {
+#pragma unroll
+        for (int s = 0; s < NA; ++s)
+            if (t - s >= 0 && t - s < NB) mac96(c0, c1, c2, A[s], B[t - s]);
+        P[t] = c0;
+        c0 = c1;
+        c1 = c2;
+        c2 = 0;
+    }
+    P[NA + NB - 1] = c0;
+}
+
+// One level nf = NF -> nk = NK fraction limbs (NK <= 8 <= L, so m_top = the top NK
+// limbs Mt[8 - NK .. 8) of m): the formulas of the register / CTA levels below.
+template <int NF, int NK>
+HK_DEV void scalar_recip_level(const uint32_t (&Mt)[8], const uint32_t (&Zi)[NF + 1], uint32_t (&Zo)[NK + 1]) {
+    uint32_t mtop[NK];
+#pragma unroll
+    for (int q = 0; q < NK; ++q) mtop[q] = Mt[8 - NK + q];
+    uint32_t T[NK + NF + 1];
+    scalar_mul<NK, NF + 1>(mtop, Zi, T); // FT = NK + NF fraction limbs
+    const bool neg = T[NK + NF] != 0u;   // T >= 1  ->  e <= 0
+    uint32_t E[NK];
+#pragma unroll
+    for (int q = 0; q < NK; ++q) E[q] = neg ? T[NF + q] : ~T[NF + q];
+    uint32_t D[NF + 1 + NK];
+    scalar_mul<NF + 1, NK>(Zi, E, D);
+    uint32_t c = 0; // borrow / carry
+#pragma unroll
+    for (int q = 0; q <= NK; ++q) {
+        const uint32_t zv = q >= NK - NF ? Zi[q - (NK - NF)] : 0u;
+        const uint32_t dv = D[NF + q];
+        const uint64_t d = neg ? (uint64_t)zv - dv - c : (uint64_t)zv + dv + c;
+        Zo[q] = uint32_t(d);
+        c = neg ? uint32_t(d >> 63) : uint32_t(d >> 32);
+    }
+}
+
+constexpr int kScalarLevel = 8; // fraction limbs the scalar levels deliver (L >= kScalarLevel only)
+
+// z ~ 1/m to 8 fraction limbs from the binary64 seed Z2 (2 fraction limbs + integer limb)
+HK_DEV void scalar_recip8(const uint32_t (&Mt)[8], const uint32_t (&Z2)[3], uint32_t (&Z8)[9]) {
+    uint32_t Z3[4], Z4[5], Z6[7];
+    scalar_recip_level<2, 3>(Mt, Z2, Z3);
+    scalar_recip_level<3, 4>(Mt, Z3, Z4);
+    scalar_recip_level<4, 6>(Mt, Z4, Z6);
+    scalar_recip_level<6, 8>(Mt, Z6, Z8);
+}
+
 // The small Newton levels (nk <= kRegLevel limbs): warp 0 alone with one limb per
 // lane in registers — no shared-memory staging, no block barriers.
 #ifndef HK_REG_LEVEL
 #define HK_REG_LEVEL 30
+#endif
+#ifndef HK_SCALAR_RECIP_LEVELS
+#define HK_SCALAR_RECIP_LEVELS 1
 #endif
 constexpr int kRegLevel = HK_REG_LEVEL;
 
@@ -578,9 +643,28 @@ HK_DEV Meta cta_recip(const uint32_t* Md, Meta dm, uint32_t* out, int L, uint32_
             Zr = ln == 0 ? uint32_t(lo) : ln == 1 ? uint32_t(lo >> 32) : ln == 2 ? uint32_t(mant >> (64 - sh)) : 0u;
         }
         int nfr = 2;
+        if (L >= kScalarLevel && HK_SCALAR_RECIP_LEVELS) { // levels up to 8 limbs in scalar code (every lane the same)
+            uint32_t Mt8[8], Z2[3], Z8[9];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) Mt8[q] = Md[L - 8 + q];
+            {
+                const int sh = ex + 11;
+                const uint64_t lo = mant << sh;
+                Z2[0] = uint32_t(lo);
+                Z2[1] = uint32_t(lo >> 32);
+                Z2[2] = uint32_t(mant >> (64 - sh));
+            }
+            scalar_recip8(Mt8, Z2, Z8);
+            Zr = 0u;
+#pragma unroll
+            for (int q = 0; q <= 8; ++q)
+                if (ln == q) Zr = Z8[q];
+            nfr = kScalarLevel;
+        }
         HK_TRACE(13);
         for (int r = 0; r < nreg; ++r) {
             const int nk = sched[ns - 1 - r];
+            if (nk <= nfr) continue; // covered by the scalar levels
             const int mn = nk >= L ? L : nk;
             const uint32_t mv = shfl(Mt, (L - mn - mbase + ln) & 31);
             const uint32_t mtop = ln < mn ? mv : 0u;
