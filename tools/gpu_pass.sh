@@ -12,6 +12,11 @@ for w in $what; do
     tests) timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_gputests.log 2>&1; echo "tests rc=$?";;
     bench) timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/${tag}_bench_c4.json 2> gpurun_out/${tag}_bench_c4.err; echo "bench rc=$?";;
     c2) timeout 300 python bench.py --config c2 --steps 10 --warmup 3 > gpurun_out/${tag}_bench_c2.json 2> gpurun_out/${tag}_bench_c2.err; echo "c2 rc=$?";;
+    c1) timeout 300 python bench.py --config c1 --steps 20 --warmup 3 > gpurun_out/${tag}_bench_c1.json 2> gpurun_out/${tag}_bench_c1.err; echo "c1 rc=$?";;
+    ncuflow)
+      timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ldlt_flow -s 2 -c 1 \
+        -o gpurun_out/${tag}_prof_lflow_c1 -f python tools/one_run.py c1 4 > gpurun_out/${tag}_ncu_lflow_c1.log 2>&1; echo "ncu lflow rc=$?"
+      ;;
     c3) timeout 300 python bench.py --config c3 --steps 3 --warmup 3 > gpurun_out/${tag}_bench_c3.json 2> gpurun_out/${tag}_bench_c3.err; echo "c3 rc=$?";;
     ncu)
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_tc_bulk -s 300 -c 1 \

@@ -22,5 +22,5 @@ with api.Context(L) as ctx:
         except api.PrecisionError:  # dev what-if runs (wrong values): still report the LDLT's device time
             print(f"ldlt {ctx.timings()[1] * 1e3:.2f} ms (precision error: what-if run)", flush=True)
             continue
-        print(f"fix {ctx.fix_count()} wall {1e3 * (time.perf_counter() - t):.2f} ms ldlt {rec.ldlt_s * 1e3:.2f} invL {rec.invL_s * 1e3:.2f} "
-              f"lambda {rec.lambda_hi[0]!r}", flush=True)
+        print(f"fix {ctx.fix_count()} wall {1e3 * (time.perf_counter() - t):.2f} ms ldlt {rec.ldlt_s * 1e3:.2f} invL {rec.invL_s * 1e3:.2f} invH {rec.invH_s * 1e3:.2f} eig {rec.eigen_s * 1e3:.2f} "
+              f"h2d {rec.h2d_s * 1e3:.2f} d2h {rec.d2h_s * 1e3:.2f} lambda {rec.lambda_hi[0]!r}", flush=True)
