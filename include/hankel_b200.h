@@ -101,6 +101,14 @@ int hk_get_L_column(hk_ctx* ctx, int col, uint32_t* limbs, int32_t* exps, int32_
  * (inversion.hpp:40, 45-46).  hk_get_Linv returns n*m values row-major; entry
  * (r,c) is L^{-1}(r,c) for c < r, and 0 for c >= r (unit diagonal implicit). */
 int hk_invert_L_partial(hk_ctx* ctx, int m);
+/* hk_ldlt followed by hk_invert_L_partial(m) as ONE call — the pair compute()
+ * runs back to back (pipeline.cpp:41-58).  Where both stages are latency-bound
+ * (one GPU, small p) the row-elimination steps of L^{-1} (inversion.cpp:93-102)
+ * ride in the factorisation's graph, step i right after column i of L is in
+ * place; otherwise the two passes run one after the other.  Results are
+ * bit-identical either way; hk_timings()[1] / [2] = the LDLT proper and what
+ * was left of L^{-1} after it. */
+int hk_ldlt_invert(hk_ctx* ctx, int m);
 int hk_get_Linv(hk_ctx* ctx, uint32_t* limbs, int32_t* exps, int32_t* signs);
 
 /* k x k leading block of H^{-1} = sum_l Linv(l,j) Linv(l,c) / D_l, k <= m.

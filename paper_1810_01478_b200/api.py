@@ -56,6 +56,7 @@ def lib():
             "hk_compute_generated": (C.c_int, [vp, C.c_uint, C.c_uint, C.c_int, C.c_int, f64p, f64p, f64p,
                                                C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "hk_ldlt": (C.c_int, [vp]),
+            "hk_ldlt_invert": (C.c_int, [vp, C.c_int]),
             "hk_get_D": (C.c_int, [vp, u32p, i32p, i32p]),
             "hk_get_L_column": (C.c_int, [vp, C.c_int, u32p, i32p, i32p]),
             "hk_invert_L_partial": (C.c_int, [vp, C.c_int]),
@@ -287,6 +288,15 @@ class Context:
     def invert_L_partial(self, m: int):
         _check(lib().hk_invert_L_partial(self.h, m), self.h)
         self.m = m
+
+    def decompose_invert(self, m: int):
+        """decompose + invert_L_partial(m) as compute() runs them (hk_ldlt_invert: L^-1 steps
+        interleaved with the factorisation where both are latency-bound; same bits)."""
+        self.m = m
+        rc = lib().hk_ldlt_invert(self.h, m)
+        if rc == HK_ERR_PRECISION:
+            self.bad_column = lib().hk_bad_column(self.h)
+        _check(rc, self.h)
 
     def Linv(self) -> MPArray:
         out = MPArray.empty(self.n * self.m, self.L)

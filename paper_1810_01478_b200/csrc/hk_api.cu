@@ -168,6 +168,8 @@ struct hk_ctx {
     cudaStream_t st2 = nullptr; // high-priority look-ahead stream
     cudaStream_t st3 = nullptr; // high-priority: off-diagonal part of the look-ahead column
     cudaStream_t st4 = nullptr; // side stream: StoreL (L in place), off both critical streams
+    cudaStream_t st5 = nullptr; // L^-1 steps interleaved with the LDLT (hk_ldlt_invert)
+    cudaEvent_t evJoin4 = nullptr, evMid = nullptr; // its join; end of the LDLT proper (timing split)
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
     std::vector<cudaEvent_t> evP, evR, evU, evD, evO, evC, evB1; // per-step dependencies (graph capture)
     cudaEvent_t evJoin2 = nullptr, evJoin3 = nullptr;
@@ -1120,7 +1122,28 @@ void ensure_tc_scratch(hk_ctx* c, int m = 0) {
     ensure_tc_items(c, p_items, std::max(tri, nm + c->n));
 }
 
-void enqueue_ldlt_steps(hk_ctx* c) {
+// One L^-1 step of the N-step schedule (small p): few items a CTA per FMA, many a warp per FMA
+void enqueue_inv_step(hk_ctx* c, int i, int m, cudaStream_t st, const int* err = nullptr) {
+    const int N = c->n, L = c->L;
+    const int b = i < m ? i : m;
+    const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
+    if (items <= 4LL * c->sm_count) {
+        hk::CItemInvStep f{c->S.view(), c->X.view(), N, L, m, i};
+        f.err = err;
+        launch_cta(c, f, items, ws_cta_words(L), st);
+    } else {
+        hk::ItemInvStep f{c->S.view(), c->X.view(), N, L, m, i};
+        f.err = err;
+        launch(c, f, items, ws_op_words(L), st);
+    }
+}
+
+// inv_m > 0 (hk_ldlt_invert): the L^-1 row-elimination step i (inversion.cpp:93-102)
+// rides in the same graph on a low-priority stream, right after column i of L
+// is in place (StoreL(i)) and step i-1 — the steps need nothing else from the
+// factorisation, so for latency-bound sizes the first m columns of L^-1 are
+// ready a step after the LDLT ends instead of a whole pass later.
+void enqueue_ldlt_steps(hk_ctx* c, int inv_m = 0) {
     const int N = c->n, L = c->L;
     const int wo = ws_op_words(L), wr = ws_recip_words(L);
     cudaStream_t la = c->st2, bulk = c->st;
@@ -1138,6 +1161,13 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     ck(cudaEventRecord(c->evFork, bulk), "fork");
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
     ck(cudaStreamWaitEvent(side, c->evFork, 0), "fork wait side");
+    cudaStream_t inv = c->st5;
+    if (inv_m > 0) {
+        ck(cudaStreamWaitEvent(inv, c->evFork, 0), "fork wait inv");
+        hk::ItemInvInit ii{c->S.view(), c->X.view(), N, L, inv_m};
+        ii.zero = 1; // column c of X is set at step c, before any use
+        launch(c, ii, (long long)N * inv_m, 64, inv);
+    }
     const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
     (void)wr;
     launch_recip(c, 0, la);
@@ -1161,6 +1191,10 @@ void enqueue_ldlt_steps(hk_ctx* c) {
             if (!dev_skip("storel"))
                 launch(c, hk::ItemStoreL{c->S.view(), b_buf(c, i - 1), N, L, i - 1}, N - i, 64, side);
             ck(cudaEventRecord(evR[i - 1], side), "evR");
+            if (inv_m > 0 && i - 1 < N - 1) { // L^-1 step i-1: column i-1 of L is in place
+                ck(cudaStreamWaitEvent(inv, evR[i - 1], 0), "wait R inv");
+                enqueue_inv_step(c, i - 1, inv_m, inv, c->d_err);
+            }
         }
         if (i + 1 < N) {
             // P(i+1): the diagonal entry -> reciprocal on `la`, the rest of the
@@ -1203,6 +1237,11 @@ void enqueue_ldlt_steps(hk_ctx* c) {
     }
     ck(cudaEventRecord(c->evJoin3, side), "join3");
     ck(cudaStreamWaitEvent(bulk, c->evJoin3, 0), "join3 wait");
+    if (inv_m > 0) {
+        graph_event(c->evMid, bulk); // the LDLT proper ends here (ldlt_s / invL_s split)
+        ck(cudaEventRecord(c->evJoin4, inv), "join4");
+        ck(cudaStreamWaitEvent(bulk, c->evJoin4, 0), "join4 wait");
+    }
 }
 
 void ensure_step_events(hk_ctx* c, int N) {
@@ -1292,6 +1331,9 @@ int hk_create(int device, int limbs, hk_ctx** out) {
         ck(cudaEventCreateWithFlags(&c->evJoin2, cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->evJoin3, cudaEventDisableTiming), "event");
         ck(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking), "cudaStreamCreate side");
+        ck(cudaStreamCreateWithPriority(&c->st5, cudaStreamNonBlocking, lo), "cudaStreamCreate inv");
+        ck(cudaEventCreateWithFlags(&c->evJoin4, cudaEventDisableTiming), "event");
+        ck(cudaEventCreate(&c->evMid), "event");
         ck(cudaMalloc(&c->d_err, 2 * sizeof(int)), "cudaMalloc err"); // [0] failing column, [1] inexact-moment flag
         ck(cudaEventCreate(&c->ev[0]), "event");
         ck(cudaEventCreate(&c->ev[1]), "event");
@@ -1367,6 +1409,9 @@ void hk_destroy(hk_ctx* c) {
     if (c->evJoin2) cudaEventDestroy(c->evJoin2);
     if (c->evJoin3) cudaEventDestroy(c->evJoin3);
     if (c->st4) cudaStreamDestroy(c->st4);
+    if (c->st5) cudaStreamDestroy(c->st5);
+    if (c->evJoin4) cudaEventDestroy(c->evJoin4);
+    if (c->evMid) cudaEventDestroy(c->evMid);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
     if (c->st2) cudaStreamDestroy(c->st2);
@@ -1451,11 +1496,26 @@ int hk_get_moments(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
     });
 }
 
-int hk_ldlt(hk_ctx* c) {
+} // extern "C"
+
+namespace {
+// The L^-1 steps can ride in the LDLT graph (hk_ldlt_invert) when both run the
+// N-step schedules on one GPU and L^-1 is latency-bound (small p, IMAD steps).
+// HK_INV_OVERLAP=0 keeps the two passes apart.
+bool can_overlap_inverse(const hk_ctx* c) {
+    if (c->world > 1 || c->virt || c->nccl_comm) return false;
+    if (use_ldlt_flow(c) || use_tc_inv(c)) return false;
+    const char* e = getenv("HK_INV_OVERLAP");
+    return !e || e[0] != '0';
+}
+
+// hk_ldlt (inv_m == 0) / the overlapped part of hk_ldlt_invert (inv_m > 0)
+int ldlt_impl(hk_ctx* c, int inv_m) {
     return guarded(c, [&] {
         if (c->n < 1) return fail(c, HK_ERR_INVALID, "hk_ldlt: no moments loaded");
         if (c->world > 1 || c->virt || c->nccl_comm) return dist_ldlt(c);
         const int N = c->n, L = c->L;
+        if (inv_m > 0) c->X.ensure((long long)N * inv_m, L);
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
@@ -1489,37 +1549,68 @@ int hk_ldlt(hk_ctx* c) {
         const std::vector<const void*> sig{c->S.d, c->S.m, c->R.d, c->B.d, c->mu.d,
                                            use_fuse(c) ? nullptr : (const void*)c->tc_P, c->tc_A, c->tc_fb,
                                            c->tc_fb_count, (const void*)(long long)use_tc(c),
-                                           (const void*)(long long)use_fuse(c), (const void*)(long long)c->kprof};
+                                           (const void*)(long long)use_fuse(c), (const void*)(long long)c->kprof,
+                                           c->X.d, c->X.m};
         if (sig != c->graph_sig) {
             for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
             c->graphs.clear();
             c->graph_sig = sig;
         }
-        auto it = c->graphs.find(N);
+        const int key = N + (inv_m << 20); // graphs with the L^-1 steps interleaved are cached per (n, m)
+        auto it = c->graphs.find(key);
         if (it == c->graphs.end()) {
             const long long before = c->launches;
             Capture cap(c->st);
-            enqueue_ldlt_steps(c);
+            enqueue_ldlt_steps(c, inv_m);
             const cudaGraphExec_t ge = instantiate(cap.end(), cudaGraphInstantiateFlagUseNodePriority);
-            it = c->graphs.emplace(N, ge).first;
-            c->graph_launches[N] = c->launches - before;
-            c->kev_steps_by_n[N] = c->kev_steps;
+            it = c->graphs.emplace(key, ge).first;
+            c->graph_launches[key] = c->launches - before;
+            c->kev_steps_by_n[key] = c->kev_steps;
             c->launches = before;
         }
         ck(cudaGraphLaunch(it->second, c->st), "graph launch");
-        c->launches += c->graph_launches[N];
-        c->kev_steps = c->kev_steps_by_n[N];
+        c->launches += c->graph_launches[key];
+        c->kev_steps = c->kev_steps_by_n[key];
         ck(cudaEventRecord(c->ev[1], c->st), "event");
         ck(cudaEventSynchronize(c->ev[1]), "sync");
         float ms = 0;
-        ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
-        c->t[1] = ms * 1e-3;
+        if (inv_m > 0) { // the LDLT proper ends at evMid; what is left of L^-1 after it is invL_s
+            ck(cudaEventElapsedTime(&ms, c->ev[0], c->evMid), "elapsed");
+            c->t[1] = ms * 1e-3;
+            ck(cudaEventElapsedTime(&ms, c->evMid, c->ev[1]), "elapsed");
+            c->t[2] = ms * 1e-3;
+        } else {
+            ck(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]), "elapsed");
+            c->t[1] = ms * 1e-3;
+        }
         const int rc = check_pivots(c);
         if (rc != HK_OK) return rc;
         c->factored = true;
         c->inverted = c->assembled = false;
+        if (inv_m > 0) {
+            c->m = inv_m;
+            c->inverted = true;
+        }
         return HK_OK;
     });
+}
+} // namespace
+
+extern "C" {
+
+int hk_ldlt(hk_ctx* c) { return ldlt_impl(c, 0); }
+
+// decompose + invert_L_partial(m) as one call (what compute() runs): the L^-1
+// steps interleaved with the factorisation where that pays (can_overlap_inverse),
+// otherwise the two passes one after the other.  Same results either way.
+int hk_ldlt_invert(hk_ctx* c, int m) {
+    if (!c) return HK_ERR_INVALID;
+    if (c->n >= 1 && (m < 1 || m > c->n)) return fail(c, HK_ERR_INVALID, "invert_L_partial: need 1 <= m <= n");
+    if (c->n >= 1 && can_overlap_inverse(c)) return ldlt_impl(c, m);
+    const int rc = hk_ldlt(c);
+    if (rc != HK_OK) return rc;
+    if (c->rank != 0 && !((c->world > 1 || c->virt || c->nccl_comm) && !sharded_inv_off())) return HK_OK;
+    return hk_invert_L_partial(c, m);
 }
 
 int hk_get_D(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
@@ -1687,13 +1778,12 @@ int compute_tail(hk_ctx* c, int n, int rc, int k, double* lambda_hi, double* lam
                  int* s_out, double t0) {
     const int kk = k < n ? k : n;    // pipeline.cpp:36
     const int s = kk < 3 ? kk : 3;   // pipeline.cpp:64
-    if (rc == HK_OK) rc = hk_ldlt(c);
     // L^-1 and the block are sharded too (every rank takes part); rank 0 then
     // holds the block and runs the eigensolve.  HK_DIST_INV=0: rank 0 alone
     // from the gathered columns.
     const bool root = c->rank == 0;
     const bool all = (c->world > 1 || c->virt || c->nccl_comm) && !sharded_inv_off();
-    if (rc == HK_OK && (root || all)) rc = hk_invert_L_partial(c, kk);
+    if (rc == HK_OK) rc = hk_ldlt_invert(c, kk); // (ranks that take no part in L^-1 stop after the LDLT)
     if (rc == HK_OK && (root || all)) rc = hk_assemble_block(c, kk);
     if (rc == HK_OK && root) rc = hk_smallest_eigs(c, s, lambda_hi, lambda_lo, trunc_err);
     // every rank returns rank 0's record (status, lambdas), so a caller's

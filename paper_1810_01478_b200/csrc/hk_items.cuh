@@ -220,7 +220,9 @@ struct ItemInvStep {
     MpArr S, X;
     int N, L, m, i;
     int panel = 0, rw = 1, rr = 0; // sharded: L(:, i) from the panel S, this rank's rows only
+    const int* err = nullptr;      // steps interleaved with the LDLT: nothing to do once a pivot failed
     HK_DEV void operator()(long long w, uint32_t* ws) const {
+        if (err && *(volatile const int*)err >= 0) return;
         const int b = i < m ? i : m;
         const long long nfma = (long long)(N - i - 1) * b;
         if (w < nfma) {
@@ -532,7 +534,9 @@ struct ItemDStoreL {
 struct CItemInvStep {
     MpArr S, X;
     int N, L, m, i;
+    const int* err = nullptr;
     HK_DEV void operator()(long long w, uint32_t* ws) const {
+        if (err && *(volatile const int*)err >= 0) return;
         const int b = i < m ? i : m;
         const long long nfma = (long long)(N - i - 1) * b;
         if (w < nfma) {

@@ -52,6 +52,64 @@ def test_dataflow_ldlt_same_bits_as_step_graph(api, monkeypatch):
         assert got["0"] == got["1"]
 
 
+@pytest.mark.parametrize("beta,n,L,k,tc", [((1, 1), 70, 160, 8, "1"), ((1, 2), 90, 200, 16, "1"), ((1, 2), 48, 8, 8, "0"),
+                                           ((1, 3), 40, 104, 12, "0"), ((1, 1), 3, 8, 3, "0"), ((1, 2), 1, 4, 1, "0")])
+def test_inverse_steps_interleaved_with_ldlt_same_bits(api, beta, n, L, k, tc, monkeypatch):
+    """hk_ldlt_invert: the L^-1 row-elimination steps riding in the LDLT graph (one GPU, small
+    p) against the two separate passes (HK_INV_OVERLAP=0, and the plain decompose +
+    invert_L_partial calls): pivots, L^-1, block and lambda bit for bit; replays; both stage
+    times reported."""
+    monkeypatch.setenv("HK_TC", tc)
+    monkeypatch.setenv("HK_LDLT_FLOW", "0")  # the graph LDLT (the dataflow kernel has no steps to ride on)
+    mu, _ = api.build_hankel(beta, n, L)
+    kk = min(k, n)
+    got = []
+    for mode in ("overlap", "apart", "calls"):
+        monkeypatch.setenv("HK_INV_OVERLAP", "0" if mode == "apart" else "1")
+        with api.Context(L) as ctx:
+            for rep in range(2):
+                ctx.load_moments(mu)
+                if mode == "calls":
+                    ctx.decompose()
+                    ctx.invert_L_partial(kk)
+                else:
+                    ctx.decompose_invert(kk)
+                ctx.assemble_truncated_inverse(kk)
+                lam = ctx.smallest_eigs_of_H(min(3, kk))
+                cur = (from_arr(ctx.D()), from_arr(ctx.Linv()), from_arr(ctx.block()), repr(lam))  # (trunc_err may hold NaN)
+                t = ctx.timings()
+                assert t[1] > 0 and t[2] >= 0
+                if rep:
+                    assert cur == first
+                first = cur
+            rec = ctx.compute(mu, k)  # compute() goes through the same call
+            assert rec.lambda_hi == list(lam[0])
+        got.append(cur)
+    assert got[0][0] == got[1][0] == got[2][0]
+    # X entries (r, c >= min(r, m)) are zeros in every schedule; all must agree
+    assert got[0][1] == got[1][1] == got[2][1]
+    assert got[0][2] == got[1][2] == got[2][2]
+    assert got[0][3] == got[1][3] == got[2][3]
+
+
+def test_interleaved_inverse_stops_on_a_failed_pivot(api, monkeypatch):
+    monkeypatch.setenv("HK_LDLT_FLOW", "0")
+    n, L = 16, 1
+    mu, _ = api.build_hankel((1, 1), n, L)
+    with api.Context(L) as ctx:
+        ctx.load_moments(mu)
+        with pytest.raises(api.PrecisionError):
+            ctx.decompose_invert(4)
+        col = ctx.bad_column
+        with pytest.raises(ValueError):
+            ctx.Linv()  # not inverted
+        monkeypatch.setenv("HK_INV_OVERLAP", "0")
+        ctx.load_moments(mu)
+        with pytest.raises(api.PrecisionError):
+            ctx.decompose_invert(4)
+        assert ctx.bad_column == col
+
+
 @pytest.mark.parametrize("beta,n,L,k,tc", [((1, 2), 48, 8, 8, "0"), ((1, 1), 40, 192, 8, "1")])
 def test_kernel_timing_nodes_do_not_change_results(api, beta, n, L, k, tc, monkeypatch):
     monkeypatch.setenv("HK_TC", tc)
