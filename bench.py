@@ -39,7 +39,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+# keep stdout to the one JSON line: NCCL's debug text (the version banner already at WARN; INFO if
+# the caller asks for it) goes to stderr
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 # BASELINE.json configs.  K_ref = the reference's K of the golden runs
 # (1024 ceil(N/500) + 1024); K_equiv = (p - bits(mu_{2N-2})) / 2, the fixed-point
@@ -200,7 +202,7 @@ def bench_reference(args, cfg):
         "lambda_min": recs[-1]["lambda"][0] if recs[-1]["lambda"] else None,
         "at_golden_precision": k_ref,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -254,6 +256,12 @@ def bench_ours(args, cfg):
     if world > 1 or args.sharded:  # column-sharded LDLT over NCCL (hk_create_sharded), results on rank 0
         import torch.distributed as dist
 
+        if "RANK" not in os.environ:  # `--sharded` outside torchrun: a world of one
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK=str(local), MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(port))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [api.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -285,11 +293,16 @@ def bench_ours(args, cfg):
         if world == 1 and not args.sharded:
             ctx.decompose_invert(kk)  # as compute() does: L^-1 steps ride in the LDLT graph when latency-bound
         else:
+            # every call is collective on a sharded context: all ranks factor, and (unless
+            # HK_DIST_INV=0 keeps them on rank 0) all ranks take part in L^-1 and the block;
+            # rank 0 holds the block and runs the eigensolve (as compute_tail does)
             ctx.decompose()
-            if rank != 0:
+            if rank != 0 and os.environ.get("HK_DIST_INV") == "0":
                 return [float("nan")], [0.0], [0.0]
             ctx.invert_L_partial(kk)
         ctx.assemble_truncated_inverse(kk)
+        if rank != 0:
+            return [float("nan")], [0.0], [0.0]
         return ctx.smallest_eigs_of_H(s)
 
     for _ in range(args.warmup):
@@ -485,7 +498,7 @@ def bench_ours(args, cfg):
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     ctx.close()
     if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
@@ -499,10 +512,26 @@ def relaunch_distributed(n):
         port = sk.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+    return subprocess.call(cmd, stdout=_OUT)  # the children inherit the real stdout
+
+
+_OUT = None  # the process's real stdout (main() points fd 1 at stderr for everything else)
+
+
+def emit(line):
+    out = _OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    # stdout carries exactly ONE line, the JSON: whatever a library prints there (NCCL's version
+    # banner appears under torchrun even with NCCL_DEBUG unset) is sent to stderr
+    global _OUT
+    if _OUT is None:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
