@@ -212,6 +212,12 @@ struct hk_ctx {
     long long* tc_fb = nullptr;
     int* flow_ready = nullptr;    // dataflow L^-1: per-entry flags + entry counter
     long long flow_cap = 0;
+    // L^-1 tensor-core steps riding in the LDLT graph: their own A operand, redo list and counters
+    uint8_t* inv_A = nullptr;
+    int inv_A_n = 0;
+    long long* inv_fb = nullptr;
+    size_t inv_fb_cap = 0;
+    int* inv_fb_count = nullptr;
     int* lflow = nullptr;         // dataflow LDLT: control words, per-entry flags, per-column counts
     long long lflow_cap = 0;      // entries it was sized for
     // ---- sharded (multi-GPU) state; world == 1 means the single-GPU path
@@ -500,7 +506,7 @@ void tc_products(hk_ctx* c, hk::TcBulkArgs a, hk::MpArr rows, unsigned gx, cudaS
     if (a.dev & 64) a.dev_cnt = c->dev_cnt; // dev: issuer wait-cycle counters (hk_create), printed by hk_destroy
     const char* sl = getenv("HK_TC_SLEEP"); // barrier-poll back-off (ns) of the non-issuing warps
     a.sleep_ns = sl ? atoi(sl) : 0;
-    hk::ItemTcPrep prep{rows, c->tc_A, N, L, a.i, a.mode};
+    hk::ItemTcPrep prep{rows, const_cast<uint8_t*>(a.A), N, L, a.i, a.mode};
     prep.panel = prep_panel;
     const long long nprep = prep.count();
     launch_ex(hk::k_tc_prep, dim3(unsigned((nprep + 255) / 256)), dim3(256), 0, st, pdl, prep, nprep);
@@ -585,12 +591,13 @@ void launch_cols(hk_ctx* c, const F& f, int ncols, int maxrows, int ws_words, cu
 
 // Exact redo of the items the rounding pass could not certify (device-side count).
 template <class F>
-void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset, bool pdl = false) {
+void launch_fix(hk_ctx* c, const F& f, cudaStream_t st, int* count, int* reset, bool pdl = false,
+                const long long* fb = nullptr) {
     const int wo = ws_op_words(c->L);
     const int wpb = std::max(1, std::min(8, int((96 * 1024) / (wo * 4))));
     func_smem((const void*)hk::k_tc_fix<F>, 200 * 1024);
     launch_ex(hk::k_tc_fix<F>, dim3(unsigned(c->sm_count)), dim3(unsigned(32 * wpb)), size_t(wo) * 4 * wpb, st, pdl, f,
-              (const int*)count, (const long long*)c->tc_fb, wo, reset, c->fix_total);
+              (const int*)count, fb ? fb : (const long long*)c->tc_fb, wo, reset, c->fix_total);
     ck(cudaGetLastError(), "tc fix launch");
     ++c->launches;
 }
@@ -666,6 +673,11 @@ struct InvTarget {
     int rw = 1, rr = 0;         // row blocks of this rank (hk::row_mine)
     const int* otiles = nullptr; // device list of this rank's row tiles with rows > i (tc path)
     int ntiles = -1;
+    // steps riding in the LDLT graph: buffers of their own (the LDLT's are in use) and the error gate
+    uint8_t* A = nullptr;
+    int* fb_count = nullptr;
+    long long* fb = nullptr;
+    const int* err = nullptr;
 };
 
 // L^-1 step i on the tensor cores (same product kernel, mode 1).
@@ -687,16 +699,20 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false, const I
     G = std::min(G, std::min(int(hk::kTcMaxGroups), hk::tc_nchunks(L) / 2));
     if (G < 1) G = 1;
     if (b > 0 && tiles > 0) {
-        hk::TcBulkArgs a{hk::MpArr{}, tg->X, c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err};
+        hk::TcBulkArgs a{hk::MpArr{}, tg->X, tg->A ? tg->A : c->tc_A, c->tc_P, N, L, i, i + 1, 1, m, b, c->d_err};
         a.groups = G;
         a.gcarry = c->tc_gcarry;
         a.otiles = tg->otiles;
+        a.inv_gate = tg->err ? 1 : 0;
         tc_products(c, a, tg->Lsrc, unsigned(b), st, pdl, tg->ntiles, tg->panel);
     }
-    int* cnt = c->tc_fb_count + (i & 1);
-    int* nxt = c->tc_fb_count + ((i + 1) & 1);
+    int* fbc = tg->fb_count ? tg->fb_count : c->tc_fb_count;
+    long long* fbl = tg->fb ? tg->fb : c->tc_fb;
+    int* cnt = fbc + (i & 1);
+    int* nxt = fbc + ((i + 1) & 1);
     const long long items = (long long)(N - i - 1) * b + (i < m ? N - i - 1 : 0);
-    hk::ItemTcRoundInv ri{tg->Lsrc, tg->X, c->tc_P, N, L, m, i, b, cnt, c->tc_fb};
+    hk::ItemTcRoundInv ri{tg->Lsrc, tg->X, c->tc_P, N, L, m, i, b, cnt, fbl};
+    ri.err = tg->err;
     ri.G = G;
     ri.gcarry = c->tc_gcarry;
     ri.force_fb = force_fix();
@@ -707,7 +723,7 @@ void enqueue_inv_tc(hk_ctx* c, int i, cudaStream_t st, bool pdl = false, const I
     if (b > 0) {
         hk::FixInv fx{tg->Lsrc, tg->X, N, L, m, i, b};
         fx.panel = tg->panel;
-        launch_fix(c, fx, st, cnt, nxt, pdl);
+        launch_fix(c, fx, st, cnt, nxt, pdl, fbl);
     } else {
         ck(cudaMemsetAsync(nxt, 0, sizeof(int), st), "memset fb");
     }
@@ -1122,6 +1138,31 @@ void ensure_tc_scratch(hk_ctx* c, int m = 0) {
     ensure_tc_items(c, p_items, std::max(tri, nm + c->n));
 }
 
+// Buffers of the tensor-core L^-1 steps when they ride in the LDLT graph: the
+// LDLT's A operand, redo list and counters are in use at the same time
+void ensure_inv_overlap(hk_ctx* c, int m) {
+    const size_t nm = (size_t)c->n * m;
+    ensure_tc_items(c, nm, std::max((size_t)c->n * (c->n + 1) / 2, nm + c->n)); // product scratch + group carries (L^-1 only)
+    if (c->inv_A_n < c->n) {
+        if (c->inv_A) cudaFree(c->inv_A);
+        c->inv_A = nullptr;
+        c->inv_A_n = 0;
+        ck(cudaMalloc(&c->inv_A, hk::tc_apre_bytes(c->n, c->L)), "cudaMalloc inv A");
+        c->inv_A_n = c->n;
+    }
+    if (!c->inv_fb_count) {
+        ck(cudaMalloc(&c->inv_fb_count, 2 * sizeof(int)), "cudaMalloc inv fb count");
+        ck(cudaMemset(c->inv_fb_count, 0, 2 * sizeof(int)), "memset inv fb count");
+    }
+    if (nm + c->n > c->inv_fb_cap) {
+        if (c->inv_fb) cudaFree(c->inv_fb);
+        c->inv_fb = nullptr;
+        c->inv_fb_cap = 0;
+        ck(cudaMalloc(&c->inv_fb, (nm + c->n) * sizeof(long long)), "cudaMalloc inv fb list");
+        c->inv_fb_cap = nm + c->n;
+    }
+}
+
 // One L^-1 step of the N-step schedule (small p): few items a CTA per FMA, many a warp per FMA
 void enqueue_inv_step(hk_ctx* c, int i, int m, cudaStream_t st, const int* err = nullptr) {
     const int N = c->n, L = c->L;
@@ -1162,11 +1203,22 @@ void enqueue_ldlt_steps(hk_ctx* c, int inv_m = 0) {
     ck(cudaStreamWaitEvent(la, c->evFork, 0), "fork wait");
     ck(cudaStreamWaitEvent(side, c->evFork, 0), "fork wait side");
     cudaStream_t inv = c->st5;
+    const bool inv_tc = inv_m > 0 && use_tc_inv(c);
+    InvTarget itg;
     if (inv_m > 0) {
         ck(cudaStreamWaitEvent(inv, c->evFork, 0), "fork wait inv");
         hk::ItemInvInit ii{c->S.view(), c->X.view(), N, L, inv_m};
         ii.zero = 1; // column c of X is set at step c, before any use
         launch(c, ii, (long long)N * inv_m, 64, inv);
+        if (inv_tc) {
+            ck(cudaMemsetAsync(c->inv_fb_count, 0, 2 * sizeof(int), inv), "memset inv fb counters");
+            itg.Lsrc = c->S.view();
+            itg.X = c->X.view();
+            itg.A = c->inv_A;
+            itg.fb_count = c->inv_fb_count;
+            itg.fb = c->inv_fb;
+            itg.err = c->d_err;
+        }
     }
     const int wc = ws_cta_words(L), wcr = ws_cta_recip_words(L);
     (void)wr;
@@ -1193,7 +1245,10 @@ void enqueue_ldlt_steps(hk_ctx* c, int inv_m = 0) {
             ck(cudaEventRecord(evR[i - 1], side), "evR");
             if (inv_m > 0 && i - 1 < N - 1) { // L^-1 step i-1: column i-1 of L is in place
                 ck(cudaStreamWaitEvent(inv, evR[i - 1], 0), "wait R inv");
-                enqueue_inv_step(c, i - 1, inv_m, inv, c->d_err);
+                if (inv_tc)
+                    enqueue_inv_tc(c, i - 1, inv, pdl, &itg);
+                else
+                    enqueue_inv_step(c, i - 1, inv_m, inv, c->d_err);
             }
         }
         if (i + 1 < N) {
@@ -1395,6 +1450,9 @@ void hk_destroy(hk_ctx* c) {
     if (c->tc_gcarry) cudaFree(c->tc_gcarry);
     if (c->flow_ready) cudaFree(c->flow_ready);
     if (c->lflow) cudaFree(c->lflow);
+    if (c->inv_A) cudaFree(c->inv_A);
+    if (c->inv_fb) cudaFree(c->inv_fb);
+    if (c->inv_fb_count) cudaFree(c->inv_fb_count);
     for (auto e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : c->evP) cudaEventDestroy(e);
@@ -1499,14 +1557,21 @@ int hk_get_moments(hk_ctx* c, uint32_t* limbs, int32_t* exps, int32_t* signs) {
 } // extern "C"
 
 namespace {
+constexpr bool kInvOverlapTc = true; // default of HK_INV_OVERLAP_TC (C3 496 -> 448 ms, C4 4.65 -> 4.23 s)
+
 // The L^-1 steps can ride in the LDLT graph (hk_ldlt_invert) when both run the
 // N-step schedules on one GPU and L^-1 is latency-bound (small p, IMAD steps).
 // HK_INV_OVERLAP=0 keeps the two passes apart.
 bool can_overlap_inverse(const hk_ctx* c) {
     if (c->world > 1 || c->virt || c->nccl_comm) return false;
-    if (use_ldlt_flow(c) || use_tc_inv(c)) return false;
+    if (use_ldlt_flow(c)) return false;
     const char* e = getenv("HK_INV_OVERLAP");
-    return !e || e[0] != '0';
+    if (e && e[0] == '0') return false;
+    if (use_tc_inv(c)) { // tensor-core steps: they need the product scratch the unfused LDLT uses
+        const char* t = getenv("HK_INV_OVERLAP_TC");
+        return use_fuse(c) && (t ? t[0] == '1' : kInvOverlapTc);
+    }
+    return true;
 }
 
 // hk_ldlt (inv_m == 0) / the overlapped part of hk_ldlt_invert (inv_m > 0)
@@ -1515,7 +1580,10 @@ int ldlt_impl(hk_ctx* c, int inv_m) {
         if (c->n < 1) return fail(c, HK_ERR_INVALID, "hk_ldlt: no moments loaded");
         if (c->world > 1 || c->virt || c->nccl_comm) return dist_ldlt(c);
         const int N = c->n, L = c->L;
-        if (inv_m > 0) c->X.ensure((long long)N * inv_m, L);
+        if (inv_m > 0) {
+            c->X.ensure((long long)N * inv_m, L);
+            c->m = inv_m; // (the tensor-core step enqueue reads it)
+        }
         const long long ntri = (long long)N * (N + 1) / 2;
         c->S.ensure(ntri, L);
         c->R.ensure(N, L);
@@ -1540,6 +1608,7 @@ int ldlt_impl(hk_ctx* c, int inv_m) {
         }
         c->B.ensure(3LL * N, L);
         ensure_tc_scratch(c);
+        if (inv_m > 0 && use_tc_inv(c)) ensure_inv_overlap(c, inv_m);
         ensure_step_events(c, N);
         ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(int), c->st), "memset err");
         ck(cudaEventRecord(c->ev[0], c->st), "event");
@@ -1550,7 +1619,7 @@ int ldlt_impl(hk_ctx* c, int inv_m) {
                                            use_fuse(c) ? nullptr : (const void*)c->tc_P, c->tc_A, c->tc_fb,
                                            c->tc_fb_count, (const void*)(long long)use_tc(c),
                                            (const void*)(long long)use_fuse(c), (const void*)(long long)c->kprof,
-                                           c->X.d, c->X.m};
+                                           c->X.d, c->X.m, c->inv_A, c->inv_fb, c->inv_fb_count, c->tc_P, c->tc_gcarry};
         if (sig != c->graph_sig) {
             for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
             c->graphs.clear();
@@ -1832,6 +1901,9 @@ int hk_set_limbs(hk_ctx* c, int limbs) {
         }
         for (void* p : {(void*)c->tc_P, (void*)c->tc_A, (void*)c->tc_fb, (void*)c->tc_gcarry})
             if (p) cudaFree(p);
+        if (c->inv_A) cudaFree(c->inv_A);
+        c->inv_A = nullptr;
+        c->inv_A_n = 0;
         c->tc_P = nullptr;
         c->tc_A = nullptr;
         c->tc_fb = nullptr;

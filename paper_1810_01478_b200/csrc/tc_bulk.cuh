@@ -178,6 +178,7 @@ struct TcBulkArgs {
     int sleep_ns = 0;           // back-off of the epilogue / window-builder barrier polls
     int stages = 0;             // ring depth override (dev sweeps; 0 = default for the mode)
     const int* otiles = nullptr; // mode 1, sharded L^-1: this rank's row tiles (blockIdx.y -> otiles[y])
+    int inv_gate = 0;            // mode 1 riding in the LDLT graph: stop once the LDLT raised a precision error
     unsigned long long* dev_cnt = nullptr; // dev (bit 64): issuer cycles waiting on empty / full / efull / accE, total
 };
 
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_bulk(TcBulkArgs a) {
     extern __shared__ __align__(1024) uint8_t tsm[];
     __shared__ uint64_t full[kTcStages], empty[kTcStages], efull[kTcStages], accF[2], accE[2];
     __shared__ uint32_t taddr_s;
-    if (a.mode != 1 && !(a.dev & 256) && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
+    if ((a.mode != 1 || a.inv_gate) && !(a.dev & 256) && *(volatile const int*)a.err >= 0) return; // LDLT precision error raised
     const int N = a.N, L = a.L, nb = tc_nb(L);
     const int locj = a.first_loc + int(blockIdx.x);
     const int j = a.mode == 0 ? a.jfirst + int(blockIdx.x) : a.mode == 2 ? a.owned[locj] : a.i + 1; // first valid row
@@ -778,7 +779,9 @@ struct ItemTcRoundInv {
     int G = 1;                       // chunk groups of the product kernel
     const uint64_t* gcarry = nullptr; // their carries, added here
     int panel = 0, rw = 1, rr = 0;   // sharded: L(:, i) from the panel S, this rank's rows only
+    const int* err = nullptr;        // steps riding in the LDLT graph: nothing to do once a pivot failed
     HK_DEV void operator()(long long w, uint32_t* ws) const {
+        if (err && *(volatile const int*)err >= 0) return;
         const long long nfma = (long long)(N - i - 1) * b;
         if (w >= nfma) {
             const int j = i + 1 + int(w - nfma);

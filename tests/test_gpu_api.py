@@ -92,6 +92,30 @@ def test_inverse_steps_interleaved_with_ldlt_same_bits(api, beta, n, L, k, tc, m
     assert got[0][3] == got[1][3] == got[2][3]
 
 
+@pytest.mark.parametrize("beta,n,L,k", [((1, 1), 150, 192, 8), ((1, 3), 96, 1152, 12), ((1, 2), 300, 392, 16)])
+def test_tensor_core_inverse_steps_in_ldlt_graph_with_forced_redo(api, beta, n, L, k, monkeypatch):
+    """The tensor-core L^-1 steps riding in the (fused, tensor-core) LDLT graph keep their own A
+    operand, redo list and counters: with every 7th item of both stages forced to the exact
+    redo (HK_TC_FORCE_FIX) the two lists are in use at the same time, and the bits must equal
+    the two separate passes'."""
+    monkeypatch.setenv("HK_TC", "1")
+    monkeypatch.setenv("HK_LDLT_FLOW", "0")
+    mu, _ = api.build_hankel(beta, n, L)
+    got = {}
+    for force in ("0", "1"):
+        for overlap in ("1", "0"):
+            monkeypatch.setenv("HK_TC_FORCE_FIX", force)
+            monkeypatch.setenv("HK_INV_OVERLAP", overlap)
+            with api.Context(L) as ctx:
+                rec, D, M = run(ctx, mu, k)
+                X = from_arr(ctx.Linv())
+                rec2, D2, M2 = run(ctx, mu, k)
+                assert D2 == D and M2 == M and from_arr(ctx.Linv()) == X
+                assert ctx.fused_violations() == 0
+            got[(force, overlap)] = (rec.lambda_hi, rec.lambda_lo, D, X, M)
+    assert got[("0", "1")] == got[("0", "0")] == got[("1", "1")] == got[("1", "0")]
+
+
 def test_interleaved_inverse_stops_on_a_failed_pivot(api, monkeypatch):
     monkeypatch.setenv("HK_LDLT_FLOW", "0")
     n, L = 16, 1
