@@ -116,6 +116,29 @@ def test_tensor_core_inverse_steps_in_ldlt_graph_with_forced_redo(api, beta, n, 
     assert got[("0", "1")] == got[("0", "0")] == got[("1", "1")] == got[("1", "0")]
 
 
+@pytest.mark.parametrize("beta,n,L,tc", [((1, 1), 60, 136, "1"), ((1, 2), 50, 16, "0")])
+def test_one_context_many_k_and_n(api, beta, n, L, tc, monkeypatch):
+    """One context, compute() with changing k and n (the cached graphs are keyed by (n, m); the
+    buffers of the interleaved L^-1 steps grow): every result equals a fresh context's."""
+    monkeypatch.setenv("HK_TC", tc)
+    monkeypatch.setenv("HK_LDLT_FLOW", "0")
+    cases = [(n, 4), (n, 9), (n - 7, 9), (n, 4), (n + 5, 12), (n, 9)]
+
+    def result(ctx, mu, k):
+        rec, D, M = run(ctx, mu, k)
+        return repr((rec.lambda_hi, rec.lambda_lo, rec.trunc_err)), D, M, from_arr(ctx.Linv())
+
+    want = {}
+    for nn, k in set(cases):
+        mu, _ = api.build_hankel(beta, nn, L)
+        with api.Context(L) as ctx:
+            want[(nn, k)] = result(ctx, mu, k)
+    with api.Context(L) as ctx:
+        for nn, k in cases:
+            mu, _ = api.build_hankel(beta, nn, L)
+            assert result(ctx, mu, k) == want[(nn, k)], (nn, k)
+
+
 def test_interleaved_inverse_stops_on_a_failed_pivot(api, monkeypatch):
     monkeypatch.setenv("HK_LDLT_FLOW", "0")
     n, L = 16, 1
